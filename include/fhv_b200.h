@@ -1,0 +1,209 @@
+/*
+ * fhv_b200.h -- C ABI of the B200-native fragment-history-volume hot path.
+ *
+ * One shared library (paper_2211_15460_b200/libfhv_b200.so, sm_100a).  Plain
+ * pointers and sizes only; every buffer is allocated by the caller (PyTorch)
+ * unless stated, the library never frees caller memory.  All calls are
+ * enqueued on `stream` (a cudaStream_t); calls that must return a
+ * data-dependent size to the host (fragment totals) synchronise that stream.
+ * Return value: an FHV_* status code.
+ *
+ * Which reference interface each entry point replaces (
+ * `fhv/X.py:N` = /root/reference/pkg/src/fhv/X.py line N):
+ *
+ *   reference operator API          fhv/_backend.py:25-29  kernels() -> module with
+ *     coverage(...)                 fhv/_ckern.pyx:25-105   per triangle
+ *     linked_insert(...)            fhv/_ckern.pyx:112-123  per batch
+ *     pofa_scatter(...)             fhv/_ckern.pyx:126-143  per batch
+ *     raycast_image(...)            fhv/_ckern.pyx:653-743  per image span
+ *
+ * The three per-triangle / per-batch kernels are only ever called from the
+ * capture drivers, and a per-triangle launch is meaningless on a GPU, so the
+ * boundary moves one level up to the drivers that call them:
+ *   fhv_build_ppfl    <- build_ppfl        fhv/storage.py:553-571 (capture_pass + PpflSink + linked_insert)
+ *   fhv_build_pofl    <- build_pofl        fhv/storage.py:574-587 (capture_pass + PoflSink + linked_insert + set_paths)
+ *   fhv_pofa_count    <- pofa_build pass 1 fhv/storage.py:602-608 (CountingSink, cumsum, total check)
+ *   fhv_pofa_scatter  <- pofa_build pass 2 fhv/storage.py:610-620 (PofaWriteSink + pofa_scatter + checks + pyramid)
+ *   fhv_capture_list  <- capture_pass + ListSink  fhv/raster.py:350-388, 309-320
+ *   fhv_splat         <- splat_render      fhv/render.py:249-320
+ *   fhv_raycast       <- render_raycast    fhv/raycast.py:469-577 (rays generated on device)
+ *   fhv_raycast_image <- raycast_image     fhv/_ckern.pyx:653-743 (1:1: caller-provided rays, pixel span)
+ */
+#ifndef FHV_B200_H
+#define FHV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python layer maps them to the reference's exceptions */
+enum {
+  FHV_OK = 0,
+  FHV_OVERFLOW = 1,       /* pool overflow: records past capacity dropped (FragmentPool.overflowed) */
+  FHV_PASS_MISMATCH = 2,  /* PofaBuildError (fhv/storage.py:73-74, 431-433, 614-619) */
+  FHV_BAD_ARGS = 3,       /* ValueError / FhvError on arguments */
+  FHV_CUDA_ERROR = 4,     /* a CUDA runtime call failed */
+  FHV_RANGE = 5,          /* FhvError: fragment position outside [0,1]^3 (fhv/storage.py:152-155) */
+  FHV_BASIS = 6,          /* ValueError from tangent_basis (fhv/raster.py:154-157) */
+  FHV_NOMEM = 7,          /* MemoryError */
+  FHV_TOO_MANY = 8,       /* FhvError: >= 2^32 fragments (fhv/storage.py:604-606) */
+  FHV_SPLAT_BIG = 9,      /* SceneError: splat footprint > 4096 px (fhv/render.py:285-286) */
+};
+
+/* capture flags */
+enum {
+  FHV_ALLOC_ATOMIC = 1,  /* paper-style slots from a warp-aggregated atomic counter (nondeterministic pool order) */
+  FHV_EXACT_ORDER = 2,   /* chains (PPFL/POFL) / in-leaf order (POFA) identical to the sequential reference */
+};
+
+/* splat flags */
+enum {
+  FHV_SPLAT_PACKED = 1,  /* one 64-bit atomicMin on (f32 depth | u32 index); default is the exact f64 two-pass z-test */
+};
+
+typedef struct fhv_ctx fhv_ctx; /* per-device scratch arena (grow-only); one per host thread / stream */
+
+/* triangle soup, device pointers (Scene arrays, fhv/scene.py:105-126) */
+typedef struct {
+  int64_t n_tri;
+  const double *pos;  /* [T][3][3] vertex positions */
+  const double *vnrm; /* [T][3][3] vertex normals   */
+  const double *fnrm; /* [T][3]    face normals     */
+  const uint32_t *mat;
+  const uint32_t *obj;
+} fhv_tris_t;
+
+/* resolved capture strategy (paper_2211_15460_b200/raster.py CapturePlan) */
+typedef struct {
+  int32_t strategy; /* 0 one_view, 1 three_separate, 2 three_way_geometry, 3 normal_space */
+  int32_t res;      /* square capture grid edge, fhv/raster.py:359 */
+  double pitch;     /* normal_space sample spacing, fhv/raster.py:381 */
+  double proj[3][16]; /* row-major world->clip per capture axis */
+} fhv_capture_cfg_t;
+
+/* FragmentPool (fhv/storage.py:188-248), struct-of-arrays, device pointers */
+typedef struct {
+  int64_t capacity;
+  float *pos;     /* [cap][3] */
+  float *nrm;     /* [cap][3] */
+  uint32_t *mat;
+  uint32_t *obj;
+  int32_t *prev;  /* prev_index */
+} fhv_pool_t;
+
+/* materials + lights, device pointers (fhv/render.py:106-113, fhv/raycast.py:460-466) */
+typedef struct {
+  int32_t n_lights;
+  const uint8_t *light_kind;   /* 0 directional, 1 point */
+  const double *light_vec;     /* [K][3] direction (unit) or position */
+  const double *light_color;   /* [K][3] */
+  const double *light_ambient; /* [K][3] */
+  int32_t n_mats;
+  const double *diffuse;   /* [M][3] */
+  const double *specular;  /* [M][3] */
+  const double *shininess; /* [M] */
+  const double *alpha;     /* [M] */
+} fhv_shading_t;
+
+/* camera packed by Camera.scalars(): [persp, eye3, r3, u3, f3, w, h, half_w,
+   half_h, tan(fov/2), aspect, near, far, extent] (host memory, 22 doubles) */
+#define FHV_CAM_SCALARS 22
+
+/* read-only per-octant volume for ray casting (FhvPofa / FhvPofl) */
+typedef struct {
+  int32_t layout; /* 0 POFA (offsets, counts), 1 POFL (heads, prev) */
+  int32_t levels;
+  const uint32_t *offsets;
+  const uint32_t *counts;
+  const int32_t *heads;
+  const int32_t *prev;
+  const uint8_t *pyramid; /* levels 0..L-1 concatenated */
+  const float *pos;
+  const float *nrm;
+  const uint32_t *mat;
+  const uint32_t *obj;
+} fhv_volume_t;
+
+/* optional per-pixel id buffer of splat_render (GBuffer, fhv/render.py:87-103) */
+typedef struct {
+  double *position; /* [P][3] or NULL */
+  double *normal;   /* [P][3] or NULL */
+  int32_t *material_id;
+  int32_t *object_id;
+  uint8_t *valid;
+} fhv_gbuffer_t;
+
+const char *fhv_version(void);
+fhv_ctx *fhv_ctx_create(void);
+void fhv_ctx_destroy(fhv_ctx *ctx);
+/* kernels launched by this context since creation (for launch accounting) */
+int64_t fhv_ctx_launches(const fhv_ctx *ctx);
+
+/* Every fragment in reference emission order (job, y, x), f64 attributes.
+   max_out bounds the outputs; *n_out receives the total.  Synchronises. */
+int fhv_capture_list(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg,
+                     int64_t max_out, int64_t *job, int32_t *px, int32_t *py, double *wpos,
+                     double *wnrm, int64_t *n_out, void *stream);
+
+/* build_ppfl: heads[W*H] and pool->prev must be pre-filled with -1 by the
+   caller; width = PixelDirectory.width.  *next_free = fragments emitted
+   (FragmentPool.next_free).  Synchronises.  Returns FHV_OVERFLOW if
+   next_free > capacity. */
+int fhv_build_ppfl(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int64_t width,
+                   fhv_pool_t *pool, int32_t *heads, int32_t flags, int64_t *next_free, void *stream);
+
+/* build_pofl: heads[8^L] pre-filled with -1; pyramid (sum 8^k bytes) is
+   written.  Synchronises. */
+int fhv_build_pofl(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int32_t levels,
+                   fhv_pool_t *pool, int32_t *heads, uint8_t *pyramid, int32_t flags,
+                   int64_t *next_free, void *stream);
+
+/* pofa_build pass 1: counts[8^L] per-leaf fragment counts, offsets = their
+   exclusive prefix sum, pyramid from counts > 0, *total = pool size.  The
+   rasterised job table stays in ctx for fhv_pofa_scatter.  Synchronises. */
+int fhv_pofa_count(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int32_t levels,
+                   uint32_t *counts, uint32_t *offsets, uint8_t *pyramid, int64_t *total,
+                   void *stream);
+
+/* pofa_build pass 2: scatter every fragment into its leaf's range
+   [offsets[c], offsets[c]+counts[c]); prev_index = -1.  Verifies cursors ==
+   counts (FHV_PASS_MISMATCH otherwise).  Must follow fhv_pofa_count on the
+   same ctx with the same inputs.  Synchronises. */
+int fhv_pofa_scatter(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg,
+                     int32_t levels, const uint32_t *counts, const uint32_t *offsets, fhv_pool_t *pool,
+                     int32_t flags, void *stream);
+
+/* splat_render over pool[0:n): out_rgba [H][W][4] f64, out_depth [H][W] f64,
+   out_winner [H][W] int32 (pool index or -1, may be NULL), gbuffer may be
+   NULL.  Synchronises (footprint check). */
+int fhv_splat(fhv_ctx *ctx, int64_t n, const float *pos, const float *nrm, const uint32_t *mat,
+              const uint32_t *obj, const double *cam, double radius, const double *background,
+              const fhv_shading_t *shading, double *out_rgba, double *out_depth, int32_t *out_winner,
+              const fhv_gbuffer_t *gbuffer, int32_t flags, void *stream);
+
+/* render_raycast for rows [row0, row1) of the camera image: out_rgba
+   [H][W][4] f64, out_ids [H][W] int32 (first-hit object id, NULL to skip),
+   counters int64[4] on DEVICE (+= visited, tested, hits, early).  Async. */
+int fhv_raycast(fhv_ctx *ctx, const fhv_volume_t *vol, const fhv_shading_t *shading, const double *cam,
+                const double *background, double radius, double cutoff, int32_t mode, double shadow_eps,
+                int64_t row0, int64_t row1, double *out_rgba, int32_t *out_ids, int64_t *counters,
+                void *stream);
+
+/* raycast_image 1:1 (fhv/_ckern.pyx:653-743): rays from caller arrays
+   origins/dirs [P][3] f64 (device), pixels [start, end).  Async. */
+int fhv_raycast_image(fhv_ctx *ctx, int64_t start, int64_t end, const double *origins,
+                      const double *dirs, const fhv_volume_t *vol, const fhv_shading_t *shading,
+                      const double *eye, const double *background, double radius, double cutoff,
+                      int32_t mode, double shadow_eps, double *out_rgba, int32_t *out_ids,
+                      int64_t *counters, void *stream);
+
+/* make_triangle face normals for a bulk scene (fhv/scene.py:137-139). Async. */
+int fhv_face_normals(fhv_ctx *ctx, int64_t n_tri, const double *pos, double *fnrm, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FHV_B200_H */

@@ -1,0 +1,155 @@
+"""ctypes binding of libfhv_b200.so (the C ABI declared in include/fhv_b200.h).
+
+There is no CPU fallback: if the extension is missing or no CUDA device is
+present, every entry point raises.  Build with ``python -c "import
+__graft_entry__ as g; g.build()"`` (or ``python -m paper_2211_15460_b200.build``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfhv_b200.so")
+
+c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+
+FHV_OK, FHV_OVERFLOW, FHV_PASS_MISMATCH, FHV_BAD_ARGS, FHV_CUDA_ERROR = 0, 1, 2, 3, 4
+FHV_RANGE, FHV_BASIS, FHV_NOMEM, FHV_TOO_MANY, FHV_SPLAT_BIG = 5, 6, 7, 8, 9
+FHV_ALLOC_ATOMIC, FHV_EXACT_ORDER = 1, 2
+FHV_SPLAT_PACKED = 1
+
+
+class Tris(ctypes.Structure):
+    _fields_ = [("n_tri", c_i64), ("pos", c_vp), ("vnrm", c_vp), ("fnrm", c_vp), ("mat", c_vp), ("obj", c_vp)]
+
+
+class CaptureCfg(ctypes.Structure):
+    _fields_ = [("strategy", c_i32), ("res", c_i32), ("pitch", c_f64), ("proj", c_f64 * 48)]
+
+
+class Pool(ctypes.Structure):
+    _fields_ = [("capacity", c_i64), ("pos", c_vp), ("nrm", c_vp), ("mat", c_vp), ("obj", c_vp), ("prev", c_vp)]
+
+
+class Shading(ctypes.Structure):
+    _fields_ = [("n_lights", c_i32), ("light_kind", c_vp), ("light_vec", c_vp), ("light_color", c_vp),
+                ("light_ambient", c_vp), ("n_mats", c_i32), ("diffuse", c_vp), ("specular", c_vp),
+                ("shininess", c_vp), ("alpha", c_vp)]
+
+
+class Volume(ctypes.Structure):
+    _fields_ = [("layout", c_i32), ("levels", c_i32), ("offsets", c_vp), ("counts", c_vp), ("heads", c_vp),
+                ("prev", c_vp), ("pyramid", c_vp), ("pos", c_vp), ("nrm", c_vp), ("mat", c_vp), ("obj", c_vp)]
+
+
+class GBuf(ctypes.Structure):
+    _fields_ = [("position", c_vp), ("normal", c_vp), ("material_id", c_vp), ("object_id", c_vp), ("valid", c_vp)]
+
+
+_P = ctypes.POINTER
+_SIGS = {
+    "fhv_version": (ctypes.c_char_p, []),
+    "fhv_ctx_create": (c_vp, []),
+    "fhv_ctx_destroy": (None, [c_vp]),
+    "fhv_ctx_launches": (c_i64, [c_vp]),
+    "fhv_capture_list": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                        _P(c_i64), c_vp]),
+    "fhv_build_ppfl": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i64, _P(Pool), c_vp, c_i32, _P(c_i64),
+                                      c_vp]),
+    "fhv_build_pofl": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, _P(Pool), c_vp, c_vp, c_i32,
+                                      _P(c_i64), c_vp]),
+    "fhv_pofa_count": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, c_vp, c_vp, c_vp, _P(c_i64), c_vp]),
+    "fhv_pofa_scatter": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, c_vp, c_vp, _P(Pool), c_i32,
+                                        c_vp]),
+    "fhv_splat": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_f64, c_vp, _P(Shading), c_vp, c_vp,
+                                 c_vp, _P(GBuf), c_i32, c_vp]),
+    "fhv_raycast": (ctypes.c_int, [c_vp, _P(Volume), _P(Shading), c_vp, c_vp, c_f64, c_f64, c_i32, c_f64, c_i64,
+                                   c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "fhv_raycast_image": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, _P(Volume), _P(Shading), c_vp, c_vp,
+                                         c_f64, c_f64, c_i32, c_f64, c_vp, c_vp, c_vp, c_vp]),
+    "fhv_face_normals": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp]),
+}
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+_ctxs: dict = {}
+_lock = threading.Lock()
+
+
+class ExtensionMissing(RuntimeError):
+    pass
+
+
+def load(require_cuda: bool = True):
+    """Load the shared library (idempotent).  Raises if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ExtensionMissing(f"{LIB_PATH} not built; run __graft_entry__.build()")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    if require_cuda and not torch.cuda.is_available():
+        raise RuntimeError("fhv_b200 needs a CUDA device (B200); there is no CPU fallback")
+    return _lib
+
+
+def ctx(device: torch.device):
+    """Per-device scratch context (created on first use)."""
+    lib = load()
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    with _lock:
+        c = _ctxs.get(idx)
+        if c is None:
+            with torch.cuda.device(idx):
+                c = lib.fhv_ctx_create()
+            if not c:
+                raise MemoryError("fhv_ctx_create failed")
+            _ctxs[idx] = c
+    return c
+
+
+def launches(device: torch.device) -> int:
+    return int(load().fhv_ctx_launches(ctx(device)))
+
+
+def stream_ptr(device: torch.device):
+    return c_vp(torch.cuda.current_stream(device).cuda_stream)
+
+
+def ptr(t):
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return c_vp(t.data_ptr()) if t.numel() else None
+
+
+def check(rc: int, what: str, allow=(FHV_OK,)):
+    """Map an FHV_* status to the reference's exception types."""
+    if rc in allow:
+        return rc
+    from .scene import SceneError
+    from .storage import FhvError, PofaBuildError
+    msg = f"{what}: status {rc}"
+    if rc == FHV_PASS_MISMATCH:
+        raise PofaBuildError(f"{what}: per-octant cursors do not match counted sizes")
+    if rc == FHV_RANGE:
+        raise FhvError(f"{what}: position outside [0,1]^3")
+    if rc == FHV_BASIS:
+        raise ValueError(f"{what}: tangent_basis received a non-unit normal")
+    if rc == FHV_TOO_MANY:
+        raise FhvError(f"{what}: fragment count exceeds 32-bit directory range")
+    if rc == FHV_SPLAT_BIG:
+        raise SceneError("splat footprint too large; reduce the radius")
+    if rc == FHV_NOMEM:
+        raise MemoryError(msg)
+    if rc == FHV_BAD_ARGS:
+        raise FhvError(f"{what}: invalid arguments")
+    raise RuntimeError(msg)

@@ -1,0 +1,54 @@
+"""Build libfhv_b200.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+    python -m paper_2211_15460_b200.build [--force]
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SOURCES = ["fhv_abi.cu", "fhv_scan.cu", "fhv_capture.cu", "fhv_splat.cu", "fhv_raycast.cu"]
+HEADERS = ["fhv_common.cuh", "fhv_internal.h"]
+OUT = os.path.join(HERE, "libfhv_b200.so")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    # exactness: never contract mul+add; explicit __fma_rn where numpy/BLAS fuse
+    "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
+    "-shared", "--expt-relaxed-constexpr", "-diag-suppress", "177,549",
+]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.sep not in cand or os.path.exists(cand)):
+            return cand
+    return "nvcc"
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(OUT):
+        return False
+    t = os.path.getmtime(OUT)
+    deps = [os.path.join(HERE, "csrc", f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "fhv_b200.h")]
+    return all(os.path.getmtime(d) <= t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return OUT
+    cmd = [_nvcc(), *NVCC_FLAGS, "-o", OUT] + [os.path.join(HERE, "csrc", f) for f in SOURCES]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True, cwd=HERE)
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(OUT)

@@ -1,0 +1,71 @@
+// fhv_internal.h -- host-side plumbing shared by the .cu translation units:
+// the per-device scratch arena (fhv_ctx) and kernel-launch helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fhv_b200.h"
+
+namespace fhv {
+
+// small device-resident control block (one per ctx)
+struct Control {
+  int status;                     // sticky FHV_* code raised by kernels
+  int pad;
+  unsigned long long items_total; // work items of the current capture
+  unsigned long long frags_total; // fragments counted by pass 1
+  unsigned long long alloc;       // FHV_ALLOC_ATOMIC slot counter / pass-2 emitted
+  unsigned long long kx, ky;      // splat footprint maxima
+  unsigned long long scan_total;  // last scan total
+  unsigned int tile_counter;      // decoupled look-back tile ticket
+  unsigned int pad2;
+  unsigned long long spare[8];
+};
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace fhv
+
+struct fhv_ctx {
+  int device = 0;
+  fhv::DevBuf bufs[24];
+  fhv::Control* ctl = nullptr;       // device
+  fhv::Control* ctl_host = nullptr;  // pinned mirror
+  int64_t launches = 0;
+  // state carried from fhv_pofa_count to fhv_pofa_scatter
+  int64_t n_jobs = 0, n_items = 0, pass1_total = 0;
+  int32_t pass1_levels = -1;
+  int64_t pass1_tris = -1;
+  int last_cuda_error = 0;
+};
+
+namespace fhv {
+
+enum BufId {
+  kJobs = 0, kJobItems, kJobItemOff, kItemJob, kItemP0, kItemCnt, kItemOff, kScanStatus,
+  kCursors, kChainScratch, kSplatKey, kSplatWin, kSplatBox, kRays, kTmp0, kTmp1, kNumBufs
+};
+
+// grow-only scratch; returns nullptr on allocation failure
+void* scratch(fhv_ctx* ctx, BufId id, size_t bytes);
+int check_cuda(fhv_ctx* ctx, cudaError_t e);
+int sync_control(fhv_ctx* ctx, cudaStream_t s);  // copies ctl -> ctl_host, syncs, returns status
+int reset_control(fhv_ctx* ctx, cudaStream_t s);
+
+// exclusive scans (decoupled look-back, single pass); total lands in ctl->scan_total
+int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, int64_t n, cudaStream_t s);
+// POFA directory: offsets = excl-scan(counts), pyramid level L-1 from counts > 0, then upper levels
+int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
+                            int levels, cudaStream_t s);
+int pyramid_from_heads(fhv_ctx* ctx, const int32_t* heads, uint8_t* pyramid, int levels, cudaStream_t s);
+int pyramid_upper_levels(fhv_ctx* ctx, uint8_t* pyramid, int levels, cudaStream_t s);
+
+}  // namespace fhv

@@ -1,0 +1,510 @@
+// fhv_raycast.cu -- image-order reconstruction by octree ray casting over a
+// per-octant fragment volume (POFA ranges or POFL chains).
+//
+// Reference: render_raycast / _render_compiled (fhv/raycast.py:469-577) and
+// the compiled kernel raycast_image / _ray_eval / _leaf_hits / _transmit /
+// _shade_hit (fhv/_ckern.pyx:196-743).  One thread per primary ray:
+//   * f64 slab traversal of the occupancy pyramid, children entered nearest
+//     first (sorted by (t_enter, child)), stack of packed (level, code)
+//     entries (the reference keeps 56-byte entries with boxes; boxes are
+//     exact dyadic rationals, so they are recomputed from the code);
+//   * the 8 child slab tests of a node share 3 planes per axis: 9 IEEE
+//     divisions per node instead of 48, bit-identical values;
+//   * per-leaf hits sorted by (t, pool index) in a small register buffer,
+//     with an exact rescan fallback when a leaf has more hits;
+//   * front-to-back compositing, alpha cutoff after each leaf, shadow rays
+//     (mode 2) as a second traversal per hit and light;
+//   * RaycastStats counters reproduced exactly (warp-reduced atomics).
+#include "fhv_common.cuh"
+#include "fhv_internal.h"
+
+namespace fhv {
+
+constexpr int kRayMaxLevels = 12;
+constexpr int kStack = 7 * kRayMaxLevels + 1;
+constexpr int kHitBuf = 8;
+
+struct RayParams {
+  fhv_volume_t v;
+  fhv_shading_t s;
+  double eye[3];
+  double bg[4];
+  double radius, r2, cutoff, eps;
+  int mode;
+  // ray source: camera (cam != 0) or arrays
+  int from_camera, persp;
+  double rr[3], uu[3], ff[3];
+  long long W, H;
+  double half_w, half_h, t, aspect, near_;
+  const double* origins;
+  const double* dirs;
+  long long start, end;
+  double* out_rgba;
+  int32_t* out_ids;
+  long long* counters;
+};
+
+struct Stats {
+  unsigned long long visited, tested, hits, early;
+};
+
+// _slab (fhv/_ckern.pyx:196-236) for one axis, given plane parameters
+__device__ __forceinline__ bool slab_axis(double o, double d, double lo, double hi, double ta, double tb, double& t0,
+                                          double& t1) {
+  if (d == 0.0) return !(o < lo || o > hi);
+  if (ta > tb) {
+    const double s = ta;
+    ta = tb;
+    tb = s;
+  }
+  if (ta > t0) t0 = ta;
+  if (tb < t1) t1 = tb;
+  return true;
+}
+
+__device__ __forceinline__ bool slab_box(const double o[3], const double d[3], const double lo[3], const double hi[3],
+                                         double t0, double t1, double* te) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double ta = 0.0, tb = 0.0;
+    if (d[a] != 0.0) {
+      ta = __ddiv_rn(__dsub_rn(lo[a], o[a]), d[a]);
+      tb = __ddiv_rn(__dsub_rn(hi[a], o[a]), d[a]);
+    }
+    if (!slab_axis(o[a], d[a], lo[a], hi[a], ta, tb, t0, t1)) return false;
+  }
+  if (t0 > t1) return false;
+  *te = t0;
+  return true;
+}
+
+// fragment hit test (fhv/_ckern.pyx:277-291): plain f64, left to right
+__device__ __forceinline__ bool hit_test(const RayParams& x, long long k, const double o[3], const double d[3],
+                                         double tmin, double tmax, double* tout) {
+  const double px = (double)__ldg(&x.v.pos[3 * k]);
+  const double py = (double)__ldg(&x.v.pos[3 * k + 1]);
+  const double pz = (double)__ldg(&x.v.pos[3 * k + 2]);
+  const double t = __dadd_rn(__dadd_rn(__dmul_rn(__dsub_rn(px, o[0]), d[0]), __dmul_rn(__dsub_rn(py, o[1]), d[1])),
+                             __dmul_rn(__dsub_rn(pz, o[2]), d[2]));
+  if (t < tmin || t > tmax) return false;
+  const double ex = __dsub_rn(__dsub_rn(px, o[0]), __dmul_rn(t, d[0]));
+  const double ey = __dsub_rn(__dsub_rn(py, o[1]), __dmul_rn(t, d[1]));
+  const double ez = __dsub_rn(__dsub_rn(pz, o[2]), __dmul_rn(t, d[2]));
+  if (plain3(ex, ey, ez) <= x.r2) {
+    *tout = t;
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ bool hit_less(double ta, long long ia, double tb, long long ib) {
+  return ta < tb || (ta == tb && ia < ib);
+}
+
+// iterate a leaf's fragments (POFA range or POFL chain)
+template <class F>
+__device__ __forceinline__ void for_leaf(const RayParams& x, long long code, F&& f) {
+  if (x.v.layout == 0) {
+    const long long beg = __ldg(&x.v.offsets[code]);
+    const long long cnt = __ldg(&x.v.counts[code]);
+    for (long long k = beg; k < beg + cnt; ++k) f(k);
+  } else {
+    for (long long k = __ldg(&x.v.heads[code]); k >= 0; k = __ldg(&x.v.prev[k])) f(k);
+  }
+}
+
+// visit the hits of one leaf in (t, index) order; visit(t, idx) -> false stops
+template <class V>
+__device__ bool leaf_hits(const RayParams& x, long long code, const double o[3], const double d[3], double tmin,
+                          double tmax, Stats& st, V&& visit) {
+  double bt[kHitBuf];
+  long long bi[kHitBuf];
+  int nb = 0;
+  long long nh = 0, tested = 0;
+  for_leaf(x, code, [&](long long k) {
+    ++tested;
+    double t;
+    if (!hit_test(x, k, o, d, tmin, tmax, &t)) return;
+    ++nh;
+    // keep the kHitBuf smallest (t, idx), sorted
+    if (nb == kHitBuf && !hit_less(t, k, bt[kHitBuf - 1], bi[kHitBuf - 1])) return;
+    int j = nb < kHitBuf ? nb : kHitBuf - 1;
+    while (j > 0 && hit_less(t, k, bt[j - 1], bi[j - 1])) {
+      bt[j] = bt[j - 1];
+      bi[j] = bi[j - 1];
+      --j;
+    }
+    bt[j] = t;
+    bi[j] = k;
+    if (nb < kHitBuf) ++nb;
+  });
+  st.tested += tested;
+  for (int q = 0; q < nb; ++q)
+    if (!visit(bt[q], bi[q])) return false;
+  if (nh <= kHitBuf) return true;
+  // exact fallback: repeatedly select the next (t, idx) after the last one
+  double lt = bt[kHitBuf - 1];
+  long long li = bi[kHitBuf - 1];
+  for (long long done = kHitBuf; done < nh; ++done) {
+    double mt = 0.0;
+    long long mi = -1;
+    for_leaf(x, code, [&](long long k) {
+      double t;
+      if (!hit_test(x, k, o, d, tmin, tmax, &t)) return;
+      if (!hit_less(lt, li, t, k)) return;
+      if (mi < 0 || hit_less(t, k, mt, mi)) {
+        mt = t;
+        mi = k;
+      }
+    });
+    if (mi < 0) break;
+    if (!visit(mt, mi)) return false;
+    lt = mt;
+    li = mi;
+  }
+  return true;
+}
+
+// DFS over the occupancy pyramid, nearest child first (fhv/_ckern.pyx:548-633).
+// visit_leaf(code) -> false stops.
+template <class V>
+__device__ void traverse(const RayParams& x, const double o[3], const double d[3], double tmax, Stats& st,
+                         V&& visit_leaf) {
+  const double zero3[3] = {0.0, 0.0, 0.0}, one3[3] = {1.0, 1.0, 1.0};
+  double te;
+  if (!slab_box(o, d, zero3, one3, 0.0, tmax, &te)) return;
+  const int L = x.v.levels;
+  unsigned long long stack[kStack];
+  int sp = 0;
+  stack[sp++] = 0ull;  // level 0, code 0
+  while (sp > 0) {
+    const unsigned long long e = stack[--sp];
+    const int level = (int)(e >> 58);
+    const unsigned long long code = e & ((1ull << 58) - 1);
+    if (level == L) {
+      st.visited++;
+      if (!visit_leaf((long long)code)) return;
+      continue;
+    }
+    const unsigned mask = __ldg(&x.v.pyramid[pyr_level_offset(level) + (long long)code]);
+    if (mask == 0) continue;
+    const double half = __ddiv_rn(0.5, (double)(1 << level));
+    const double size = __dmul_rn(2.0, half);
+    const double lo[3] = {__dmul_rn((double)compact3(code), size), __dmul_rn((double)compact3(code >> 1), size),
+                          __dmul_rn((double)compact3(code >> 2), size)};
+    // plane parameters for lo, lo+half, lo+2*half on each axis
+    double tp[3][3];
+    double pl[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      pl[a][0] = lo[a];
+      pl[a][1] = __dadd_rn(lo[a], half);
+      pl[a][2] = __dadd_rn(pl[a][1], half);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) tp[a][k] = d[a] != 0.0 ? __ddiv_rn(__dsub_rn(pl[a][k], o[a]), d[a]) : 0.0;
+    }
+    double cte[8];
+    int cc[8];
+    int nc = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (!((mask >> c) & 1u)) continue;
+      const int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
+      double t0 = 0.0, t1 = tmax;
+      if (!slab_axis(o[0], d[0], pl[0][bx], pl[0][bx + 1], tp[0][bx], tp[0][bx + 1], t0, t1)) continue;
+      if (!slab_axis(o[1], d[1], pl[1][by], pl[1][by + 1], tp[1][by], tp[1][by + 1], t0, t1)) continue;
+      if (!slab_axis(o[2], d[2], pl[2][bz], pl[2][bz + 1], tp[2][bz], tp[2][bz + 1], t0, t1)) continue;
+      if (t0 > t1) continue;
+      int m = nc - 1;
+      while (m >= 0 && (cte[m] > t0 || (cte[m] == t0 && cc[m] > c))) {
+        cte[m + 1] = cte[m];
+        cc[m + 1] = cc[m];
+        --m;
+      }
+      cte[m + 1] = t0;
+      cc[m + 1] = c;
+      ++nc;
+    }
+    const unsigned long long lvl = (unsigned long long)(level + 1) << 58;
+    for (int j = nc - 1; j >= 0; --j) stack[sp++] = lvl | (code * 8ull + (unsigned long long)cc[j]);
+  }
+}
+
+// _transmit (fhv/_ckern.pyx:326-435)
+__device__ double transmit(const RayParams& x, const double p[3], int li, long long ex_obj, long long ex_cell,
+                           Stats& st) {
+  double l[3], tmax;
+  if (x.s.light_kind[li] == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) l[k] = x.s.light_vec[3 * li + k];
+    tmax = __longlong_as_double(0x7ff0000000000000ll);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) l[k] = __dsub_rn(x.s.light_vec[3 * li + k], p[k]);
+    const double len = __dsqrt_rn(plain3(l[0], l[1], l[2]));
+    if (len == 0.0) return 1.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) l[k] = __ddiv_rn(l[k], len);
+    tmax = len;
+  }
+  double o[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) o[k] = __dadd_rn(p[k], __dmul_rn(x.eps, l[k]));
+  double tau = 1.0;
+  traverse(x, o, l, tmax, st, [&](long long code) {
+    return leaf_hits(x, code, o, l, 0.0, tmax, st, [&](double, long long k) {
+      if ((long long)__ldg(&x.v.obj[k]) == ex_obj && code == ex_cell) return true;
+      tau = __dmul_rn(tau, __dsub_rn(1.0, x.s.alpha[__ldg(&x.v.mat[k])]));
+      return tau != 0.0;
+    });
+  });
+  return tau;
+}
+
+// _shade_hit (fhv/_ckern.pyx:438-523): plain f64 Blinn-Phong
+__device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats& st, double out[3]) {
+  const double p[3] = {(double)x.v.pos[3 * i], (double)x.v.pos[3 * i + 1], (double)x.v.pos[3 * i + 2]};
+  const double n[3] = {(double)x.v.nrm[3 * i], (double)x.v.nrm[3 * i + 1], (double)x.v.nrm[3 * i + 2]};
+  const long long m = x.v.mat[i];
+  const double* dif = x.s.diffuse + 3 * m;
+  const double* spc = x.s.specular + 3 * m;
+  const double shin = x.s.shininess[m];
+  double v[3] = {__dsub_rn(x.eye[0], p[0]), __dsub_rn(x.eye[1], p[1]), __dsub_rn(x.eye[2], p[2])};
+  const double vl = __dsqrt_rn(plain3(v[0], v[1], v[2]));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v[k] = vl > 0.0 ? __ddiv_rn(v[k], vl) : 0.0;
+  double r = 0.0, g = 0.0, b = 0.0;
+  for (int li = 0; li < x.s.n_lights; ++li) {
+    double l[3];
+    if (x.s.light_kind[li] == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) l[k] = x.s.light_vec[3 * li + k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) l[k] = __dsub_rn(x.s.light_vec[3 * li + k], p[k]);
+      const double ll = __dsqrt_rn(plain3(l[0], l[1], l[2]));
+#pragma unroll
+      for (int k = 0; k < 3; ++k) l[k] = ll > 0.0 ? __ddiv_rn(l[k], ll) : 0.0;
+    }
+    double h[3] = {__dadd_rn(l[0], v[0]), __dadd_rn(l[1], v[1]), __dadd_rn(l[2], v[2])};
+    const double hl = __dsqrt_rn(plain3(h[0], h[1], h[2]));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) h[k] = hl > 0.0 ? __ddiv_rn(h[k], hl) : 0.0;
+    double ndl = __dadd_rn(__dadd_rn(__dmul_rn(n[0], l[0]), __dmul_rn(n[1], l[1])), __dmul_rn(n[2], l[2]));
+    if (ndl < 0.0) ndl = 0.0;
+    double ndh = __dadd_rn(__dadd_rn(__dmul_rn(n[0], h[0]), __dmul_rn(n[1], h[1])), __dmul_rn(n[2], h[2]));
+    if (ndh < 0.0) ndh = 0.0;
+    double tau = 1.0;
+    if (x.mode == 2) tau = transmit(x, p, li, (long long)x.v.obj[i], leaf, st);
+    const double sp = pow(ndh, shin);
+    const double* amb = x.s.light_ambient + 3 * li;
+    const double* col = x.s.light_color + 3 * li;
+    r = __dadd_rn(r, __dmul_rn(amb[0], dif[0]));
+    g = __dadd_rn(g, __dmul_rn(amb[1], dif[1]));
+    b = __dadd_rn(b, __dmul_rn(amb[2], dif[2]));
+    const double tn = __dmul_rn(tau, ndl), ts = __dmul_rn(tau, sp);
+    r = __dadd_rn(r, __dmul_rn(__dmul_rn(tn, dif[0]), col[0]));
+    g = __dadd_rn(g, __dmul_rn(__dmul_rn(tn, dif[1]), col[1]));
+    b = __dadd_rn(b, __dmul_rn(__dmul_rn(tn, dif[2]), col[2]));
+    r = __dadd_rn(r, __dmul_rn(__dmul_rn(ts, spc[0]), col[0]));
+    g = __dadd_rn(g, __dmul_rn(__dmul_rn(ts, spc[1]), col[1]));
+    b = __dadd_rn(b, __dmul_rn(__dmul_rn(ts, spc[2]), col[2]));
+  }
+  out[0] = r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);
+  out[1] = g < 0.0 ? 0.0 : (g > 1.0 ? 1.0 : g);
+  out[2] = b < 0.0 ? 0.0 : (b > 1.0 ? 1.0 : b);
+}
+
+// primary_rays (fhv/raycast.py:148-172), elementwise numpy semantics
+__device__ __forceinline__ void camera_ray(const RayParams& x, long long k, double o[3], double d[3]) {
+  const long long iy = k / x.W, ix = k - iy * x.W;
+  const double nx = __dsub_rn(__dmul_rn(__ddiv_rn(__dadd_rn((double)ix, 0.5), (double)x.W), 2.0), 1.0);
+  const double ny = __dsub_rn(1.0, __dmul_rn(__ddiv_rn(__dadd_rn((double)iy, 0.5), (double)x.H), 2.0));
+  if (!x.persp) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double hw = __dmul_rn(x.half_w, x.rr[c]), hh = __dmul_rn(x.half_h, x.uu[c]);
+      o[c] = __dadd_rn(__dadd_rn(__dadd_rn(x.eye[c], __dmul_rn(nx, hw)), __dmul_rn(ny, hh)), __dmul_rn(x.near_, x.ff[c]));
+      d[c] = x.ff[c];
+    }
+  } else {
+    const double ta = __dmul_rn(x.t, x.aspect);
+    double v[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      v[c] = __dadd_rn(__dadd_rn(x.ff[c], __dmul_rn(nx, __dmul_rn(ta, x.rr[c]))), __dmul_rn(ny, __dmul_rn(x.t, x.uu[c])));
+    const double len = __dsqrt_rn(plain3(v[0], v[1], v[2]));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      d[c] = __ddiv_rn(v[c], len);
+      o[c] = x.eye[c];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) k_raycast(RayParams x) {
+  Stats st = {0, 0, 0, 0};
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  for (long long k = x.start + blockIdx.x * (long long)blockDim.x + threadIdx.x; k < x.end;
+       k += (long long)gridDim.x * blockDim.x) {
+    double o[3], d[3];
+    if (x.from_camera) {
+      camera_ray(x, k, o, d);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        o[c] = x.origins[3 * k + c];
+        d[c] = x.dirs[3 * k + c];
+      }
+    }
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, acc = 0.0;
+    bool any_hit = false;
+    long long first_obj = -1;
+    traverse(x, o, d, inf, st, [&](long long code) {
+      bool stop = false;
+      leaf_hits(x, code, o, d, 0.0, inf, st, [&](double, long long i) {
+        st.hits++;
+        if (first_obj < 0) first_obj = (long long)x.v.obj[i];
+        double col[3];
+        if (x.mode == 0) {
+          shade_hit(x, i, code, st, col);
+          c0 = col[0];
+          c1 = col[1];
+          c2 = col[2];
+          acc = 1.0;
+          any_hit = true;
+          stop = true;
+          return false;
+        }
+        const double a = x.s.alpha[x.v.mat[i]];
+        shade_hit(x, i, code, st, col);
+        const double tc = __dmul_rn(__dsub_rn(1.0, acc), a);
+        c0 = __dadd_rn(c0, __dmul_rn(tc, col[0]));
+        c1 = __dadd_rn(c1, __dmul_rn(tc, col[1]));
+        c2 = __dadd_rn(c2, __dmul_rn(tc, col[2]));
+        acc = __dadd_rn(acc, tc);
+        any_hit = true;
+        return true;
+      });
+      if (stop) return false;
+      if (x.cutoff >= 0.0 && acc >= x.cutoff) {
+        st.early++;
+        return false;
+      }
+      return true;
+    });
+    double4 px;
+    if (x.mode == 0) {
+      px = any_hit ? make_double4(c0, c1, c2, 1.0) : make_double4(x.bg[0], x.bg[1], x.bg[2], x.bg[3]);
+    } else {
+      const double ra = __dsub_rn(1.0, acc);
+      px.x = __dadd_rn(c0, __dmul_rn(__dmul_rn(ra, x.bg[3]), x.bg[0]));
+      px.y = __dadd_rn(c1, __dmul_rn(__dmul_rn(ra, x.bg[3]), x.bg[1]));
+      px.z = __dadd_rn(c2, __dmul_rn(__dmul_rn(ra, x.bg[3]), x.bg[2]));
+      px.w = __dadd_rn(acc, __dmul_rn(ra, x.bg[3]));
+    }
+    reinterpret_cast<double4*>(x.out_rgba)[k] = px;
+    if (x.out_ids && first_obj >= 0) x.out_ids[k] = (int32_t)first_obj;
+  }
+  unsigned long long v[4] = {st.visited, st.tested, st.hits, st.early};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+  }
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (v[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&x.counters[q]), v[q]);
+  }
+}
+
+namespace {
+inline int grid_for(long long n, int block, int per_sm = 16) {
+  long long g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 148LL * per_sm) g = 148LL * per_sm;
+  return (int)g;
+}
+
+int launch(fhv_ctx* ctx, RayParams& x, void* stream) {
+  if (x.end <= x.start) return FHV_OK;
+  k_raycast<<<grid_for(x.end - x.start, 128), 128, 0, (cudaStream_t)stream>>>(x);
+  ctx->launches++;
+  return check_cuda(ctx, cudaGetLastError());
+}
+
+int common(RayParams& x, const fhv_volume_t* vol, const fhv_shading_t* shading, const double* background, double radius,
+           double cutoff, int32_t mode, double eps, double* out_rgba, int32_t* out_ids, int64_t* counters) {
+  if (!vol || !shading || !background || !out_rgba || !counters) return FHV_BAD_ARGS;
+  if (vol->levels < 1 || vol->levels > kRayMaxLevels || !vol->pyramid) return FHV_BAD_ARGS;
+  if (vol->layout == 0 && (!vol->offsets || !vol->counts)) return FHV_BAD_ARGS;
+  if (vol->layout == 1 && (!vol->heads || !vol->prev)) return FHV_BAD_ARGS;
+  if (mode < 0 || mode > 2 || !(radius > 0.0)) return FHV_BAD_ARGS;
+  x.v = *vol;
+  x.s = *shading;
+  for (int c = 0; c < 4; ++c) x.bg[c] = background[c];
+  x.radius = radius;
+  x.r2 = radius * radius;
+  x.cutoff = cutoff;
+  x.eps = eps;
+  x.mode = mode;
+  x.out_rgba = out_rgba;
+  x.out_ids = out_ids;
+  x.counters = (long long*)counters;
+  return FHV_OK;
+}
+}  // namespace
+
+}  // namespace fhv
+
+using namespace fhv;
+
+extern "C" int fhv_raycast(fhv_ctx* ctx, const fhv_volume_t* vol, const fhv_shading_t* shading, const double* cam,
+                           const double* background, double radius, double cutoff, int32_t mode, double shadow_eps,
+                           int64_t row0, int64_t row1, double* out_rgba, int32_t* out_ids, int64_t* counters,
+                           void* stream) {
+  if (!ctx || !cam) return FHV_BAD_ARGS;
+  RayParams x;
+  std::memset(&x, 0, sizeof(x));
+  int rc = common(x, vol, shading, background, radius, cutoff, mode, shadow_eps, out_rgba, out_ids, counters);
+  if (rc) return rc;
+  x.from_camera = 1;
+  x.persp = cam[0] != 0.0;
+  for (int c = 0; c < 3; ++c) {
+    x.eye[c] = cam[1 + c];
+    x.rr[c] = cam[4 + c];
+    x.uu[c] = cam[7 + c];
+    x.ff[c] = cam[10 + c];
+  }
+  x.W = (long long)cam[13];
+  x.H = (long long)cam[14];
+  x.half_w = cam[15];
+  x.half_h = cam[16];
+  x.t = cam[17];
+  x.aspect = cam[18];
+  x.near_ = cam[19];
+  if (row0 < 0 || row1 > x.H || row0 > row1) return FHV_BAD_ARGS;
+  x.start = row0 * x.W;
+  x.end = row1 * x.W;
+  return launch(ctx, x, stream);
+}
+
+extern "C" int fhv_raycast_image(fhv_ctx* ctx, int64_t start, int64_t end, const double* origins, const double* dirs,
+                                 const fhv_volume_t* vol, const fhv_shading_t* shading, const double* eye,
+                                 const double* background, double radius, double cutoff, int32_t mode,
+                                 double shadow_eps, double* out_rgba, int32_t* out_ids, int64_t* counters,
+                                 void* stream) {
+  if (!ctx || !origins || !dirs || !eye || start < 0 || end < start) return FHV_BAD_ARGS;
+  RayParams x;
+  std::memset(&x, 0, sizeof(x));
+  int rc = common(x, vol, shading, background, radius, cutoff, mode, shadow_eps, out_rgba, out_ids, counters);
+  if (rc) return rc;
+  x.from_camera = 0;
+  for (int c = 0; c < 3; ++c) x.eye[c] = eye[c];
+  x.origins = origins;
+  x.dirs = dirs;
+  x.start = start;
+  x.end = end;
+  return launch(ctx, x, stream);
+}

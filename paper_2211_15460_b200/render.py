@@ -1,0 +1,71 @@
+"""Point-splat reconstruction on the device (splat_render, fhv/render.py:249-320).
+
+Also re-exports the shading / compositing value types (see lights.py) so the
+module mirrors ``fhv.render``.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceShading, host_f64
+from .lights import (GBuffer, ImageBuffer, Light, composite_over, front_to_back_accumulate, headlight,
+                     material_arrays, read_float_dump, read_ppm, resolve_over_background, srgb_encode,
+                     write_float_dump, write_ppm)
+from .scene import Camera, SceneError
+
+__all__ = ["GBuffer", "ImageBuffer", "Light", "composite_over", "front_to_back_accumulate", "headlight",
+           "material_arrays", "read_float_dump", "read_ppm", "resolve_over_background", "splat_render",
+           "srgb_encode", "write_float_dump", "write_ppm"]
+
+
+def splat_render(pool, camera: Camera, lights, splat_radius_world: float, materials,
+                 background=(0.0, 0.0, 0.0, 0.0), id_buffer: GBuffer | None = None, *,
+                 packed: bool = False, n: int | None = None, out: ImageBuffer | None = None) -> ImageBuffer:
+    """Z-tested point splatting of a fragment pool into a novel view.
+
+    Returns an ImageBuffer whose ``pixels`` (h, w, 4) and ``depth`` (h, w)
+    are float64 CUDA tensors.  ``id_buffer`` (GBuffer of CUDA tensors, e.g.
+    from :func:`device_gbuffer`) receives the winners' attributes.
+    ``packed=True`` selects the single 64-bit (f32 depth | index) atomicMin
+    variant.  ``out`` reuses preallocated image tensors.
+    """
+    if splat_radius_world <= 0.0:
+        raise SceneError("splat radius must be > 0")
+    dev = pool.device
+    w, h = camera.resolution
+    if out is None:
+        out = ImageBuffer(w, h, torch.empty((h, w, 4), dtype=torch.float64, device=dev),
+                          torch.empty((h, w), dtype=torch.float64, device=dev))
+    count = pool.stored_count if n is None else int(n)
+    shading = DeviceShading(materials, lights, dev)
+    gb = None
+    if id_buffer is not None:
+        gb = _lib.GBuf(_lib.ptr(id_buffer.position), _lib.ptr(id_buffer.normal), _lib.ptr(id_buffer.material_id),
+                       _lib.ptr(id_buffer.object_id), _lib.ptr(id_buffer.valid))
+    cam = host_f64(camera.scalars())
+    bg = host_f64(background)
+    lib = _lib.load()
+    rc = lib.fhv_splat(_lib.ctx(dev), count, _lib.ptr(pool.position), _lib.ptr(pool.normal),
+                       _lib.ptr(pool.material_id), _lib.ptr(pool.object_id), cam.ctypes.data, float(splat_radius_world),
+                       bg.ctypes.data, shading.struct(), _lib.ptr(out.pixels), _lib.ptr(out.depth), None,
+                       gb, _lib.FHV_SPLAT_PACKED if packed else 0, _lib.stream_ptr(dev))
+    _lib.check(rc, "splat_render")
+    return out
+
+
+def device_gbuffer(width: int, height: int, device) -> GBuffer:
+    """GBuffer of CUDA tensors for splat_render's id_buffer."""
+    return GBuffer(torch.zeros((height, width, 3), dtype=torch.float64, device=device),
+                   torch.zeros((height, width, 3), dtype=torch.float64, device=device),
+                   torch.full((height, width), -1, dtype=torch.int32, device=device),
+                   torch.full((height, width), -1, dtype=torch.int32, device=device),
+                   torch.zeros((height, width), dtype=torch.uint8, device=device))
+
+
+def image_numpy(img: ImageBuffer) -> ImageBuffer:
+    """Host copy with the reference's numpy dtypes."""
+    px = img.pixels.cpu().numpy() if isinstance(img.pixels, torch.Tensor) else np.asarray(img.pixels)
+    dp = img.depth.cpu().numpy() if isinstance(img.depth, torch.Tensor) else np.asarray(img.depth)
+    return ImageBuffer(img.width, img.height, px, dp)

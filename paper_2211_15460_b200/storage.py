@@ -1,0 +1,586 @@
+"""Fragment stores on the device: PPFL, POFL and POFA.
+
+Drop-in for ``fhv/storage.py``: same builder names and signatures
+(``build_ppfl``, ``build_pofl``, ``pofa_build``), same volume types
+(``FhvPpfl``, ``FhvPofl``, ``FhvPofa``) and pool/directory fields, but every
+array is a CUDA tensor written by the sm_100a capture kernels
+(``csrc/fhv_capture.cu``) through the C ABI.  ``threads`` is accepted and
+ignored (the reference's GIL-bound thread pool has no analogue here).
+
+Pool order: by default fragment k of the reference's sequential emission
+order lands at pool index k (``alloc="ordered"``), so pools are bit-identical
+to the reference.  Linked-list chains are linked with atomicExch and are
+multiset-equal per key; ``exact_order=True`` additionally restores the
+reference's chain order (and, for POFA, the in-leaf order), making every
+array bit-identical.  ``alloc="atomic"`` is the paper's GPU allocator
+(warp-aggregated atomicAdd on one counter): nondeterministic order.
+"""
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import capture_cfg, default_device, device_scene
+from .raster import CaptureStats, CaptureStrategy, RasterConfig, capture_plan
+from .scene import Material, Scene
+
+__all__ = [
+    "FhvError", "FhvPofa", "FhvPofl", "FhvPpfl", "FragmentPool", "FragmentRecord", "MAX_LEVELS",
+    "OccupancyPyramid", "PixelDirectory", "PofaBuildError", "PofaDirectory", "PoflDirectory", "RECORD_DTYPE",
+    "RECORD_SIZE_ALIGNED", "RECORD_SIZE_PACKED", "build_pofl", "build_ppfl", "cell_box", "cell_code", "cell_of",
+    "load_snapshot", "memory_report", "morton_decode", "morton_encode", "pofa_build", "rebuild_pofl_as_pofa",
+    "save_snapshot", "snapshot_bytes",
+]
+
+MAX_LEVELS = 20
+RECORD_DTYPE = np.dtype([("position", "<f4", (3,)), ("normal", "<f4", (3,)), ("material_id", "<u4"),
+                         ("object_id", "<u4"), ("prev_index", "<i4")])
+RECORD_SIZE_PACKED = 36
+RECORD_SIZE_ALIGNED = 48
+
+
+class FhvError(ValueError):
+    """Invalid storage parameters or corrupted structure (fhv/storage.py:69-70)."""
+
+
+class PofaBuildError(FhvError):
+    """The two capture passes of an array build disagreed (fhv/storage.py:73-74)."""
+
+
+# ---------------------------------------------------------------------------
+# Morton codes and cells (host utilities, fhv/storage.py:83-172)
+
+_U = np.uint64
+
+
+def _spread(v):
+    v = v & _U(0x1FFFFF)
+    for sh, m in ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F),
+                  (4, 0x10C30C30C30C30C3), (2, 0x1249249249249249)):
+        v = (v | (v << _U(sh))) & _U(m)
+    return v
+
+
+def _compact(v):
+    v = v & _U(0x1249249249249249)
+    for sh, m in ((2, 0x10C30C30C30C30C3), (4, 0x100F00F00F00F00F), (8, 0x1F0000FF0000FF),
+                  (16, 0x1F00000000FFFF), (32, 0x1FFFFF)):
+        v = (v | (v >> _U(sh))) & _U(m)
+    return v
+
+
+def _check_levels(levels: int) -> None:
+    if not 0 <= levels <= MAX_LEVELS:
+        raise FhvError(f"levels {levels} outside [0, {MAX_LEVELS}]")
+
+
+def morton_encode(x, y, z, levels: int):
+    _check_levels(levels)
+    scalar = np.isscalar(x) and np.isscalar(y) and np.isscalar(z)
+    xyz = [np.asarray(v, dtype=np.int64) for v in (x, y, z)]
+    side = np.int64(1) << levels
+    for name, v in zip("xyz", xyz):
+        if np.any(v < 0) or np.any(v >= side):
+            raise FhvError(f"{name} cell index outside [0, 2^{levels})")
+    code = (_spread(xyz[0].astype(_U)) | (_spread(xyz[1].astype(_U)) << _U(1))
+            | (_spread(xyz[2].astype(_U)) << _U(2))).astype(np.int64)
+    return int(code) if scalar else code
+
+
+def morton_decode(code, levels: int):
+    _check_levels(levels)
+    scalar = np.isscalar(code)
+    c = np.asarray(code, dtype=np.int64)
+    if np.any(c < 0) or np.any(c >= (np.int64(1) << (3 * levels))):
+        raise FhvError(f"code outside [0, 8^{levels})")
+    u = c.astype(_U)
+    out = tuple(_compact(u >> _U(k)).astype(np.int64) for k in range(3))
+    return tuple(int(v) for v in out) if scalar else out
+
+
+def cell_of(position, levels: int) -> np.ndarray:
+    _check_levels(levels)
+    p = np.asarray(position, dtype=np.float64)
+    if not np.all(np.isfinite(p)):
+        raise FhvError("non-finite position")
+    if np.any(p < -1e-6) or np.any(p > 1.0 + 1e-6):
+        raise FhvError("position outside [0,1]^3")
+    side = np.int64(1) << levels
+    return np.clip(np.floor(p * float(side)).astype(np.int64), 0, side - 1)
+
+
+def cell_code(position, levels: int):
+    idx = cell_of(position, levels)
+    return morton_encode(idx[..., 0], idx[..., 1], idx[..., 2], levels)
+
+
+def cell_box(code: int, level: int):
+    x, y, z = morton_decode(int(code), level)
+    size = 1.0 / (1 << level)
+    lo = np.array([x, y, z], dtype=np.float64) * size
+    return lo, lo + size
+
+
+# ---------------------------------------------------------------------------
+# pool and directories (device tensors)
+
+
+@dataclass
+class FragmentRecord:
+    position: np.ndarray
+    normal: np.ndarray
+    material_id: int
+    object_id: int
+    prev_index: int
+
+
+class FragmentPool:
+    """Pre-allocated fragment storage, struct-of-arrays on the device
+    (fhv/storage.py:188-248).  ``next_free`` keeps counting past capacity;
+    records beyond it are dropped and ``overflowed`` is set."""
+
+    def __init__(self, capacity: int, device=None):
+        if capacity < 0:
+            raise FhvError("capacity must be >= 0")
+        dev = default_device(device)
+        self.capacity = int(capacity)
+        self.device = dev
+        self.position = torch.empty((capacity, 3), dtype=torch.float32, device=dev)
+        self.normal = torch.empty((capacity, 3), dtype=torch.float32, device=dev)
+        self.material_id = torch.empty(capacity, dtype=torch.uint32, device=dev)
+        self.object_id = torch.empty(capacity, dtype=torch.uint32, device=dev)
+        self.prev_index = torch.full((capacity,), -1, dtype=torch.int32, device=dev)
+        self.next_free = 0
+        self.overflowed = False
+
+    @property
+    def stored_count(self) -> int:
+        return min(self.next_free, self.capacity)
+
+    def struct(self) -> _lib.Pool:
+        return _lib.Pool(self.capacity, _lib.ptr(self.position), _lib.ptr(self.normal), _lib.ptr(self.material_id),
+                         _lib.ptr(self.object_id), _lib.ptr(self.prev_index))
+
+    def numpy(self) -> dict:
+        """Host copies of the stored prefix (reference dtypes)."""
+        n = self.stored_count
+        return {"position": self.position[:n].cpu().numpy(), "normal": self.normal[:n].cpu().numpy(),
+                "material_id": self.material_id[:n].cpu().numpy(), "object_id": self.object_id[:n].cpu().numpy(),
+                "prev_index": self.prev_index[:n].cpu().numpy()}
+
+    def record(self, i: int) -> FragmentRecord:
+        if not 0 <= i < self.stored_count:
+            raise FhvError(f"record index {i} out of range")
+        return FragmentRecord(self.position[i].cpu().numpy(), self.normal[i].cpu().numpy(),
+                              int(self.material_id[i]), int(self.object_id[i]), int(self.prev_index[i]))
+
+    def to_struct_array(self) -> np.ndarray:
+        h = self.numpy()
+        out = np.empty(self.stored_count, dtype=RECORD_DTYPE)
+        for k in RECORD_DTYPE.names:
+            out[k] = h[k]
+        return out
+
+    @staticmethod
+    def from_struct_array(arr: np.ndarray, device=None) -> "FragmentPool":
+        pool = FragmentPool(len(arr), device)
+        pool.position.copy_(torch.from_numpy(np.ascontiguousarray(arr["position"])))
+        pool.normal.copy_(torch.from_numpy(np.ascontiguousarray(arr["normal"])))
+        pool.material_id.copy_(torch.from_numpy(np.ascontiguousarray(arr["material_id"]).view(np.int32)).view(torch.uint32))
+        pool.object_id.copy_(torch.from_numpy(np.ascontiguousarray(arr["object_id"]).view(np.int32)).view(torch.uint32))
+        pool.prev_index.copy_(torch.from_numpy(np.ascontiguousarray(arr["prev_index"])))
+        pool.next_free = len(arr)
+        return pool
+
+
+@dataclass
+class PixelDirectory:
+    width: int
+    height: int
+    heads: torch.Tensor  # int32 (h*w,), -1 = empty
+
+    def head(self, x: int, y: int) -> int:
+        return int(self.heads[y * self.width + x])
+
+
+@dataclass
+class PoflDirectory:
+    levels: int
+    heads: torch.Tensor  # int32 (8^L,)
+
+
+@dataclass
+class PofaDirectory:
+    levels: int
+    offsets: torch.Tensor  # uint32 (8^L,)
+    counts: torch.Tensor   # uint32 (8^L,)
+
+
+def _pyr_offsets(L: int):
+    return [((1 << (3 * k)) - 1) // 7 for k in range(L + 1)]
+
+
+class OccupancyPyramid:
+    """Levels 0..L-1 of 8-bit child masks, stored concatenated on the device
+    (the layout the ray-cast kernel reads, fhv/raycast.py:539-544)."""
+
+    def __init__(self, leaf_levels: int, data: torch.Tensor | None = None, device=None):
+        _check_levels(leaf_levels)
+        if leaf_levels < 1:
+            raise FhvError("octree needs at least one level")
+        self.leaf_levels = leaf_levels
+        n = _pyr_offsets(leaf_levels)[-1]
+        self.data = data if data is not None else torch.zeros(n, dtype=torch.uint8, device=default_device(device))
+
+    @property
+    def levels(self) -> list:
+        off = _pyr_offsets(self.leaf_levels)
+        return [self.data[off[k]:off[k + 1]] for k in range(self.leaf_levels)]
+
+    def mask(self, level: int, node: int) -> int:
+        return int(self.data[_pyr_offsets(self.leaf_levels)[level] + node])
+
+    def leaf_occupancy(self) -> torch.Tensor:
+        last = self.levels[-1].to(torch.int32)
+        bits = (last[:, None] >> torch.arange(8, device=last.device, dtype=torch.int32)) & 1
+        return bits.bool().reshape(-1)
+
+    def occupied_leaves(self) -> torch.Tensor:
+        return torch.nonzero(self.leaf_occupancy()).reshape(-1).to(torch.int64)
+
+    def equals(self, other: "OccupancyPyramid") -> bool:
+        return self.leaf_levels == other.leaf_levels and bool(torch.equal(self.data.cpu(), other.data.cpu()))
+
+
+# ---------------------------------------------------------------------------
+# built volumes
+
+
+@dataclass
+class FhvPpfl:
+    directory: PixelDirectory
+    pool: FragmentPool
+    capture_resolution: int
+    stats: CaptureStats | None = None
+    materials: list | None = None
+    layout = "PPFL"
+
+    def pixel_indices(self, x: int, y: int) -> np.ndarray:
+        return _chain(self.directory.heads, self.pool.prev_index, y * self.directory.width + x)
+
+
+@dataclass
+class FhvPofl:
+    directory: PoflDirectory
+    pyramid: OccupancyPyramid
+    pool: FragmentPool
+    capture_resolution: int
+    stats: CaptureStats | None = None
+    materials: list | None = None
+    layout = "POFL"
+
+    @property
+    def levels(self) -> int:
+        return self.directory.levels
+
+    def leaf_indices(self, code: int) -> np.ndarray:
+        return _chain(self.directory.heads, self.pool.prev_index, code)
+
+    def occupied_leaves(self) -> torch.Tensor:
+        return torch.nonzero(self.directory.heads >= 0).reshape(-1).to(torch.int64)
+
+
+@dataclass
+class FhvPofa:
+    directory: PofaDirectory
+    pyramid: OccupancyPyramid
+    pool: FragmentPool
+    capture_resolution: int
+    stats: CaptureStats | None = None
+    materials: list | None = None
+    layout = "POFA"
+
+    @property
+    def levels(self) -> int:
+        return self.directory.levels
+
+    def leaf_indices(self, code: int) -> np.ndarray:
+        off = int(self.directory.offsets[code])
+        return np.arange(off, off + int(self.directory.counts[code]), dtype=np.int64)
+
+    def occupied_leaves(self) -> torch.Tensor:
+        return torch.nonzero(self.directory.counts > 0).reshape(-1).to(torch.int64)
+
+
+def _chain(heads, prev, key) -> np.ndarray:
+    out, i = [], int(heads[key])
+    while i >= 0:
+        out.append(i)
+        i = int(prev[i])
+    return np.asarray(out, dtype=np.int64)
+
+
+# ---------------------------------------------------------------------------
+# builders (C ABI)
+
+
+def _flags(alloc: str, exact_order: bool) -> int:
+    if alloc not in ("ordered", "atomic"):
+        raise FhvError(f"unknown alloc mode {alloc!r}")
+    return (_lib.FHV_ALLOC_ATOMIC if alloc == "atomic" else 0) | (_lib.FHV_EXACT_ORDER if exact_order else 0)
+
+
+def build_ppfl(scene: Scene, cfg: RasterConfig, strategy: CaptureStrategy | None = None,
+               capacity: int | None = None, overalloc: float = 10.0, threads: int = 1, *,
+               exact_order: bool = False, alloc: str = "ordered", device=None) -> FhvPpfl:
+    """Per-pixel linked lists (fhv/storage.py:553-571); OneView only."""
+    strategy = strategy or CaptureStrategy.one_view()
+    if strategy.kind != "one_view":
+        raise FhvError("per-pixel layout requires the single-view strategy")
+    w, h = cfg.resolution
+    if capacity is None:
+        capacity = int(w * h * overalloc)
+    plan = capture_plan(scene, strategy, cfg)
+    ds = device_scene(scene, device)
+    dev = ds.device
+    pool = FragmentPool(capacity, dev)
+    heads = torch.full((w * h,), -1, dtype=torch.int32, device=dev)
+    nf = ctypes_i64()
+    lib = _lib.load()
+    tris, c, p = ds.struct(), capture_cfg(plan), pool.struct()
+    rc = lib.fhv_build_ppfl(_lib.ctx(dev), tris, c, w, p, _lib.ptr(heads), _flags(alloc, exact_order), nf,
+                            _lib.stream_ptr(dev))
+    _lib.check(rc, "build_ppfl", allow=(_lib.FHV_OK, _lib.FHV_OVERFLOW))
+    pool.next_free = int(nf.value)
+    pool.overflowed = pool.next_free > pool.capacity
+    return FhvPpfl(PixelDirectory(w, h, heads), pool, h, plan.stats(pool.next_free), scene.materials)
+
+
+def build_pofl(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int,
+               capacity: int | None = None, overalloc: float = 10.0, threads: int = 1, *,
+               exact_order: bool = False, alloc: str = "ordered", device=None) -> FhvPofl:
+    """Per-octant linked lists + occupancy pyramid (fhv/storage.py:574-587)."""
+    if levels < 1:
+        raise FhvError("octree needs at least one level")
+    _check_levels(levels)
+    w, h = cfg.resolution
+    if capacity is None:
+        capacity = int(w * h * overalloc)
+    plan = capture_plan(scene, strategy, cfg)
+    ds = device_scene(scene, device)
+    dev = ds.device
+    pool = FragmentPool(capacity, dev)
+    heads = torch.full((8 ** levels,), -1, dtype=torch.int32, device=dev)
+    pyr = OccupancyPyramid(levels, device=dev)
+    nf = ctypes_i64()
+    lib = _lib.load()
+    tris, c, p = ds.struct(), capture_cfg(plan), pool.struct()
+    rc = lib.fhv_build_pofl(_lib.ctx(dev), tris, c, levels, p, _lib.ptr(heads), _lib.ptr(pyr.data),
+                            _flags(alloc, exact_order), nf, _lib.stream_ptr(dev))
+    _lib.check(rc, "build_pofl", allow=(_lib.FHV_OK, _lib.FHV_OVERFLOW))
+    pool.next_free = int(nf.value)
+    pool.overflowed = pool.next_free > pool.capacity
+    return FhvPofl(PoflDirectory(levels, heads), pyr, pool, h, plan.stats(pool.next_free), scene.materials)
+
+
+def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int, threads: int = 1, *,
+               exact_order: bool = False, device=None) -> FhvPofa:
+    """Two-pass per-octant arrays (fhv/storage.py:590-621): per-leaf histogram,
+    exclusive scan (+ pyramid), exact pool, scatter into leaf ranges."""
+    if levels < 1:
+        raise FhvError("octree needs at least one level")
+    if levels > 11:
+        raise FhvError(f"levels {levels}: dense POFA directories beyond L=11 exceed device memory")
+    plan = capture_plan(scene, strategy, cfg)
+    ds = device_scene(scene, device)
+    dev = ds.device
+    n_leaf = 8 ** levels
+    counts = torch.empty(n_leaf, dtype=torch.uint32, device=dev)
+    offsets = torch.empty(n_leaf, dtype=torch.uint32, device=dev)
+    pyr = OccupancyPyramid(levels, device=dev)
+    lib = _lib.load()
+    tris, c = ds.struct(), capture_cfg(plan)
+    total = ctypes_i64()
+    cx = _lib.ctx(dev)
+    st = _lib.stream_ptr(dev)
+    rc = lib.fhv_pofa_count(cx, tris, c, levels, _lib.ptr(counts), _lib.ptr(offsets), _lib.ptr(pyr.data), total, st)
+    _lib.check(rc, "pofa_build pass 1")
+    pool = FragmentPool(int(total.value), dev)
+    p = pool.struct()
+    rc = lib.fhv_pofa_scatter(cx, tris, c, levels, _lib.ptr(counts), _lib.ptr(offsets), p,
+                              _lib.FHV_EXACT_ORDER if exact_order else 0, st)
+    _lib.check(rc, "pofa_build pass 2")
+    pool.next_free = pool.capacity
+    return FhvPofa(PofaDirectory(levels, offsets, counts), pyr, pool, int(cfg.resolution[1]),
+                   plan.stats(pool.next_free), scene.materials)
+
+
+def ctypes_i64():
+    import ctypes
+    return ctypes.c_int64(0)
+
+
+def rebuild_pofl_as_pofa(fhv: FhvPofl) -> FhvPofa:
+    """Repack a POFL into POFA (fhv/storage.py:624-652): group by leaf in
+    Morton order, keep emission (pool) order inside each leaf.  Uses device
+    tensor ops (a stable sort by leaf code); not on the timed path."""
+    pool = fhv.pool
+    n, L, dev = pool.stored_count, fhv.levels, pool.device
+    pos = pool.position[:n].to(torch.float64)
+    side = float(1 << L)
+    idx = torch.clamp(torch.floor(pos * side).to(torch.int64), 0, (1 << L) - 1).cpu().numpy()
+    codes = morton_encode(idx[:, 0], idx[:, 1], idx[:, 2], L) if n else np.empty(0, np.int64)
+    counts64 = np.bincount(codes, minlength=8 ** L)
+    counts = counts64.astype(np.uint32)
+    offsets = np.concatenate(([0], np.cumsum(counts[:-1], dtype=np.int64))).astype(np.uint32)
+    perm = torch.from_numpy(np.lexsort((np.arange(n), codes))).to(dev)
+    new = FragmentPool(n, dev)
+    new.position.copy_(pool.position[:n][perm])
+    new.normal.copy_(pool.normal[:n][perm])
+    new.material_id.copy_(pool.material_id[:n].view(torch.int32)[perm].view(torch.uint32))
+    new.object_id.copy_(pool.object_id[:n].view(torch.int32)[perm].view(torch.uint32))
+    new.next_free = n
+    occ = np.repeat(False, 8 ** L) if n == 0 else counts > 0
+    pyr = _pyramid_from_occupancy_host(occ, L, dev)
+    d = PofaDirectory(L, torch.from_numpy(offsets.view(np.int32)).to(dev).view(torch.uint32),
+                      torch.from_numpy(counts.view(np.int32)).to(dev).view(torch.uint32))
+    return FhvPofa(d, pyr, new, fhv.capture_resolution, fhv.stats, fhv.materials)
+
+
+def _pyramid_from_occupancy_host(occ: np.ndarray, L: int, dev) -> OccupancyPyramid:
+    levels = [None] * L
+    bits = 1 << np.arange(8, dtype=np.uint32)
+    cur = np.asarray(occ, dtype=bool)
+    for k in range(L - 1, -1, -1):
+        masks = (cur.reshape(-1, 8).astype(np.uint32) * bits).sum(axis=1).astype(np.uint8)
+        levels[k] = masks
+        cur = masks > 0
+    return OccupancyPyramid(L, torch.from_numpy(np.concatenate(levels)).to(dev))
+
+
+# ---------------------------------------------------------------------------
+# memory accounting (fhv/storage.py:659-719; host arithmetic)
+
+
+def memory_report(layout: str, *, resolution=None, levels=None, record_size: int = RECORD_SIZE_ALIGNED,
+                  capacity=None, exact_count=None, overalloc: float = 10.0, gbuffer_payload_bytes: int = 28) -> dict:
+    if record_size not in (RECORD_SIZE_PACKED, RECORD_SIZE_ALIGNED):
+        raise FhvError(f"record_size must be 36 or 48, got {record_size}")
+    comp: dict = {}
+    params: dict = {"record_size": record_size}
+    if layout == "DS":
+        if resolution is None:
+            raise FhvError("DS report needs a resolution")
+        w, h = resolution
+        comp["gbuffer"] = w * h * gbuffer_payload_bytes
+        params.update(gbuffer_payload_bytes=gbuffer_payload_bytes, resolution=[w, h])
+    elif layout == "PPFL":
+        if resolution is None:
+            raise FhvError("PPFL report needs a resolution")
+        w, h = resolution
+        capacity = int(w * h * overalloc) if capacity is None else capacity
+        comp["pixel_directory"] = 4 * w * h
+        comp["fragment_pool"] = record_size * capacity
+        params.update(resolution=[w, h], capacity=capacity, overalloc=overalloc)
+    elif layout == "POFL":
+        if levels is None:
+            raise FhvError("POFL report needs levels")
+        if capacity is None:
+            if resolution is None:
+                raise FhvError("POFL report needs a capacity or a resolution")
+            capacity = int(resolution[0] * resolution[1] * overalloc)
+        comp["octree_nodes"] = 4 * sum(8 ** k for k in range(levels + 1))
+        comp["fragment_pool"] = record_size * capacity
+        params.update(levels=levels, capacity=capacity, overalloc=overalloc)
+    elif layout == "POFA":
+        if levels is None or exact_count is None:
+            raise FhvError("POFA report needs levels and an exact count")
+        comp["octree_inner_nodes"] = 4 * sum(8 ** k for k in range(levels))
+        comp["leaf_directory"] = 8 * (8 ** levels)
+        comp["fragment_pool"] = record_size * exact_count
+        params.update(levels=levels, exact_count=exact_count)
+    else:
+        raise FhvError(f"unknown layout {layout!r}")
+    total = sum(comp.values())
+    return {"layout": layout, "params": params, "components": comp, "total_bytes": total,
+            "total_mib": total / (1024.0 * 1024.0)}
+
+
+# ---------------------------------------------------------------------------
+# FHV1 snapshots (fhv/storage.py:725-808), byte-exact with the reference
+
+SNAPSHOT_MAGIC = b"FHV1"
+_HEADER = struct.Struct("<4s4sIIIIQ")
+
+
+def snapshot_bytes(fhv) -> bytes:
+    pool = fhv.pool
+    count = pool.stored_count
+    parts = []
+    if fhv.layout == "PPFL":
+        d = fhv.directory
+        parts += [_HEADER.pack(SNAPSHOT_MAGIC, b"PPFL", 0, d.width, d.height, RECORD_SIZE_PACKED, count),
+                  d.heads.cpu().numpy().astype("<i4").tobytes()]
+    elif fhv.layout in ("POFL", "POFA"):
+        r = fhv.capture_resolution
+        parts.append(_HEADER.pack(SNAPSHOT_MAGIC, fhv.layout.encode(), fhv.levels, r, r, RECORD_SIZE_PACKED, count))
+        if fhv.layout == "POFL":
+            parts.append(fhv.directory.heads.cpu().numpy().astype("<i4").tobytes())
+        else:
+            parts.append(fhv.directory.offsets.cpu().numpy().astype("<u4").tobytes())
+            parts.append(fhv.directory.counts.cpu().numpy().astype("<u4").tobytes())
+        parts.append(fhv.pyramid.data.cpu().numpy().tobytes())
+    else:
+        raise FhvError(f"cannot snapshot layout {fhv.layout!r}")
+    parts.append(pool.to_struct_array().tobytes())
+    return b"".join(parts)
+
+
+def save_snapshot(fhv, path) -> None:
+    with open(path, "wb") as fh:
+        fh.write(snapshot_bytes(fhv))
+
+
+def load_snapshot(path, materials=None, device=None):
+    blob = open(path, "rb").read()
+    if len(blob) < _HEADER.size:
+        raise FhvError("snapshot truncated")
+    magic, layout, levels, w, h, rec, count = _HEADER.unpack_from(blob)
+    if magic != SNAPSHOT_MAGIC:
+        raise FhvError("bad snapshot magic")
+    if rec != RECORD_SIZE_PACKED:
+        raise FhvError(f"unsupported record size {rec}")
+    dev = default_device(device)
+    off = _HEADER.size
+
+    def take(dtype, n):
+        nonlocal off
+        a = np.frombuffer(blob, dtype=dtype, count=n, offset=off).copy()
+        off += a.nbytes
+        return a
+
+    def dev32(a):
+        return torch.from_numpy(a.view(np.int32)).to(dev)
+
+    if layout == b"PPFL":
+        heads = take("<i4", w * h)
+        pool = FragmentPool.from_struct_array(take(RECORD_DTYPE, count), dev)
+        return FhvPpfl(PixelDirectory(w, h, dev32(heads)), pool, h, materials=materials)
+    if layout in (b"POFL", b"POFA"):
+        if layout == b"POFL":
+            heads = take("<i4", 8 ** levels)
+        else:
+            offs = take("<u4", 8 ** levels)
+            cnts = take("<u4", 8 ** levels)
+        pyr = np.concatenate([take(np.uint8, 8 ** k) for k in range(levels)])
+        pool = FragmentPool.from_struct_array(take(RECORD_DTYPE, count), dev)
+        pyramid = OccupancyPyramid(levels, torch.from_numpy(pyr).to(dev))
+        if layout == b"POFL":
+            return FhvPofl(PoflDirectory(levels, dev32(heads)), pyramid, pool, h, materials=materials)
+        return FhvPofa(PofaDirectory(levels, dev32(offs).view(torch.uint32), dev32(cnts).view(torch.uint32)),
+                       pyramid, pool, h, materials=materials)
+    raise FhvError(f"unknown snapshot layout {layout!r}")
