@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark of the FHV hot path on B200: capture + novel-view reconstruction.
+
+Workload (default --config C3): ``scatter1M`` -- 48
+icospheres, 983,040 triangles, synthetic (seeded), captured with the
+NormalSpace strategy at pitch 1/1080 into a POFA octree of depth 8 (two-pass
+count / scan / scatter), then one 1920x1080 perspective novel view
+reconstructed by exact z-tested point splatting.  One step = capture + one
+reconstruct.  ``value`` = fragments captured per second of step time
+(inputs resident in HBM); ``e2e`` = the same through the public API with the
+scene copied host->device (pinned) and the image copied back every step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port, oracle/fhv_oracle.c, threads=1 like the reference's fastest
+setting) on the same workload and prints the same JSON line shape.
+Multi-GPU (torchrun, N>1): each rank runs its own full-size replica of the
+workload (weak scaling, no data-path collective); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+METRIC = "fragments captured/s + novel-view frames/s at 1080p (GB/s vs HBM peak)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--config", default="C3", choices=("C3",))
+    ap.add_argument("--exact-order", action="store_true", help="bit-identical in-leaf order (extra fix-up pass)")
+    ap.add_argument("--packed", action="store_true", help="packed 64-bit splat z-test")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="few steps, no clocks/e2e/cpu (for ncu)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+
+def workload():
+    from paper_2211_15460_b200 import sample_scenes
+    from paper_2211_15460_b200.lights import headlight
+    from paper_2211_15460_b200.raster import CaptureStrategy, RasterConfig
+    from paper_2211_15460_b200.scene import capture_camera, viewpoint_camera
+    scene = sample_scenes.scatter1m()
+    cam = capture_camera(scene, "+z", 1080)
+    cfg = RasterConfig((1920, 1080), RasterConfig.from_camera(cam).projection, extent=1.0)
+    view = viewpoint_camera("+x", (1920, 1080), "perspective")
+    return {"scene": scene, "cfg": cfg, "strategy": CaptureStrategy.normal_space(), "levels": 8, "view": view,
+            "lights": [headlight(view)], "radius": 1.0 / 1080}
+
+
+CONFIG = {"workload": "C3 scatter1M: 983,040 tris, NormalSpace capture pitch 1/1080 -> POFA L=8, "
+                      "+ 1920x1080 perspective splat reconstruct",
+          "triangles": 983040, "capture_res": 1080, "levels": 8, "view": [1920, 1080],
+          "l2_note": "inputs + outputs per step (~0.9 GB) exceed the 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle port)
+
+
+def cpu_run(w):
+    """One full C3 step on the host with the oracle port (threads=1)."""
+    from oracle import oracle as orc
+    t0 = time.perf_counter()
+    vol = orc.pofa_build(w["scene"], w["strategy"], w["cfg"], w["levels"])
+    t1 = time.perf_counter()
+    orc.splat(vol["pool"], vol["next_free"], w["view"], w["lights"], w["radius"], w["scene"].materials)
+    t2 = time.perf_counter()
+    return vol["next_free"], t1 - t0, t2 - t1
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = workload()
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_run(w)
+    tot_s, frags = 0.0, 0
+    for _ in range(args.steps):
+        n, tc, ts = cpu_run(w)
+        tot_s += tc + ts
+        frags += n
+    value = frags / tot_s
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frag/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded icosphere field)", "config": CONFIG,
+            "cpu_baseline": {"value": value, "unit": "frag/s", "cores": 1, "kind": "port",
+                             "sample": "full C3 step per step (POFA capture + 1080p splat), oracle/fhv_oracle.c"},
+            "e2e": {"value": value, "unit": "frag/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_15460_b200 as fhv
+    from paper_2211_15460_b200 import _lib
+    from paper_2211_15460_b200.device import DeviceShading, device_scene
+    from paper_2211_15460_b200.lights import ImageBuffer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    w = workload()
+    scene, cfg, strat, L, view = w["scene"], w["cfg"], w["strategy"], w["levels"], w["view"]
+    ds = device_scene(scene, dev)
+    shading = DeviceShading(scene.materials, w["lights"], dev)
+    W, H = view.resolution
+    img = ImageBuffer(W, H, torch.empty((H, W, 4), dtype=torch.float64, device=dev),
+                      torch.empty((H, W), dtype=torch.float64, device=dev))
+
+    def step():
+        vol = fhv.pofa_build(scene, strat, cfg, L, exact_order=args.exact_order, device=dev)
+        fhv.splat_render(vol.pool, view, w["lights"], w["radius"], scene.materials, out=img, packed=args.packed,
+                         shading=shading)
+        return vol
+
+    for _ in range(args.warmup):
+        vol = step()
+    torch.cuda.synchronize()
+    n_frags = vol.pool.next_free
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region --------------------------------------
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _lib.prof_enable(dev, True)
+    _lib.prof_collect(dev)  # reset
+    launches0 = _lib.launches(dev)
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            vol = step()
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    gpu_launches = _lib.launches(dev) - launches0
+    prof = _lib.prof_collect(dev)
+    _lib.prof_enable(dev, False)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+    ms_step = ms / args.steps
+    value = world * n_frags * args.steps / (ms / 1e3)
+
+    # per-stage shares + roofline of the dominant kernel
+    stage_ms = {k: v[0] / args.steps for k, v in prof.items()}
+    dominant = max(prof, key=lambda k: prof[k][0])
+    T = scene.n_triangles
+    P = W * H
+    algo_bytes = {  # minimal bytes per launch
+        "emit_pofa": 176 * T + 36 * n_frags,
+        "count_leaves": 176 * T + 4 * 8 ** L,
+        "scan_leaves": 8 * 8 ** L + 8 ** (L - 1),
+        "splat_depth": 12 * n_frags + 8 * P,
+        "splat_index": 12 * n_frags + 8 * P,
+        "splat_resolve": 8 * P + 4 * P + 40 * P,
+        "job_setup": 72 + 24 + 80 * T,
+    }
+    peak, peak_kind = peaks()
+    roof = None
+    if dominant in algo_bytes:
+        per_launch_ms = prof[dominant][0] / prof[dominant][1]
+        ach = algo_bytes[dominant] / (per_launch_ms / 1e3) / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", f"ncu_{dominant}.json")
+        if os.path.exists(tf):
+            try:
+                traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": traffic, "algorithmic_bytes": algo_bytes[dominant],
+                "peak_kind": peak_kind, "ms_per_launch": round(per_launch_ms, 4)}
+    capture_ms = sum(v for k, v in stage_ms.items() if not k.startswith("splat"))
+    recon_ms = sum(v for k, v in stage_ms.items() if k.startswith("splat"))
+    step_bytes = (2 * 176 * T + 36 * n_frags + 12 * 8 ** L + (8 ** L - 1) // 7  # POFA capture
+                  + 12 * n_frags + 28 * P + 40 * P)                              # splat + f64 rgba/depth
+    # ---- end to end: pinned host scene in, image out ------------------------
+    if not args.profile_only:
+        pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in
+               (scene.positions, scene.normals, scene.face_normals, scene.material_id.view(np.int32),
+                scene.object_id.view(np.int32))]
+        dst = [ds.pos, ds.vnrm, ds.fnrm, ds.mat.view(torch.int32), ds.obj.view(torch.int32)]
+        out_px = torch.empty((H, W, 4), dtype=torch.float64).pin_memory()
+        out_dp = torch.empty((H, W), dtype=torch.float64).pin_memory()
+        h2d = sum(p.numel() * p.element_size() for p in pin)
+        d2h = out_px.numel() * 8 + out_dp.numel() * 8
+        barrier()
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
+        for _ in range(args.steps):
+            for d, s in zip(dst, pin):
+                d.copy_(s, non_blocking=True)
+            step()
+            out_px.copy_(img.pixels, non_blocking=True)
+            out_dp.copy_(img.depth, non_blocking=True)
+        e3.record(stream)
+        barrier()
+        ms_e2e = e2.elapsed_time(e3)
+        t2 = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t2.item())
+        e2e = {"value": world * n_frags * args.steps / (ms_e2e / 1e3), "unit": "frag/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps}
+    else:
+        e2e = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
+        n, tc, ts = cpu_run(w)
+        cpu = {"value": n / (tc + ts), "unit": "frag/s", "cores": 1, "kind": "port",
+               "sample": f"one full C3 step on the host (oracle/fhv_oracle.c): capture {tc:.2f} s + splat {ts:.2f} s",
+               "capture_s": tc, "splat_s": ts}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "frag/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded icosphere field, no dataset)",
+                "config": dict(CONFIG, fragments=n_frags, parallelism=f"replicas{world}" if world > 1 else "single",
+                               exact_order=bool(args.exact_order), splat="packed" if args.packed else "exact"),
+                "novel_view_fps": 1e3 / recon_ms if recon_ms else None,
+                "capture_frag_per_s": n_frags / (capture_ms / 1e3) if capture_ms else None,
+                "step_gbs": step_bytes / (ms_step / 1e3) / 1e9, "step_bytes": step_bytes,
+                "stage_ms": {k: round(v, 4) for k, v in sorted(stage_ms.items(), key=lambda kv: -kv[1])},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

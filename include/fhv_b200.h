@@ -142,6 +142,14 @@ void fhv_ctx_destroy(fhv_ctx *ctx);
 /* kernels launched by this context since creation (for launch accounting) */
 int64_t fhv_ctx_launches(const fhv_ctx *ctx);
 
+/* per-kernel CUDA-event timing on the launching stream (off by default).
+   fhv_prof_collect synchronises the recorded events, writes accumulated
+   milliseconds and launch counts per stage (up to n entries), resets the
+   accumulators and returns the number of stages. */
+int fhv_prof_enable(fhv_ctx *ctx, int on);
+int fhv_prof_collect(fhv_ctx *ctx, double *ms, int64_t *count, int n);
+const char *fhv_prof_stage_name(int stage);
+
 /* Every fragment in reference emission order (job, y, x), f64 attributes.
    max_out bounds the outputs; *n_out receives the total.  Synchronises. */
 int fhv_capture_list(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg,

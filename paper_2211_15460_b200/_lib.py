@@ -56,6 +56,9 @@ _SIGS = {
     "fhv_ctx_create": (c_vp, []),
     "fhv_ctx_destroy": (None, [c_vp]),
     "fhv_ctx_launches": (c_i64, [c_vp]),
+    "fhv_prof_enable": (ctypes.c_int, [c_vp, ctypes.c_int]),
+    "fhv_prof_collect": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int]),
+    "fhv_prof_stage_name": (ctypes.c_char_p, [ctypes.c_int]),
     "fhv_capture_list": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                         _P(c_i64), c_vp]),
     "fhv_build_ppfl": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i64, _P(Pool), c_vp, c_i32, _P(c_i64),
@@ -118,6 +121,24 @@ def ctx(device: torch.device):
 
 def launches(device: torch.device) -> int:
     return int(load().fhv_ctx_launches(ctx(device)))
+
+
+def prof_enable(device: torch.device, on: bool = True) -> None:
+    load().fhv_prof_enable(ctx(device), 1 if on else 0)
+
+
+def prof_collect(device: torch.device) -> dict:
+    """{stage: (total_ms, launches)} since the last collect (syncs)."""
+    import numpy as np
+    lib = load()
+    ms = np.zeros(64)
+    cnt = np.zeros(64, dtype=np.int64)
+    n = lib.fhv_prof_collect(ctx(device), ms.ctypes.data, cnt.ctypes.data, 64)
+    out = {}
+    for i in range(n):
+        if cnt[i]:
+            out[lib.fhv_prof_stage_name(i).decode()] = (float(ms[i]), int(cnt[i]))
+    return out
 
 
 def stream_ptr(device: torch.device):

@@ -50,11 +50,74 @@ int sync_control(fhv_ctx* ctx, cudaStream_t s) {
   return ctx->ctl_host->status;
 }
 
+static cudaEvent_t get_event(fhv_ctx* ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+LaunchScope::LaunchScope(fhv_ctx* c, int st, cudaStream_t stream) : ctx(c), stage(st), s(stream) {
+  ctx->launches++;
+  if (ctx->prof) {
+    e0 = get_event(ctx);
+    cudaEventRecord(e0, s);
+  }
+}
+
+LaunchScope::~LaunchScope() {
+  if (ctx->prof && e0) {
+    cudaEvent_t e1 = get_event(ctx);
+    cudaEventRecord(e1, s);
+    ctx->pending.push_back({stage, e0, e1});
+  }
+}
+
+static const char* kStageNames[kNumStages] = {
+    "job_setup", "scan", "item_expand", "count", "count_leaves", "emit_list", "emit_ppfl", "emit_pofl",
+    "emit_pofa", "chain_order", "leaf_order", "scan_leaves", "pyramid", "splat_depth", "splat_index",
+    "splat_resolve", "raycast", "face_normals"};
+
 }  // namespace fhv
 
 using namespace fhv;
 
 extern "C" const char* fhv_version(void) { return "fhv_b200 0.1 sm_100a"; }
+
+extern "C" int fhv_prof_enable(fhv_ctx* ctx, int on) {
+  if (!ctx) return FHV_BAD_ARGS;
+  ctx->prof = on != 0;
+  return FHV_OK;
+}
+
+extern "C" const char* fhv_prof_stage_name(int stage) {
+  return (stage >= 0 && stage < kNumStages) ? kStageNames[stage] : nullptr;
+}
+
+extern "C" int fhv_prof_collect(fhv_ctx* ctx, double* ms, int64_t* count, int n) {
+  if (!ctx) return -FHV_BAD_ARGS;
+  for (auto& p : ctx->pending) {
+    cudaEventSynchronize(p.e1);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, p.e0, p.e1);
+    ctx->stage_ms[p.stage] += t;
+    ctx->stage_count[p.stage] += 1;
+    ctx->event_pool.push_back(p.e0);
+    ctx->event_pool.push_back(p.e1);
+  }
+  ctx->pending.clear();
+  for (int i = 0; i < kNumStages && i < n; ++i) {
+    if (ms) ms[i] = ctx->stage_ms[i];
+    if (count) count[i] = ctx->stage_count[i];
+    ctx->stage_ms[i] = 0.0;
+    ctx->stage_count[i] = 0;
+  }
+  return kNumStages;
+}
 
 extern "C" fhv_ctx* fhv_ctx_create(void) {
   fhv_ctx* ctx = new fhv_ctx();
@@ -78,6 +141,11 @@ extern "C" void fhv_ctx_destroy(fhv_ctx* ctx) {
     if (b.ptr) cudaFree(b.ptr);
   cudaFree(ctx->ctl);
   cudaFreeHost(ctx->ctl_host);
+  for (auto& p : ctx->pending) {
+    cudaEventDestroy(p.e0);
+    cudaEventDestroy(p.e1);
+  }
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
   delete ctx;
 }
 

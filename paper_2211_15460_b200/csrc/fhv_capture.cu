@@ -684,8 +684,10 @@ int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s) {
   uint32_t* job_items = (uint32_t*)scratch(ctx, kJobItems, (size_t)p.n_jobs * 4);
   auto* job_item_off = (unsigned long long*)scratch(ctx, kJobItemOff, (size_t)p.n_jobs * 8);
   if (!jobs || !job_items || !job_item_off) return FHV_NOMEM;
-  k_job_setup<<<grid_for(p.n_jobs, 128), 128, 0, s>>>(p, jobs, job_items, &ctx->ctl->status);
-  ctx->launches++;
+  {
+    LaunchScope L_(ctx, kStJobSetup, s);
+    k_job_setup<<<grid_for(p.n_jobs, 128), 128, 0, s>>>(p, jobs, job_items, &ctx->ctl->status);
+  }
   if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
   if ((rc = scan_u32_to_u64(ctx, job_items, job_item_off, p.n_jobs, s))) return rc;
   if ((rc = sync_control(ctx, s))) return rc;
@@ -696,8 +698,10 @@ int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s) {
   uint32_t* item_job = (uint32_t*)scratch(ctx, kItemJob, (size_t)n_items * 4);
   uint32_t* item_p0 = (uint32_t*)scratch(ctx, kItemP0, (size_t)n_items * 4);
   if (!item_job || !item_p0) return FHV_NOMEM;
-  k_item_expand<<<grid_for(p.n_jobs * 32, 256), 256, 0, s>>>(p.n_jobs, job_items, job_item_off, item_job, item_p0);
-  ctx->launches++;
+  {
+    LaunchScope L_(ctx, kStItemExpand, s);
+    k_item_expand<<<grid_for(p.n_jobs * 32, 256), 256, 0, s>>>(p.n_jobs, job_items, job_item_off, item_job, item_p0);
+  }
   return check_cuda(ctx, cudaGetLastError());
 }
 
@@ -711,11 +715,13 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
     const JobSetup* jobs = (const JobSetup*)ctx->bufs[kJobs].ptr;
     const uint32_t* ij = (const uint32_t*)ctx->bufs[kItemJob].ptr;
     const uint32_t* ip = (const uint32_t*)ctx->bufs[kItemP0].ptr;
-    if (leaves)
-      k_count<true><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, n, item_cnt, levels, leaf_counts, &ctx->ctl->status);
-    else
-      k_count<false><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, n, item_cnt, levels, nullptr, &ctx->ctl->status);
-    ctx->launches++;
+    {
+      LaunchScope L_(ctx, leaves ? kStCountLeaves : kStCount, s);
+      if (leaves)
+        k_count<true><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, n, item_cnt, levels, leaf_counts, &ctx->ctl->status);
+      else
+        k_count<false><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, n, item_cnt, levels, nullptr, &ctx->ctl->status);
+    }
     int rc = check_cuda(ctx, cudaGetLastError());
     if (rc) return rc;
   }
@@ -730,11 +736,13 @@ int emit(fhv_ctx* ctx, const CaptureParams& p, const EmitOut& o, bool atomic_all
   const uint32_t* ij = (const uint32_t*)ctx->bufs[kItemJob].ptr;
   const uint32_t* ip = (const uint32_t*)ctx->bufs[kItemP0].ptr;
   const auto* io = (const unsigned long long*)ctx->bufs[kItemOff].ptr;
-  if (atomic_alloc)
-    k_emit<kMode, true><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, io, n, o, ctx->ctl);
-  else
-    k_emit<kMode, false><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, io, n, o, ctx->ctl);
-  ctx->launches++;
+  {
+    LaunchScope L_(ctx, kStEmitList + kMode, s);
+    if (atomic_alloc)
+      k_emit<kMode, true><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, io, n, o, ctx->ctl);
+    else
+      k_emit<kMode, false><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, io, n, o, ctx->ctl);
+  }
   return check_cuda(ctx, cudaGetLastError());
 }
 
@@ -758,8 +766,10 @@ int chain_order(fhv_ctx* ctx, int32_t* heads, int32_t* prev, long long n_keys, l
   if (!spill) return FHV_NOMEM;
   int rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->spare[0], 0, 8, s));
   if (rc) return rc;
-  k_chain_order<<<grid_for(n_keys, 128), 128, 0, s>>>(heads, prev, n_keys, spill, &ctx->ctl->spare[0]);
-  ctx->launches++;
+  {
+    LaunchScope L_(ctx, kStChainOrder, s);
+    k_chain_order<<<grid_for(n_keys, 128), 128, 0, s>>>(heads, prev, n_keys, spill, &ctx->ctl->spare[0]);
+  }
   return check_cuda(ctx, cudaGetLastError());
 }
 
@@ -893,9 +903,11 @@ extern "C" int fhv_pofa_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_
   o.flags = flags;
   if ((rc = emit<kPofa>(ctx, p, o, false, s))) return rc;
   if (flags & FHV_EXACT_ORDER) {
-    k_leaf_order<<<grid_for(n_leaves, 128, 32), 128, 0, s>>>(offsets, counts, n_leaves, pool->pos, pool->nrm,
+    {
+      LaunchScope L_(ctx, kStLeafOrder, s);
+      k_leaf_order<<<grid_for(n_leaves, 128, 32), 128, 0, s>>>(offsets, counts, n_leaves, pool->pos, pool->nrm,
                                                              pool->mat, pool->obj, pool->prev);
-    ctx->launches++;
+    }
     if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
   }
   if ((rc = sync_control(ctx, s))) return rc;
@@ -908,7 +920,9 @@ extern "C" int fhv_pofa_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_
 extern "C" int fhv_face_normals(fhv_ctx* ctx, int64_t n_tri, const double* pos, double* fnrm, void* stream) {
   if (!ctx || n_tri < 0 || (n_tri && (!pos || !fnrm))) return FHV_BAD_ARGS;
   if (n_tri == 0) return FHV_OK;
-  k_face_normals<<<grid_for(n_tri, 256), 256, 0, (cudaStream_t)stream>>>(n_tri, pos, fnrm);
-  ctx->launches++;
+  {
+    LaunchScope L_(ctx, kStFaceNormals, (cudaStream_t)stream);
+    k_face_normals<<<grid_for(n_tri, 256), 256, 0, (cudaStream_t)stream>>>(n_tri, pos, fnrm);
+  }
   return check_cuda(ctx, cudaGetLastError());
 }

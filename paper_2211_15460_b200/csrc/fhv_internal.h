@@ -34,8 +34,26 @@ struct DevBuf {
 
 }  // namespace fhv
 
+namespace fhv {
+// profiled stages (one per kernel family); names in fhv_abi.cu
+enum Stage {
+  kStJobSetup = 0, kStScan, kStItemExpand, kStCount, kStCountLeaves, kStEmitList, kStEmitPpfl, kStEmitPofl,
+  kStEmitPofa, kStChainOrder, kStLeafOrder, kStScanLeaves, kStPyramid, kStSplatDepth, kStSplatIndex,
+  kStSplatResolve, kStRaycast, kStFaceNormals, kNumStages
+};
+struct PendingEvent {
+  int stage;
+  cudaEvent_t e0, e1;
+};
+}  // namespace fhv
+
 struct fhv_ctx {
   int device = 0;
+  bool prof = false;
+  std::vector<fhv::PendingEvent> pending;
+  std::vector<cudaEvent_t> event_pool;
+  double stage_ms[fhv::kNumStages] = {};
+  long long stage_count[fhv::kNumStages] = {};
   fhv::DevBuf bufs[24];
   fhv::Control* ctl = nullptr;       // device
   fhv::Control* ctl_host = nullptr;  // pinned mirror
@@ -52,6 +70,17 @@ namespace fhv {
 enum BufId {
   kJobs = 0, kJobItems, kJobItemOff, kItemJob, kItemP0, kItemCnt, kItemOff, kScanStatus,
   kCursors, kChainScratch, kSplatKey, kSplatWin, kSplatBox, kRays, kTmp0, kTmp1, kNumBufs
+};
+
+// Counts a launch and, when profiling is on, brackets it with CUDA events on
+// the launching stream:  { LaunchScope L(ctx, kStCount, s); k<<<...>>>(); }
+struct LaunchScope {
+  fhv_ctx* ctx;
+  int stage;
+  cudaStream_t s;
+  cudaEvent_t e0 = nullptr;
+  LaunchScope(fhv_ctx* c, int st, cudaStream_t stream);
+  ~LaunchScope();
 };
 
 // grow-only scratch; returns nullptr on allocation failure

@@ -429,8 +429,10 @@ inline int grid_for(long long n, int block, int per_sm = 16) {
 
 int launch(fhv_ctx* ctx, RayParams& x, void* stream) {
   if (x.end <= x.start) return FHV_OK;
-  k_raycast<<<grid_for(x.end - x.start, 128), 128, 0, (cudaStream_t)stream>>>(x);
-  ctx->launches++;
+  {
+    LaunchScope L_(ctx, kStRaycast, (cudaStream_t)stream);
+    k_raycast<<<grid_for(x.end - x.start, 128), 128, 0, (cudaStream_t)stream>>>(x);
+  }
   return check_cuda(ctx, cudaGetLastError());
 }
 

@@ -203,8 +203,10 @@ int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, i
   if (rc) return rc;
   rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->tile_counter, 0, sizeof(unsigned), s));
   if (rc) return rc;
-  k_scan_u32_u64<B, I><<<tiles, B, 0, s>>>(in, out, n, st, ctx->ctl, tiles);
-  ctx->launches++;
+  {
+    LaunchScope L_(ctx, kStScan, s);
+    k_scan_u32_u64<B, I><<<tiles, B, 0, s>>>(in, out, n, st, ctx->ctl, tiles);
+  }
   return check_cuda(ctx, cudaGetLastError());
 }
 
@@ -214,8 +216,10 @@ int pyramid_upper_levels(fhv_ctx* ctx, uint8_t* pyramid, int levels, cudaStream_
     uint8_t* dst = pyramid + pyr_level_offset(k);
     const uint8_t* src = pyramid + pyr_level_offset(k + 1);
     // level k+1 starts at (8^(k+1)-1)/7, not 8-aligned in general -> byte loads
-    k_pyramid_up_small<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n);
-    ctx->launches++;
+    {
+      LaunchScope L_(ctx, kStPyramid, s);
+      k_pyramid_up_small<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n);
+    }
   }
   return check_cuda(ctx, cudaGetLastError());
 }
@@ -231,9 +235,11 @@ int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offs
   if (rc) return rc;
   rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->tile_counter, 0, sizeof(unsigned), s));
   if (rc) return rc;
-  k_scan_leaves<B><<<tiles, B, 0, s>>>(reinterpret_cast<const uint4*>(counts), reinterpret_cast<uint4*>(offsets),
+  {
+    LaunchScope L_(ctx, kStScanLeaves, s);
+    k_scan_leaves<B><<<tiles, B, 0, s>>>(reinterpret_cast<const uint4*>(counts), reinterpret_cast<uint4*>(offsets),
                                        pyramid + pyr_level_offset(levels - 1), n_nodes, st, ctx->ctl, tiles);
-  ctx->launches++;
+  }
   rc = check_cuda(ctx, cudaGetLastError());
   if (rc) return rc;
   return pyramid_upper_levels(ctx, pyramid, levels, s);
@@ -241,9 +247,11 @@ int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offs
 
 int pyramid_from_heads(fhv_ctx* ctx, const int32_t* heads, uint8_t* pyramid, int levels, cudaStream_t s) {
   const int64_t n_nodes = 1ll << (3 * (levels - 1));
-  k_pyramid_heads<<<grid_for(n_nodes, 256), 256, 0, s>>>(reinterpret_cast<const int4*>(heads),
+  {
+    LaunchScope L_(ctx, kStPyramid, s);
+    k_pyramid_heads<<<grid_for(n_nodes, 256), 256, 0, s>>>(reinterpret_cast<const int4*>(heads),
                                                          pyramid + pyr_level_offset(levels - 1), n_nodes);
-  ctx->launches++;
+  }
   int rc = check_cuda(ctx, cudaGetLastError());
   if (rc) return rc;
   return pyramid_upper_levels(ctx, pyramid, levels, s);

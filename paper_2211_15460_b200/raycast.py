@@ -108,7 +108,8 @@ def _volume(fhv) -> "_lib.Volume":
 
 def render_raycast(fhv, camera: Camera, lights, cfg: RaycastConfig | None = None, materials=None,
                    background=(0.0, 0.0, 0.0, 0.0), threads: int = 1, collect_ids: bool = False, *,
-                   rows: tuple | None = None, out: ImageBuffer | None = None, sync: bool = True):
+                   rows: tuple | None = None, out: ImageBuffer | None = None, sync: bool = True,
+                   shading: DeviceShading | None = None):
     """Ray-cast every pixel; returns (ImageBuffer, RaycastStats[, ids]) with
     CUDA tensors.  ``threads`` is accepted and ignored.  ``rows=(r0, r1)``
     renders a row band only (multi-GPU slabs)."""
@@ -126,7 +127,8 @@ def render_raycast(fhv, camera: Camera, lights, cfg: RaycastConfig | None = None
         out = ImageBuffer(w, h, px, torch.full((h, w), float("inf"), dtype=torch.float64, device=dev))
     ids = torch.full((h, w), -1, dtype=torch.int32, device=dev) if collect_ids else None
     counters = torch.zeros(4, dtype=torch.int64, device=dev)
-    shading = DeviceShading(materials, lights, dev)
+    if shading is None:
+        shading = DeviceShading(materials, lights, dev)
     cam = host_f64(camera.scalars())
     bg = host_f64(background)
     r0, r1 = (0, h) if rows is None else rows

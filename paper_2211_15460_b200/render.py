@@ -22,14 +22,16 @@ __all__ = ["GBuffer", "ImageBuffer", "Light", "composite_over", "front_to_back_a
 
 def splat_render(pool, camera: Camera, lights, splat_radius_world: float, materials,
                  background=(0.0, 0.0, 0.0, 0.0), id_buffer: GBuffer | None = None, *,
-                 packed: bool = False, n: int | None = None, out: ImageBuffer | None = None) -> ImageBuffer:
+                 packed: bool = False, n: int | None = None, out: ImageBuffer | None = None,
+                 shading: DeviceShading | None = None) -> ImageBuffer:
     """Z-tested point splatting of a fragment pool into a novel view.
 
     Returns an ImageBuffer whose ``pixels`` (h, w, 4) and ``depth`` (h, w)
     are float64 CUDA tensors.  ``id_buffer`` (GBuffer of CUDA tensors, e.g.
     from :func:`device_gbuffer`) receives the winners' attributes.
     ``packed=True`` selects the single 64-bit (f32 depth | index) atomicMin
-    variant.  ``out`` reuses preallocated image tensors.
+    variant.  ``out`` reuses preallocated image tensors; ``shading`` a
+    prebuilt DeviceShading (materials + lights already on the device).
     """
     if splat_radius_world <= 0.0:
         raise SceneError("splat radius must be > 0")
@@ -39,7 +41,8 @@ def splat_render(pool, camera: Camera, lights, splat_radius_world: float, materi
         out = ImageBuffer(w, h, torch.empty((h, w, 4), dtype=torch.float64, device=dev),
                           torch.empty((h, w), dtype=torch.float64, device=dev))
     count = pool.stored_count if n is None else int(n)
-    shading = DeviceShading(materials, lights, dev)
+    if shading is None:
+        shading = DeviceShading(materials, lights, dev)
     gb = None
     if id_buffer is not None:
         gb = _lib.GBuf(_lib.ptr(id_buffer.position), _lib.ptr(id_buffer.normal), _lib.ptr(id_buffer.material_id),

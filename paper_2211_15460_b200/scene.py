@@ -226,7 +226,10 @@ class Scene:
 
     @property
     def n_objects(self) -> int:
-        return int(len(np.unique(self.object_id)))
+        n = self.__dict__.get("_n_objects")
+        if n is None:
+            n = self.__dict__["_n_objects"] = int(len(np.unique(self.object_id)))
+        return n
 
 
 class Camera:

@@ -143,7 +143,7 @@ class FragmentPool:
     (fhv/storage.py:188-248).  ``next_free`` keeps counting past capacity;
     records beyond it are dropped and ``overflowed`` is set."""
 
-    def __init__(self, capacity: int, device=None):
+    def __init__(self, capacity: int, device=None, fill_prev: bool = True):
         if capacity < 0:
             raise FhvError("capacity must be >= 0")
         dev = default_device(device)
@@ -153,7 +153,8 @@ class FragmentPool:
         self.normal = torch.empty((capacity, 3), dtype=torch.float32, device=dev)
         self.material_id = torch.empty(capacity, dtype=torch.uint32, device=dev)
         self.object_id = torch.empty(capacity, dtype=torch.uint32, device=dev)
-        self.prev_index = torch.full((capacity,), -1, dtype=torch.int32, device=dev)
+        self.prev_index = (torch.full((capacity,), -1, dtype=torch.int32, device=dev) if fill_prev
+                           else torch.empty(capacity, dtype=torch.int32, device=dev))
         self.next_free = 0
         self.overflowed = False
 
@@ -409,7 +410,7 @@ def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     st = _lib.stream_ptr(dev)
     rc = lib.fhv_pofa_count(cx, tris, c, levels, _lib.ptr(counts), _lib.ptr(offsets), _lib.ptr(pyr.data), total, st)
     _lib.check(rc, "pofa_build pass 1")
-    pool = FragmentPool(int(total.value), dev)
+    pool = FragmentPool(int(total.value), dev, fill_prev=False)  # pass 2 writes every prev_index
     p = pool.struct()
     rc = lib.fhv_pofa_scatter(cx, tris, c, levels, _lib.ptr(counts), _lib.ptr(offsets), p,
                               _lib.FHV_EXACT_ORDER if exact_order else 0, st)
