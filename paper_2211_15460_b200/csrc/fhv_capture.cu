@@ -235,17 +235,37 @@ __global__ void k_job_setup(CaptureParams p, JobSetup* __restrict__ jobs, uint32
   }
 }
 
-// one warp per job writes its work items
-__global__ void k_item_expand(long long n_jobs, const uint32_t* __restrict__ job_items,
-                              const unsigned long long* __restrict__ job_item_off, uint32_t* __restrict__ item_job,
-                              uint32_t* __restrict__ item_p0) {
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; j < n_jobs; j += warps) {
-    const uint32_t n = job_items[j];
-    const unsigned long long base = job_item_off[j];
-    for (uint32_t k = lane_id(); k < n; k += 32) {
-      item_job[base + k] = (uint32_t)j;
-      item_p0[base + k] = k * kItemPix;
+// work items of each job: a lane per job writes small jobs' items itself;
+// jobs with many items (large triangles) are written by the whole warp, one
+// such job at a time (ballot loop), so both 1-item and 10^4-item jobs stay
+// coalesced
+constexpr uint32_t kExpandSmall = 4;
+
+__global__ void __launch_bounds__(256) k_item_expand(long long n_jobs, const uint32_t* __restrict__ job_items,
+                                                     const unsigned long long* __restrict__ job_item_off,
+                                                     uint32_t* __restrict__ item_job, uint32_t* __restrict__ item_p0) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); j0 < n_jobs; j0 += stride) {
+    const long long j = j0 + lane_id();
+    const uint32_t n = j < n_jobs ? job_items[j] : 0u;
+    const unsigned long long base = j < n_jobs ? job_item_off[j] : 0ull;
+    if (n <= kExpandSmall) {
+      for (uint32_t k = 0; k < n; ++k) {
+        item_job[base + k] = (uint32_t)j;
+        item_p0[base + k] = k * kItemPix;
+      }
+    }
+    unsigned big = __ballot_sync(0xffffffffu, n > kExpandSmall);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t bn = __shfl_sync(0xffffffffu, n, src);
+      const unsigned long long bb = __shfl_sync(0xffffffffu, base, src);
+      const uint32_t bj = (uint32_t)(j0 + src);
+      for (uint32_t k = lane_id(); k < bn; k += 32) {
+        item_job[bb + k] = bj;
+        item_p0[bb + k] = k * kItemPix;
+      }
     }
   }
 }
@@ -700,7 +720,7 @@ int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s) {
   if (!item_job || !item_p0) return FHV_NOMEM;
   {
     LaunchScope L_(ctx, kStItemExpand, s);
-    k_item_expand<<<grid_for(p.n_jobs * 32, 256), 256, 0, s>>>(p.n_jobs, job_items, job_item_off, item_job, item_p0);
+    k_item_expand<<<grid_for(p.n_jobs, 256), 256, 0, s>>>(p.n_jobs, job_items, job_item_off, item_job, item_p0);
   }
   return check_cuda(ctx, cudaGetLastError());
 }

@@ -57,23 +57,34 @@ __device__ __forceinline__ uint64_t block_excl_scan(uint64_t x, uint64_t* total)
   return warp_tot[warp] + inc - x;
 }
 
-// decoupled look-back: thread 0 resolves the exclusive prefix of `tile`
-__device__ __forceinline__ uint64_t lookback(uint64_t* status, unsigned tile, uint64_t agg) {
+// decoupled look-back, warp-parallel: warp 0 of the tile resolves the
+// exclusive prefix of `tile`, inspecting 32 predecessors per step.  Returns
+// the prefix in every lane of warp 0.
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, unsigned tile, uint64_t agg) {
+  const unsigned lane = threadIdx.x & 31u;
   if (tile == 0) {
-    st_volatile(&status[0], kFlagPre | agg);
+    if (lane == 0) st_volatile(&status[0], kFlagPre | agg);
     return 0;
   }
-  st_volatile(&status[tile], kFlagAgg | agg);
+  if (lane == 0) st_volatile(&status[tile], kFlagAgg | agg);
   uint64_t prefix = 0;
-  int k = (int)tile - 1;
+  long long base = (long long)tile - 1;
   while (true) {
-    uint64_t s;
-    do { s = ld_volatile(&status[k]); } while ((s & ~kValMask) == 0);
-    prefix += s & kValMask;
-    if ((s & ~kValMask) == kFlagPre) break;
-    --k;
+    const long long k = base - (long long)lane;
+    uint64_t s = kFlagPre;  // before tile 0: an inclusive prefix of 0
+    if (k >= 0) {
+      do { s = ld_volatile(&status[k]); } while ((s & ~kValMask) == 0);
+    }
+    const unsigned pre = __ballot_sync(0xffffffffu, (s & ~kValMask) == kFlagPre);
+    const unsigned stop = pre ? (unsigned)(__ffs(pre) - 1) : 31u;
+    uint64_t v = lane <= stop ? (s & kValMask) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    prefix += v;
+    if (pre) break;
+    base -= 32;
   }
-  st_volatile(&status[tile], kFlagPre | ((prefix + agg) & kValMask));
+  if (lane == 0) st_volatile(&status[tile], kFlagPre | ((prefix + agg) & kValMask));
   return prefix;
 }
 
@@ -95,7 +106,10 @@ __global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restri
     sum += v[i];
   }
   const uint64_t excl = block_excl_scan<BLOCK>(sum, &total_s);
-  if (threadIdx.x == 0) prefix_s = lookback(status, tile, total_s);
+  if (threadIdx.x < 32) {
+    const uint64_t pf = lookback_warp(status, tile, total_s);
+    if (threadIdx.x == 0) prefix_s = pf;
+  }
   __syncthreads();
   uint64_t run = prefix_s + excl;
 #pragma unroll
@@ -131,7 +145,10 @@ __global__ void __launch_bounds__(BLOCK) k_scan_leaves(const uint4* __restrict__
     mask |= (v[i] != 0u ? 1u : 0u) << i;
   }
   const uint64_t excl = block_excl_scan<BLOCK>(sum, &total_s);
-  if (threadIdx.x == 0) prefix_s = lookback(status, tile, total_s);
+  if (threadIdx.x < 32) {
+    const uint64_t pf = lookback_warp(status, tile, total_s);
+    if (threadIdx.x == 0) prefix_s = pf;
+  }
   __syncthreads();
   if (node < n_nodes) {
     uint64_t run = prefix_s + excl;
@@ -146,6 +163,152 @@ __global__ void __launch_bounds__(BLOCK) k_scan_leaves(const uint4* __restrict__
     last_level[node] = (uint8_t)mask;
   }
   if (threadIdx.x == 0 && tile == n_tiles - 1) ctl->scan_total = prefix_s + total_s;
+}
+
+// Directory tiles for L >= 4: one CTA = one level-(L-4) subtree = 4096
+// leaves (4 warps x 4 iterations x 32 lanes x 8 leaves).  A lane owns one
+// level-(L-1) node (8 consecutive leaves, two 16-B loads) per iteration, so
+// the tile writes pyramid levels L-1 (lane masks), L-2 (warp ballots), L-3
+// (ballot pairs) and L-4 (the tile root) from registers, and for POFA also
+// offsets = exclusive scan of counts (warp running scan + tile look-back).
+// The last tile to finish builds the remaining levels L-5..0 from the
+// level-(L-4) bytes.  One pass over the directory: 8 B/leaf (POFA) or
+// 4 B/leaf (POFL heads) of HBM plus 8^L/7 pyramid bytes.
+constexpr int kDirWarps = 4, kDirIters = 4;
+constexpr int kDirThreads = 32 * kDirWarps;
+constexpr long long kDirTileLeaves = 8LL * 32 * kDirWarps * kDirIters;  // 4096 = 8^4
+
+template <bool kScan>
+__global__ void __launch_bounds__(kDirThreads) k_dir_tiles(const uint4* __restrict__ counts,
+                                                           uint4* __restrict__ offsets,
+                                                           const int4* __restrict__ heads, uint8_t* __restrict__ pyr,
+                                                           int levels, uint64_t* status, Control* ctl,
+                                                           unsigned n_tiles) {
+  __shared__ unsigned tile_s;
+  __shared__ uint64_t warp_tot[kDirWarps];
+  __shared__ uint64_t prefix_s;
+  __shared__ uint8_t l3[2 * kDirWarps];
+  __shared__ int last_s;
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) tile_s = kScan ? atomicAdd(&ctl->tile_counter, 1u) : blockIdx.x;
+  __syncthreads();
+  const unsigned tile = tile_s;
+  uint8_t* lv1 = pyr + pyr_level_offset(levels - 1);
+  uint8_t* lv2 = pyr + pyr_level_offset(levels - 2);
+  uint8_t* lv3 = pyr + pyr_level_offset(levels - 3);
+  uint8_t* lv4 = pyr + pyr_level_offset(levels - 4);
+  const long long node0 = (long long)tile * (kDirTileLeaves / 8) + (long long)warp * (32 * kDirIters);
+  uint32_t c[kDirIters][8];
+  unsigned ballots[kDirIters];
+#pragma unroll
+  for (int i = 0; i < kDirIters; ++i) {
+    const long long n = node0 + i * 32 + lane;
+    unsigned m = 0;
+    if (kScan) {
+      const uint4 a = __ldg(&counts[2 * n]), b = __ldg(&counts[2 * n + 1]);
+      c[i][0] = a.x; c[i][1] = a.y; c[i][2] = a.z; c[i][3] = a.w;
+      c[i][4] = b.x; c[i][5] = b.y; c[i][6] = b.z; c[i][7] = b.w;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m |= (c[i][k] != 0u ? 1u : 0u) << k;
+    } else {
+      const int4 a = __ldcs(&heads[2 * n]), b = __ldcs(&heads[2 * n + 1]);
+      const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m |= (v[k] >= 0 ? 1u : 0u) << k;
+    }
+    lv1[n] = (uint8_t)m;
+    ballots[i] = __ballot_sync(0xffffffffu, m != 0);
+  }
+  // level L-2: lane g < 4 of iteration i writes node (node0 + 32 i) / 8 + g
+#pragma unroll
+  for (int i = 0; i < kDirIters; ++i)
+    if (lane < 4) lv2[(node0 + 32 * i) / 8 + lane] = (uint8_t)((ballots[i] >> (8 * lane)) & 0xffu);
+  // level L-3: iterations (2j, 2j+1) -> one node; bit g = L-2 node g non-empty
+  if (lane < kDirIters / 2) {
+    const unsigned b0 = ballots[0], b1 = ballots[1], b2 = ballots[2], b3 = ballots[3];
+    const unsigned lo = lane == 0 ? b0 : b2, hi = lane == 0 ? b1 : b3;
+    unsigned m = 0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      m |= (((lo >> (8 * g)) & 0xffu) != 0 ? 1u : 0u) << g;
+      m |= (((hi >> (8 * g)) & 0xffu) != 0 ? 1u : 0u) << (g + 4);
+    }
+    lv3[node0 / 64 + lane] = (uint8_t)m;
+    l3[2 * warp + lane] = (uint8_t)m;
+  }
+  if (kScan) {
+    uint64_t excl[kDirIters];
+    uint64_t carry = 0;
+#pragma unroll
+    for (int i = 0; i < kDirIters; ++i) {
+      uint64_t sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += c[i][k];
+      uint64_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (unsigned)o) inc += y;
+      }
+      excl[i] = carry + inc - sum;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) warp_tot[warp] = carry;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t t = 0;
+#pragma unroll
+      for (int w = 0; w < kDirWarps; ++w) t += warp_tot[w];
+      const uint64_t pf = lookback_warp(status, tile, t);
+      if (lane == 0) {
+        prefix_s = pf;
+        if (tile == n_tiles - 1) ctl->scan_total = pf + t;
+      }
+    }
+    __syncthreads();
+    uint64_t wbase = prefix_s;
+    for (unsigned w = 0; w < warp; ++w) wbase += warp_tot[w];
+#pragma unroll
+    for (int i = 0; i < kDirIters; ++i) {
+      const long long n = node0 + i * 32 + lane;
+      uint64_t run = wbase + excl[i];
+      uint32_t o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        o[k] = (uint32_t)run;
+        run += c[i][k];
+      }
+      __stcs(&offsets[2 * n], make_uint4(o[0], o[1], o[2], o[3]));
+      __stcs(&offsets[2 * n + 1], make_uint4(o[4], o[5], o[6], o[7]));
+    }
+  } else {
+    __syncthreads();
+  }
+  // tile root (level L-4)
+  if (threadIdx.x == 0) {
+    unsigned m = 0;
+#pragma unroll
+    for (int k = 0; k < 2 * kDirWarps; ++k) m |= (l3[k] != 0 ? 1u : 0u) << k;
+    lv4[tile] = (uint8_t)m;
+    __threadfence();
+    const unsigned long long done = atomicAdd(&ctl->spare[1], 1ull);
+    last_s = done == (unsigned long long)n_tiles - 1;
+  }
+  __syncthreads();
+  if (!last_s) return;
+  __threadfence();
+  for (int k = levels - 5; k >= 0; --k) {
+    const long long nn = 1ll << (3 * k);
+    const uint8_t* below = pyr + pyr_level_offset(k + 1);
+    uint8_t* out = pyr + pyr_level_offset(k);
+    for (long long j = threadIdx.x; j < nn; j += blockDim.x) {
+      unsigned m = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) m |= (__ldcg(&below[8 * j + b]) != 0 ? 1u : 0u) << b;
+      out[j] = (uint8_t)m;
+    }
+    __syncthreads();
+  }
 }
 
 // one pyramid level from the level below: node k at level l has children
@@ -224,8 +387,36 @@ int pyramid_upper_levels(fhv_ctx* ctx, uint8_t* pyramid, int levels, cudaStream_
   return check_cuda(ctx, cudaGetLastError());
 }
 
+static int launch_dir_tiles(fhv_ctx* ctx, bool scan, const uint32_t* counts, uint32_t* offsets, const int32_t* heads,
+                            uint8_t* pyramid, int levels, cudaStream_t s) {
+  const unsigned tiles = (unsigned)(1ll << (3 * (levels - 4)));
+  uint64_t* st = nullptr;
+  if (scan) {
+    st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)tiles * sizeof(uint64_t));
+    if (!st) return FHV_NOMEM;
+    int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)tiles * sizeof(uint64_t), s));
+    if (rc) return rc;
+    rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->tile_counter, 0, sizeof(unsigned), s));
+    if (rc) return rc;
+  }
+  int rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->spare[1], 0, sizeof(unsigned long long), s));
+  if (rc) return rc;
+  {
+    LaunchScope L_(ctx, scan ? kStScanLeaves : kStPyramid, s);
+    if (scan)
+      k_dir_tiles<true><<<tiles, kDirThreads, 0, s>>>(reinterpret_cast<const uint4*>(counts),
+                                                      reinterpret_cast<uint4*>(offsets), nullptr, pyramid, levels, st,
+                                                      ctx->ctl, tiles);
+    else
+      k_dir_tiles<false><<<tiles, kDirThreads, 0, s>>>(nullptr, nullptr, reinterpret_cast<const int4*>(heads), pyramid,
+                                                       levels, nullptr, ctx->ctl, tiles);
+  }
+  return check_cuda(ctx, cudaGetLastError());
+}
+
 int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
                             int levels, cudaStream_t s) {
+  if (levels >= 4) return launch_dir_tiles(ctx, true, counts, offsets, nullptr, pyramid, levels, s);
   constexpr int B = 256;
   const int64_t n_nodes = 1ll << (3 * (levels - 1));
   const unsigned tiles = (unsigned)((n_nodes + B - 1) / B);
@@ -246,6 +437,7 @@ int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offs
 }
 
 int pyramid_from_heads(fhv_ctx* ctx, const int32_t* heads, uint8_t* pyramid, int levels, cudaStream_t s) {
+  if (levels >= 4) return launch_dir_tiles(ctx, false, nullptr, nullptr, heads, pyramid, levels, s);
   const int64_t n_nodes = 1ll << (3 * (levels - 1));
   {
     LaunchScope L_(ctx, kStPyramid, s);
