@@ -94,6 +94,19 @@ typedef struct {
   int32_t *prev;  /* prev_index */
 } fhv_pool_t;
 
+/* One rank's share of a POFA capture partitioned across GPUs by Morton range
+   (SURVEY.md section 8(e)): the rank owns leaves [cell_lo, cell_hi) (multiples
+   of the directory tile: 8^5 leaves for levels >= 5, 8^4 for levels = 4) and rasterises only the triangles whose f64
+   AABB, grown by `margin`, meets one of `boxes` (a conservative world-space
+   cover of its range, host memory; n_boxes == 0 disables binning). */
+#define FHV_SHARD_MAX_BOXES 64
+typedef struct {
+  uint64_t cell_lo, cell_hi;
+  int32_t n_boxes;
+  double margin;
+  double boxes[FHV_SHARD_MAX_BOXES][6]; /* lo xyz, hi xyz */
+} fhv_shard_t;
+
 /* materials + lights, device pointers (fhv/render.py:106-113, fhv/raycast.py:460-466) */
 typedef struct {
   int32_t n_lights;
@@ -184,6 +197,30 @@ int fhv_pofa_scatter(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg
                      int32_t levels, const uint32_t *counts, const uint32_t *offsets, fhv_pool_t *pool,
                      int32_t flags, void *stream);
 
+/* Sharded pofa_build (one rank; the caller exchanges totals between the
+   calls, e.g. one all_gather of a u64 per rank):
+   1. fhv_pofa_shard_count: bin triangles, rasterise, histogram the owned
+      leaves into counts_local[cell_hi - cell_lo]; *local_total = owned
+      fragments.  Synchronises.
+   2. fhv_pofa_shard_directory: offsets_local = base + exclusive scan of
+      counts_local (a slice of the global directory when base = the sum of
+      the lower ranks' totals); writes this shard's occupancy into pyramid
+      (levels >= L-4 exact, upper levels partial: OR them across ranks).
+      The caller zeroes pyramid first.  Async.
+   3. fhv_pofa_shard_scatter: pool->pos[offsets_local[c] - base + k] = ...
+      (pool holds this shard's local_total records).  Synchronises.
+   Must run in this order on one ctx with the same tris / cfg / shard. */
+int fhv_pofa_shard_count(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int32_t levels,
+                         const fhv_shard_t *shard, uint32_t *counts_local, int64_t *local_total,
+                         void *stream);
+int fhv_pofa_shard_directory(fhv_ctx *ctx, int32_t levels, const fhv_shard_t *shard,
+                             const uint32_t *counts_local, uint32_t *offsets_local, uint8_t *pyramid,
+                             uint64_t base, void *stream);
+int fhv_pofa_shard_scatter(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int32_t levels,
+                           const fhv_shard_t *shard, const uint32_t *counts_local,
+                           const uint32_t *offsets_local, uint64_t base, fhv_pool_t *pool, int32_t flags,
+                           void *stream);
+
 /* splat_render over pool[0:n): out_rgba [H][W][4] f64, out_depth [H][W] f64,
    out_winner [H][W] int32 (pool index or -1, may be NULL), gbuffer may be
    NULL.  Synchronises (footprint check). */
@@ -191,6 +228,31 @@ int fhv_splat(fhv_ctx *ctx, int64_t n, const float *pos, const float *nrm, const
               const uint32_t *obj, const double *cam, double radius, const double *background,
               const fhv_shading_t *shading, double *out_rgba, double *out_depth, int32_t *out_winner,
               const fhv_gbuffer_t *gbuffer, int32_t flags, void *stream);
+
+/* Sharded splat_render (one rank holding pool records with global indices
+   [index_base, index_base + n)); the caller all-reduces between the calls:
+   1. fhv_splat_shard_keys: keys[H*W] int64 = per-pixel minimum of this
+      rank's f64 depth keys (order-preserving, sign-flipped so that an int64
+      MIN all-reduce composites ranks by depth; INT64_MAX = empty);
+      footprint[2] (host) = this rank's max splat extent (kx, ky): the
+      caller max-reduces them and raises SceneError if kx*ky > 4096.
+      Synchronises.
+   2. (all-reduce MIN keys) fhv_splat_shard_winners: winners[H*W] int64 =
+      lowest global pool index among this rank's fragments whose key equals
+      the global key (INT64_MAX if none).  Async.
+   3. (all-reduce MIN winners) fhv_splat_shard_resolve: rgba / depth of the
+      pixels whose winner this rank owns, -0.0 elsewhere; write_background
+      (one rank) also writes the background / +inf of empty pixels.  Async.
+   4. (all-reduce SUM rgba, depth) = splat_render of the whole pool. */
+int fhv_splat_shard_keys(fhv_ctx *ctx, int64_t n, const float *pos, const double *cam, double radius,
+                         int64_t *keys, int64_t *footprint, void *stream);
+int fhv_splat_shard_winners(fhv_ctx *ctx, int64_t n, const float *pos, const double *cam, double radius,
+                            const int64_t *keys, int64_t index_base, int64_t *winners, void *stream);
+int fhv_splat_shard_resolve(fhv_ctx *ctx, int64_t n, const float *pos, const float *nrm, const uint32_t *mat,
+                            const double *cam, double radius, const fhv_shading_t *shading,
+                            const int64_t *keys, const int64_t *winners, int64_t own_lo,
+                            int32_t write_background, const double *background, double *out_rgba,
+                            double *out_depth, void *stream);
 
 /* render_raycast for rows [row0, row1) of the camera image: out_rgba
    [H][W][4] f64, out_ids [H][W] int32 (first-hit object id, NULL to skip),

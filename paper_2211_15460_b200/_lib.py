@@ -35,6 +35,11 @@ class Pool(ctypes.Structure):
     _fields_ = [("capacity", c_i64), ("pos", c_vp), ("nrm", c_vp), ("mat", c_vp), ("obj", c_vp), ("prev", c_vp)]
 
 
+class Shard(ctypes.Structure):
+    _fields_ = [("cell_lo", ctypes.c_uint64), ("cell_hi", ctypes.c_uint64), ("n_boxes", c_i32), ("margin", c_f64),
+                ("boxes", (c_f64 * 6) * 64)]
+
+
 class Shading(ctypes.Structure):
     _fields_ = [("n_lights", c_i32), ("light_kind", c_vp), ("light_vec", c_vp), ("light_color", c_vp),
                 ("light_ambient", c_vp), ("n_mats", c_i32), ("diffuse", c_vp), ("specular", c_vp),
@@ -68,8 +73,17 @@ _SIGS = {
     "fhv_pofa_count": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, c_vp, c_vp, c_vp, _P(c_i64), c_vp]),
     "fhv_pofa_scatter": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, c_vp, c_vp, _P(Pool), c_i32,
                                         c_vp]),
+    "fhv_pofa_shard_count": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, _P(Shard), c_vp, _P(c_i64),
+                                            c_vp]),
+    "fhv_pofa_shard_directory": (ctypes.c_int, [c_vp, c_i32, _P(Shard), c_vp, c_vp, c_vp, ctypes.c_uint64, c_vp]),
+    "fhv_pofa_shard_scatter": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, _P(Shard), c_vp, c_vp,
+                                              ctypes.c_uint64, _P(Pool), c_i32, c_vp]),
     "fhv_splat": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_f64, c_vp, _P(Shading), c_vp, c_vp,
                                  c_vp, _P(GBuf), c_i32, c_vp]),
+    "fhv_splat_shard_keys": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_f64, c_vp, c_vp, c_vp]),
+    "fhv_splat_shard_winners": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_f64, c_vp, c_i64, c_vp, c_vp]),
+    "fhv_splat_shard_resolve": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_f64, _P(Shading), c_vp, c_vp,
+                                               c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "fhv_raycast": (ctypes.c_int, [c_vp, _P(Volume), _P(Shading), c_vp, c_vp, c_f64, c_f64, c_i32, c_f64, c_i64,
                                    c_i64, c_vp, c_vp, c_vp, c_vp]),
     "fhv_raycast_image": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, _P(Volume), _P(Shading), c_vp, c_vp,
@@ -105,17 +119,21 @@ def load(require_cuda: bool = True):
 
 
 def ctx(device: torch.device):
-    """Per-device scratch context (created on first use)."""
+    """Scratch context of (device, calling host thread), created on first use.
+    A context is single-threaded (the header's contract), so host threads that
+    share a device -- e.g. the loopback shards of shard.ThreadComm -- each get
+    their own."""
     lib = load()
     idx = device.index if device.index is not None else torch.cuda.current_device()
+    key = (idx, threading.get_ident())
     with _lock:
-        c = _ctxs.get(idx)
+        c = _ctxs.get(key)
         if c is None:
             with torch.cuda.device(idx):
                 c = lib.fhv_ctx_create()
             if not c:
                 raise MemoryError("fhv_ctx_create failed")
-            _ctxs[idx] = c
+            _ctxs[key] = c
     return c
 
 

@@ -11,11 +11,12 @@
 //                  basis + window, winding order, clipped bbox, #work items
 //   scan           job items -> item offsets                      (sync #1)
 //   k_item_expand  work item = (job, 128-pixel slice of the job's bbox)
-//   k_count        lane per item: exact coverage count (+ per-leaf histogram
-//                  with warp-free run aggregation for POFA pass 1)
+//   k_raster<kCnt*> warp per 32 items, lane per bbox pixel: exact coverage
+//                  counts (+ per-leaf histogram, match_any-aggregated, for
+//                  POFA pass 1)
 //   scan           item counts -> item fragment offsets = the reference's
 //                  pool index of each item's first fragment (its "rank")
-//   k_emit<MODE>   lane per item: coverage, barycentrics, interpolation,
+//   k_raster<MODE>  same traversal: coverage, barycentrics, interpolation,
 //                  f32 record, then the store-specific insert
 //   fix-ups        EXACT_ORDER chain / in-leaf sorts, POFL pyramid (sync #2)
 //
@@ -49,9 +50,9 @@ struct CaptureParams {
   const double* fnrm;
   const uint32_t* mat;
   const uint32_t* obj;
+  const uint32_t* tri_index;              // job -> triangle indirection (binned shard), or null
+  unsigned long long cell_lo, cell_hi;    // owned leaf range (POFA shard); [0, 8^L) by default
 };
-
-enum EmitMode { kList = 0, kPpfl = 1, kPofl = 2, kPofa = 3 };
 
 struct EmitOut {
   // pool
@@ -65,10 +66,12 @@ struct EmitOut {
   int32_t* heads;
   long long width, n_keys;
   int levels;
-  // POFA
+  // POFA (indexed by code - cell_lo)
+  uint32_t* leaf_counts;
   const uint32_t* offsets;
   const uint32_t* counts;
   uint32_t* cursors;
+  unsigned long long base;  // global pool index of this shard's first record
   // list
   long long max_out;
   long long* job;
@@ -93,6 +96,7 @@ __device__ __forceinline__ void job_of(const CaptureParams& p, long long j, long
     *t = j;
     *axis = 0;
   }
+  if (p.tri_index) *t = p.tri_index[*t];
 }
 
 // order + coverage bbox, shared by both projections (coverage prologue,
@@ -271,59 +275,56 @@ __global__ void __launch_bounds__(256) k_item_expand(long long n_jobs, const uin
 }
 
 // ---------------------------------------------------------------------------
-// coverage sweep (fhv/_ckern.pyx:72-101)
+// warp-cooperative rasterisation (coverage, fhv/_ckern.pyx:72-101, fused
+// with interpolation and the store-specific insert)
+//
+// A warp takes 32 consecutive work items (lane k <-> item i0+k, each a slice
+// of <= kItemPix bbox pixels of one job, in job order) and walks their
+// concatenated pixels 32 at a time: lane l of chunk s tests flat pixel s+l,
+// whose item is found by a 5-step shuffle search over the items' pixel
+// prefix sums.  One ballot per chunk yields every item's covered count and
+// every fragment's emission rank (= its reference pool index), so the
+// per-fragment work -- barycentric divides, interpolation, keying, atomics,
+// stores -- runs 32 fragments wide instead of one item per thread in
+// sequence, and same-key fragments of a chunk are aggregated with
+// __match_any_sync into one atomic.
 
-struct Cover {
+struct CoverS {  // per-item coverage state, staged in shared memory
   double ax, ay, bx, by, cx, cy;
   double e0x, e0y, e1x, e1y, e2x, e2y;
   double area2;
-  bool tl0, tl1, tl2;
-  int x0, y0, bw;
+  int32_t x0, y0, bw;
+  uint32_t tri, swapped, tl;  // tl bit e: edge e is a top-left edge
+  uint32_t p0, pad;
 };
 
-__device__ __forceinline__ void load_cover(const JobSetup& js, Cover& c) {
+__device__ __forceinline__ void make_cover(const JobSetup& js, uint32_t p0, CoverS& c) {
   c.ax = js.ax; c.ay = js.ay; c.bx = js.bx; c.by = js.by; c.cx = js.cx; c.cy = js.cy;
   c.area2 = __dsub_rn(__dmul_rn(__dsub_rn(c.bx, c.ax), __dsub_rn(c.cy, c.ay)),
                       __dmul_rn(__dsub_rn(c.by, c.ay), __dsub_rn(c.cx, c.ax)));
   c.e0x = __dsub_rn(c.cx, c.bx); c.e0y = __dsub_rn(c.cy, c.by);  // v1 -> v2, opposite v0
   c.e1x = __dsub_rn(c.ax, c.cx); c.e1y = __dsub_rn(c.ay, c.cy);  // v2 -> v0, opposite v1
   c.e2x = __dsub_rn(c.bx, c.ax); c.e2y = __dsub_rn(c.by, c.ay);  // v0 -> v1, opposite v2
-  c.tl0 = c.e0y < 0.0 || (c.e0y == 0.0 && c.e0x > 0.0);
-  c.tl1 = c.e1y < 0.0 || (c.e1y == 0.0 && c.e1x > 0.0);
-  c.tl2 = c.e2y < 0.0 || (c.e2y == 0.0 && c.e2x > 0.0);
+  const bool tl0 = c.e0y < 0.0 || (c.e0y == 0.0 && c.e0x > 0.0);
+  const bool tl1 = c.e1y < 0.0 || (c.e1y == 0.0 && c.e1x > 0.0);
+  const bool tl2 = c.e2y < 0.0 || (c.e2y == 0.0 && c.e2x > 0.0);
+  c.tl = (tl0 ? 1u : 0u) | (tl1 ? 2u : 0u) | (tl2 ? 4u : 0u);
   c.x0 = js.x0; c.y0 = js.y0; c.bw = js.bw;
+  c.tri = js.tri;
+  c.swapped = js.swapped;
+  c.p0 = p0;
 }
 
-// visit covered pixel centres of bbox slice [p0, p1) in row-major order
-template <class F>
-__device__ __forceinline__ void sweep(const Cover& c, uint32_t p0, uint32_t p1, F&& f) {
-  const uint32_t r0 = p0 / (uint32_t)c.bw;
-  int px = c.x0 + (int)(p0 - r0 * (uint32_t)c.bw);
-  int py = c.y0 + (int)r0;
-  const int xend = c.x0 + c.bw;
-  double sy = __dadd_rn((double)py, 0.5);
-  double k0 = __dmul_rn(c.e0x, __dsub_rn(sy, c.by));
-  double k1 = __dmul_rn(c.e1x, __dsub_rn(sy, c.cy));
-  double k2 = __dmul_rn(c.e2x, __dsub_rn(sy, c.ay));
-  for (uint32_t q = p0; q < p1; ++q) {
-    const double sx = __dadd_rn((double)px, 0.5);
-    const double f0 = __dsub_rn(k0, __dmul_rn(c.e0y, __dsub_rn(sx, c.bx)));
-    if (f0 > 0.0 || (f0 == 0.0 && c.tl0)) {
-      const double f1 = __dsub_rn(k1, __dmul_rn(c.e1y, __dsub_rn(sx, c.cx)));
-      if (f1 > 0.0 || (f1 == 0.0 && c.tl1)) {
-        const double f2 = __dsub_rn(k2, __dmul_rn(c.e2y, __dsub_rn(sx, c.ax)));
-        if (f2 > 0.0 || (f2 == 0.0 && c.tl2)) f(px, py, f0, f1, f2);
-      }
-    }
-    if (++px == xend) {
-      px = c.x0;
-      ++py;
-      sy = __dadd_rn((double)py, 0.5);
-      k0 = __dmul_rn(c.e0x, __dsub_rn(sy, c.by));
-      k1 = __dmul_rn(c.e1x, __dsub_rn(sy, c.cy));
-      k2 = __dmul_rn(c.e2x, __dsub_rn(sy, c.ay));
-    }
-  }
+// pixel-centre coverage test with the top-left rule; edge functions in f64
+// exactly as the reference evaluates them (no contraction)
+__device__ __forceinline__ bool cover_test(const CoverS& c, int px, int py, double& f0, double& f1, double& f2) {
+  const double sy = __dadd_rn((double)py, 0.5), sx = __dadd_rn((double)px, 0.5);
+  f0 = __dsub_rn(__dmul_rn(c.e0x, __dsub_rn(sy, c.by)), __dmul_rn(c.e0y, __dsub_rn(sx, c.bx)));
+  if (!(f0 > 0.0 || (f0 == 0.0 && (c.tl & 1u)))) return false;
+  f1 = __dsub_rn(__dmul_rn(c.e1x, __dsub_rn(sy, c.cy)), __dmul_rn(c.e1y, __dsub_rn(sx, c.cx)));
+  if (!(f1 > 0.0 || (f1 == 0.0 && (c.tl & 2u)))) return false;
+  f2 = __dsub_rn(__dmul_rn(c.e2x, __dsub_rn(sy, c.ay)), __dmul_rn(c.e2y, __dsub_rn(sx, c.ax)));
+  return f2 > 0.0 || (f2 == 0.0 && (c.tl & 4u));
 }
 
 // triangle vertex data in winding order
@@ -334,10 +335,11 @@ struct TriData {
   uint32_t mat, obj;
 };
 
-__device__ __forceinline__ void load_tri(const CaptureParams& p, const JobSetup& js, TriData& d, bool normals) {
-  const double* P = p.pos + 9 * (long long)js.tri;
-  const double* N = p.vnrm + 9 * (long long)js.tri;
-  const int o[3] = {0, js.swapped ? 2 : 1, js.swapped ? 1 : 2};
+__device__ __forceinline__ void load_tri(const CaptureParams& p, uint32_t tri, uint32_t swapped, TriData& d,
+                                         bool normals) {
+  const double* P = p.pos + 9 * (long long)tri;
+  const double* N = p.vnrm + 9 * (long long)tri;
+  const int o[3] = {0, swapped ? 2 : 1, swapped ? 1 : 2};
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -348,9 +350,9 @@ __device__ __forceinline__ void load_tri(const CaptureParams& p, const JobSetup&
 #pragma unroll
       for (int k = 0; k < 3; ++k) d.n[i][k] = __ldg(&N[3 * o[i] + k]);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) d.f[k] = __ldg(&p.fnrm[3 * (long long)js.tri + k]);
-    d.mat = __ldg(&p.mat[js.tri]);
-    d.obj = __ldg(&p.obj[js.tri]);
+    for (int k = 0; k < 3; ++k) d.f[k] = __ldg(&p.fnrm[3 * (long long)tri + k]);
+    d.mat = __ldg(&p.mat[tri]);
+    d.obj = __ldg(&p.obj[tri]);
   }
 }
 
@@ -377,160 +379,213 @@ __device__ __forceinline__ void interp_nrm(const TriData& d, double l0, double l
   }
 }
 
-__device__ __forceinline__ unsigned long long job_pixels(const JobSetup& js) {
-  return (unsigned long long)js.bw * (unsigned long long)js.bh;
+__device__ __forceinline__ unsigned range_mask(int a, int b) {  // lanes [a, b), 0 <= a <= b <= 32
+  const unsigned hi = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
+  const unsigned lo = a >= 32 ? 0xffffffffu : ((1u << a) - 1u);
+  return hi & ~lo;
 }
 
-// ---------------------------------------------------------------------------
-// pass 1: exact counts (and the POFA per-leaf histogram, CountingSink)
+__device__ __forceinline__ int clamp32(long long v) { return v < 0 ? 0 : (v > 32 ? 32 : (int)v); }
 
-template <bool kLeaves>
-__global__ void __launch_bounds__(256) k_count(CaptureParams p, const JobSetup* __restrict__ jobs,
-                                               const uint32_t* __restrict__ item_job,
-                                               const uint32_t* __restrict__ item_p0, long long n_items,
-                                               uint32_t* __restrict__ item_cnt, int levels,
-                                               uint32_t* __restrict__ leaf_counts, int* status) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_items;
-       i += (long long)gridDim.x * blockDim.x) {
-    const JobSetup js = jobs[item_job[i]];
-    Cover c;
-    load_cover(js, c);
-    const uint32_t p0 = item_p0[i];
-    const unsigned long long pe = job_pixels(js);
-    const uint32_t p1 = (unsigned long long)p0 + kItemPix < pe ? p0 + kItemPix : (uint32_t)pe;
-    uint32_t cnt = 0;
-    if (!kLeaves) {
-      sweep(c, p0, p1, [&](int, int, double, double, double) { ++cnt; });
-    } else {
-      TriData d;
-      load_tri(p, js, d, false);
-      unsigned long long run_code = ~0ull;
-      uint32_t run = 0;
-      bool bad = false;
-      sweep(c, p0, p1, [&](int, int, double f0, double f1, double f2) {
-        ++cnt;
-        const double l0 = __ddiv_rn(f0, c.area2), l1 = __ddiv_rn(f1, c.area2), l2 = __ddiv_rn(f2, c.area2);
-        double w[3];
-        interp_pos(d, l0, l1, l2, w);
-        uint64_t code;
-        if (!cell_code(__double2float_rn(w[0]), __double2float_rn(w[1]), __double2float_rn(w[2]), levels, &code)) {
-          bad = true;
-          return;
-        }
-        if (code == run_code) {
-          ++run;
-        } else {
-          if (run) atomicAdd(&leaf_counts[run_code], run);
-          run_code = code;
-          run = 1;
-        }
-      });
-      if (run) atomicAdd(&leaf_counts[run_code], run);
-      if (bad) raise_status(status, FHV_RANGE);
-    }
-    item_cnt[i] = cnt;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// pass 2: emission + insertion
-
-__device__ __forceinline__ unsigned long long warp_alloc(unsigned long long* counter) {
-  const unsigned m = __activemask();
-  const unsigned lane = lane_id();
-  const int leader = __ffs(m) - 1;
-  unsigned long long base = 0;
-  if ((int)lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
-  base = __shfl_sync(m, base, leader);
-  return base + __popc(m & ((1u << lane) - 1u));
-}
+enum RasterMode { kCnt = 0, kCntLeaves = 1, kList = 2, kPpfl = 3, kPofl = 4, kPofa = 5 };
+constexpr int kRasterBlock = 256;
 
 template <int kMode, bool kAtomicAlloc>
-__global__ void __launch_bounds__(256) k_emit(CaptureParams p, const JobSetup* __restrict__ jobs,
-                                              const uint32_t* __restrict__ item_job,
-                                              const uint32_t* __restrict__ item_p0,
-                                              const unsigned long long* __restrict__ item_off, long long n_items,
-                                              EmitOut o, Control* ctl) {
+__global__ void __launch_bounds__(kRasterBlock, 3) k_raster(CaptureParams p, const JobSetup* __restrict__ jobs,
+                                                         const uint32_t* __restrict__ item_job,
+                                                         const uint32_t* __restrict__ item_p0,
+                                                         const unsigned long long* __restrict__ item_off,
+                                                         long long n_items, uint32_t* __restrict__ item_cnt,
+                                                         EmitOut o, Control* ctl) {
+  constexpr bool kCounting = kMode == kCnt || kMode == kCntLeaves;
+  constexpr bool kKeyed = kMode == kCntLeaves || kMode == kPofl || kMode == kPofa;
+  __shared__ CoverS cs_all[kRasterBlock / 32][32];
+  const unsigned lane = lane_id();
+  CoverS* cs = cs_all[threadIdx.x >> 5];
+  const unsigned below = (1u << lane) - 1u;
+  const long long n_groups = (n_items + 31) / 32;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   unsigned long long emitted = 0;
   bool bad_range = false, bad_pass = false, bad_key = false;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_items;
-       i += (long long)gridDim.x * blockDim.x) {
-    const uint32_t jid = item_job[i];
-    const JobSetup js = jobs[jid];
-    Cover c;
-    load_cover(js, c);
-    TriData d;
-    load_tri(p, js, d, true);
-    const uint32_t p0 = item_p0[i];
-    const unsigned long long pe = job_pixels(js);
-    const uint32_t p1 = (unsigned long long)p0 + kItemPix < pe ? p0 + kItemPix : (uint32_t)pe;
-    unsigned long long rank = kAtomicAlloc ? 0ull : item_off[i];
-    sweep(c, p0, p1, [&](int px, int py, double f0, double f1, double f2) {
-      const double l0 = __ddiv_rn(f0, c.area2), l1 = __ddiv_rn(f1, c.area2), l2 = __ddiv_rn(f2, c.area2);
-      double w[3], nn[3];
-      interp_pos(d, l0, l1, l2, w);
-      interp_nrm(d, l0, l1, l2, nn);
-      ++emitted;
+  for (long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; g < n_groups; g += nw) {
+    const long long item = g * 32 + lane;
+    uint32_t npix = 0;
+    unsigned long long rank0 = 0;
+    if (item < n_items) {
+      const JobSetup js = jobs[item_job[item]];
+      const uint32_t p0 = item_p0[item];
+      const unsigned long long pe = (unsigned long long)js.bw * (unsigned long long)js.bh;
+      npix = (unsigned long long)p0 + kItemPix < pe ? kItemPix : (uint32_t)(pe - p0);
+      make_cover(js, p0, cs[lane]);
+      if (!kCounting && !kAtomicAlloc) rank0 = item_off[item];
+    }
+    __syncwarp();
+    uint32_t inc = npix;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= (unsigned)d) inc += y;
+    }
+    const uint32_t E = inc - npix;  // my item's first flat pixel
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    uint32_t run = 0;               // live fragments of my item so far
+    for (uint32_t s = 0; s < total; s += 32) {
+      const uint32_t f = s + lane;
+      const bool valid = f < total;
+      int k = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t Ec = __shfl_sync(0xffffffffu, E, k + step);
+        if (Ec <= f && valid) k += step;
+      }
+      const uint32_t Ek = __shfl_sync(0xffffffffu, E, k);
+      const uint32_t run_k = __shfl_sync(0xffffffffu, run, k);
+      const unsigned long long rank0_k = __shfl_sync(0xffffffffu, rank0, k);
+      const CoverS& c = cs[k];
+      double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+      int px = 0, py = 0;
+      bool live = false;
+      if (valid) {
+        const uint32_t q = c.p0 + (f - Ek);
+        const uint32_t r = q / (uint32_t)c.bw;
+        px = c.x0 + (int)(q - r * (uint32_t)c.bw);
+        py = c.y0 + (int)r;
+        live = cover_test(c, px, py, f0, f1, f2);
+      }
+      TriData d;
+      double w[3] = {0.0, 0.0, 0.0};
+      double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+      uint64_t code = ~0ull;
+      if (kMode != kCnt && live) {
+        l0 = __ddiv_rn(f0, c.area2);
+        l1 = __ddiv_rn(f1, c.area2);
+        l2 = __ddiv_rn(f2, c.area2);
+        load_tri(p, c.tri, c.swapped, d, kMode != kCntLeaves);
+        interp_pos(d, l0, l1, l2, w);
+        if (kKeyed) {
+          if (!cell_code(__double2float_rn(w[0]), __double2float_rn(w[1]), __double2float_rn(w[2]), o.levels,
+                         &code)) {
+            bad_range = true;
+            live = false;
+            code = ~0ull;
+          } else if (code < p.cell_lo || code >= p.cell_hi) {  // another shard's leaf
+            live = false;
+            code = ~0ull;
+          }
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, live);
+      // emission rank of my fragment: item base + live lanes of my item before me
+      const int a_k = clamp32((long long)Ek - (long long)s);
+      const unsigned long long rank = rank0_k + run_k + __popc(m & below & ~range_mask(0, a_k));
+      {  // my item's live count
+        const int a = clamp32((long long)E - (long long)s), b = clamp32((long long)E + npix - (long long)s);
+        if (b > a) run += __popc(m & range_mask(a, b));
+      }
+      if (kMode == kCnt) continue;
+      if (kMode == kCntLeaves) {
+        const unsigned grp = __match_any_sync(0xffffffffu, code);
+        if (live && (int)lane == __ffs(grp) - 1) atomicAdd(&o.leaf_counts[code - p.cell_lo], (uint32_t)__popc(grp));
+        continue;
+      }
+      double nn[3] = {0.0, 0.0, 0.0};
+      if (live) {
+        interp_nrm(d, l0, l1, l2, nn);
+        ++emitted;
+      }
       if (kMode == kList) {
-        if ((long long)rank < o.max_out) {
-          o.job[rank] = jid;
+        if (live && (long long)rank < o.max_out) {
+          o.job[rank] = item_job[g * 32 + k];
           o.px[rank] = px;
           o.py[rank] = py;
 #pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            o.wpos[3 * rank + k] = w[k];
-            o.wnrm[3 * rank + k] = nn[k];
+          for (int e = 0; e < 3; ++e) {
+            o.wpos[3 * rank + e] = w[e];
+            o.wnrm[3 * rank + e] = nn[e];
           }
         }
-        ++rank;
-        return;
+        continue;
       }
-      const float q0 = __double2float_rn(w[0]), q1 = __double2float_rn(w[1]), q2 = __double2float_rn(w[2]);
-      long long slot = 0;
-      uint64_t key = 0;
-      if (kMode != kPofa) {
+      long long slot = -1;
+      if (kMode == kPofa) {
+        const unsigned grp = __match_any_sync(0xffffffffu, code);
+        const int leader = __ffs(grp) - 1;
+        uint32_t base = 0, cnt = 0, off = 0;
+        const unsigned long long lc = live ? code - p.cell_lo : 0ull;
+        if (live) {  // issued before the atomic so the latencies overlap
+          cnt = __ldg(&o.counts[lc]);
+          off = __ldg(&o.offsets[lc]);
+        }
+        if (live && (int)lane == leader) base = atomicAdd(&o.cursors[lc], (uint32_t)__popc(grp));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (live) {
+          const uint32_t cur = base + (uint32_t)__popc(grp & below);
+          if (cur >= cnt) {
+            bad_pass = true;
+          } else {
+            slot = (long long)(off - o.base) + cur;
+          }
+        }
+      } else {
         // slot first: records past capacity are dropped before any keying,
         // like _store_split (fhv/storage.py:338-342, 366-369, 388-392)
-        slot = kAtomicAlloc ? (long long)warp_alloc(&ctl->alloc) : (long long)rank;
-        if (slot >= o.capacity) { ++rank; return; }
+        if (kAtomicAlloc) {
+          unsigned long long base = 0;
+          if (m && lane == (unsigned)(__ffs(m) - 1)) base = atomicAdd(&ctl->alloc, (unsigned long long)__popc(m));
+          base = __shfl_sync(0xffffffffu, base, m ? __ffs(m) - 1 : 0);
+          if (live) slot = (long long)(base + __popc(m & below));
+        } else if (live) {
+          slot = (long long)rank;
+        }
+        if (slot >= o.capacity) slot = -1;
+        uint64_t key = ~0ull;
+        if (slot >= 0) {
+          if (kMode == kPpfl) {
+            key = (uint64_t)py * (uint64_t)o.width + (uint64_t)px;
+            if ((long long)key >= o.n_keys) {
+              bad_key = true;
+              slot = -1;
+              key = ~0ull;
+            }
+          } else {
+            key = code;
+          }
+        }
+        // linked insert, aggregated per key: within a group the lane order is
+        // the emission order, so the group is chained in place and spliced in
+        // front of the old head with one atomicExch by its last lane
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const int last = 31 - __clz(grp);
+        int32_t old = -1;
+        if (slot >= 0 && (int)lane == last) old = atomicExch(&o.heads[key], (int32_t)slot);
+        old = __shfl_sync(0xffffffffu, old, last);
+        const unsigned lower = grp & below;
+        const int32_t prev_slot = __shfl_sync(0xffffffffu, (int32_t)slot, lower ? 31 - __clz(lower) : (int)lane);
+        if (slot >= 0) o.prev[slot] = lower ? prev_slot : old;
       }
-      if (kMode == kPpfl) {
-        key = (uint64_t)py * (uint64_t)o.width + (uint64_t)px;
-        if ((long long)key >= o.n_keys) { bad_key = true; ++rank; return; }
-      } else if (!cell_code(q0, q1, q2, o.levels, &key)) {
-        bad_range = true;
-        ++rank;
-        return;
+      if (slot >= 0) {
+        o.pos[3 * slot] = __double2float_rn(w[0]);
+        o.pos[3 * slot + 1] = __double2float_rn(w[1]);
+        o.pos[3 * slot + 2] = __double2float_rn(w[2]);
+        o.nrm[3 * slot] = __double2float_rn(nn[0]);
+        o.nrm[3 * slot + 1] = __double2float_rn(nn[1]);
+        o.nrm[3 * slot + 2] = __double2float_rn(nn[2]);
+        o.mat[slot] = d.mat;
+        o.obj[slot] = d.obj;
+        // POFA: prev_index = -1; under EXACT_ORDER the emission rank is parked
+        // here until k_leaf_order restores the reference's in-leaf order
+        if (kMode == kPofa) o.prev[slot] = (o.flags & FHV_EXACT_ORDER) ? (int32_t)(uint32_t)rank : -1;
       }
-      if (kMode == kPofa) {
-        const uint32_t cur = atomicAdd(&o.cursors[key], 1u);
-        if (cur >= __ldg(&o.counts[key])) { bad_pass = true; ++rank; return; }
-        slot = (long long)__ldg(&o.offsets[key]) + cur;
-      }
-      o.pos[3 * slot] = q0;
-      o.pos[3 * slot + 1] = q1;
-      o.pos[3 * slot + 2] = q2;
-      o.nrm[3 * slot] = __double2float_rn(nn[0]);
-      o.nrm[3 * slot + 1] = __double2float_rn(nn[1]);
-      o.nrm[3 * slot + 2] = __double2float_rn(nn[2]);
-      o.mat[slot] = d.mat;
-      o.obj[slot] = d.obj;
-      if (kMode == kPofa) {
-        // prev_index = -1; under EXACT_ORDER the emission rank is parked here
-        // until k_leaf_order restores the reference's in-leaf order
-        o.prev[slot] = (o.flags & FHV_EXACT_ORDER) ? (int32_t)(uint32_t)rank : -1;
-      } else {
-        o.prev[slot] = atomicExch(&o.heads[key], (int32_t)slot);
-      }
-      ++rank;
-    });
+    }
+    if (kCounting && item < n_items) item_cnt[item] = run;
+    __syncwarp();
   }
   if (kMode == kPofa) {
     // pass-2 emitted count (compared with pass 1, fhv/storage.py:614-617)
     unsigned long long e = emitted;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
-    if (lane_id() == 0 && e) atomicAdd(&ctl->alloc, e);
+    if (lane == 0 && e) atomicAdd(&ctl->alloc, e);
   }
   if (bad_range) raise_status(&ctl->status, FHV_RANGE);
   if (bad_pass) raise_status(&ctl->status, FHV_PASS_MISMATCH);
@@ -602,13 +657,13 @@ __global__ void k_chain_order(int32_t* __restrict__ heads, int32_t* __restrict__
 // pofa_scatter, fhv/_ckern.pyx:135-142) from the parked ranks, then
 // prev_index = -1 (fhv/storage.py:439)
 __global__ void k_leaf_order(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts,
-                             long long n_leaves, float* __restrict__ pos, float* __restrict__ nrm,
+                             long long n_leaves, unsigned long long base, float* __restrict__ pos, float* __restrict__ nrm,
                              uint32_t* __restrict__ mat, uint32_t* __restrict__ obj, int32_t* __restrict__ prev) {
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n_leaves;
        c += (long long)gridDim.x * blockDim.x) {
     const uint32_t n = counts[c];
     if (n == 0) continue;
-    const long long off = offsets[c];
+    const long long off = (long long)(offsets[c] - base);
     uint32_t* rk = reinterpret_cast<uint32_t*>(prev + off);
     for (uint32_t i = 1; i < n; ++i) {
       const uint32_t r = rk[i];
@@ -658,6 +713,39 @@ __global__ void k_face_normals(long long n, const double* __restrict__ pos, doub
 }
 
 // ---------------------------------------------------------------------------
+// shard binning: keep a triangle iff its f64 AABB,
+// grown by the margin, meets one of the shard's boxes.  Fragments are convex
+// combinations of the vertices rounded to f32, so every fragment a triangle
+// can emit into the shard's leaves passes this test.
+
+__global__ void k_bin_tris(const double* __restrict__ pos, long long n, const double* __restrict__ boxes, int n_boxes,
+                           double margin, uint32_t* __restrict__ flag) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const double* P = pos + 9 * t;
+    double mn[3], mx[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double v0 = __ldg(&P[a]), v1 = __ldg(&P[3 + a]), v2 = __ldg(&P[6 + a]);
+      mn[a] = fmin(v0, fmin(v1, v2)) - margin;
+      mx[a] = fmax(v0, fmax(v1, v2)) + margin;
+    }
+    uint32_t keep = 0;
+    for (int b = 0; b < n_boxes && !keep; ++b) {
+      const double* B = boxes + 6 * b;
+      keep = (mn[0] <= B[3] && mx[0] >= B[0] && mn[1] <= B[4] && mx[1] >= B[1] && mn[2] <= B[5] && mx[2] >= B[2]) ? 1u
+                                                                                                                 : 0u;
+    }
+    flag[t] = keep;
+  }
+}
+
+__global__ void k_compact_tris(const uint32_t* __restrict__ flag, const unsigned long long* __restrict__ off,
+                               long long n, uint32_t* __restrict__ idx) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    if (flag[t]) idx[off[t]] = (uint32_t)t;
+}
+
+// ---------------------------------------------------------------------------
 // host orchestration
 
 namespace {
@@ -682,6 +770,9 @@ CaptureParams make_params(const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg) 
   p.fnrm = tris->fnrm;
   p.mat = tris->mat;
   p.obj = tris->obj;
+  p.tri_index = nullptr;
+  p.cell_lo = 0;
+  p.cell_hi = ~0ull;
   return p;
 }
 
@@ -735,12 +826,17 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
     const JobSetup* jobs = (const JobSetup*)ctx->bufs[kJobs].ptr;
     const uint32_t* ij = (const uint32_t*)ctx->bufs[kItemJob].ptr;
     const uint32_t* ip = (const uint32_t*)ctx->bufs[kItemP0].ptr;
+    EmitOut o;
+    std::memset(&o, 0, sizeof(o));
+    o.levels = levels;
+    o.leaf_counts = leaf_counts;
+    const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
     {
       LaunchScope L_(ctx, leaves ? kStCountLeaves : kStCount, s);
       if (leaves)
-        k_count<true><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, n, item_cnt, levels, leaf_counts, &ctx->ctl->status);
+        k_raster<kCntLeaves, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, item_cnt, o, ctx->ctl);
       else
-        k_count<false><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, n, item_cnt, levels, nullptr, &ctx->ctl->status);
+        k_raster<kCnt, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, item_cnt, o, ctx->ctl);
     }
     int rc = check_cuda(ctx, cudaGetLastError());
     if (rc) return rc;
@@ -756,12 +852,13 @@ int emit(fhv_ctx* ctx, const CaptureParams& p, const EmitOut& o, bool atomic_all
   const uint32_t* ij = (const uint32_t*)ctx->bufs[kItemJob].ptr;
   const uint32_t* ip = (const uint32_t*)ctx->bufs[kItemP0].ptr;
   const auto* io = (const unsigned long long*)ctx->bufs[kItemOff].ptr;
+  const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
   {
-    LaunchScope L_(ctx, kStEmitList + kMode, s);
+    LaunchScope L_(ctx, kStEmitList + (kMode - kList), s);
     if (atomic_alloc)
-      k_emit<kMode, true><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, io, n, o, ctx->ctl);
+      k_raster<kMode, true><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, n, nullptr, o, ctx->ctl);
     else
-      k_emit<kMode, false><<<grid_for(n, 256), 256, 0, s>>>(p, jobs, ij, ip, io, n, o, ctx->ctl);
+      k_raster<kMode, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, n, nullptr, o, ctx->ctl);
   }
   return check_cuda(ctx, cudaGetLastError());
 }
@@ -874,59 +971,142 @@ extern "C" int fhv_build_pofl(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_ca
   return build_linked(ctx, tris, cfg, true, 0, levels, pool, heads, pyramid, flags, next_free, stream);
 }
 
-extern "C" int fhv_pofa_count(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
-                              uint32_t* counts, uint32_t* offsets, uint8_t* pyramid, int64_t* total, void* stream) {
-  if (!ctx || !counts || !offsets || !pyramid || levels < 1 || levels > 10) return FHV_BAD_ARGS;
-  int rc = validate(tris, cfg);
-  if (rc) return rc;
-  cudaStream_t s = (cudaStream_t)stream;
-  const CaptureParams p = make_params(tris, cfg);
-  const long long n_leaves = 1LL << (3 * levels);
-  ctx->pass1_levels = -1;
-  if ((rc = plan(ctx, p, s))) return rc;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(counts, 0, (size_t)n_leaves * 4, s)))) return rc;
-  if ((rc = count(ctx, p, true, levels, counts, s))) return rc;
-  if ((rc = sync_control(ctx, s))) return rc;
-  const long long frags = (long long)ctx->ctl_host->scan_total;
-  if (frags >= (1LL << 32)) return FHV_TOO_MANY;
-  if ((rc = scan_leaves_and_pyramid(ctx, counts, offsets, pyramid, levels, s))) return rc;
-  if ((rc = sync_control(ctx, s))) return rc;
-  if ((long long)ctx->ctl_host->scan_total != frags) return FHV_PASS_MISMATCH;
-  ctx->pass1_total = frags;
-  ctx->pass1_levels = levels;
-  ctx->pass1_tris = tris->n_tri;
-  if (total) *total = frags;
+namespace {
+
+bool shard_ok(const fhv_shard_t* sh, int levels) {
+  const unsigned long long n_leaves = 1ull << (3 * levels);
+  if (!sh) return true;
+  if (sh->cell_lo == 0 && sh->cell_hi == n_leaves && sh->n_boxes == 0) return true;
+  const unsigned long long tl = (unsigned long long)dir_tile_leaves(levels);
+  return tl > 0 && sh->cell_lo < sh->cell_hi && sh->cell_hi <= n_leaves && sh->cell_lo % tl == 0 &&
+         sh->cell_hi % tl == 0 && sh->n_boxes >= 0 && sh->n_boxes <= FHV_SHARD_MAX_BOXES && sh->margin >= 0.0;
+}
+
+// params for one shard: binned triangle list (computed once by the count call
+// and kept in ctx for the scatter call) and the owned leaf range
+int shard_params(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int levels,
+                 const fhv_shard_t* sh, bool do_bin, CaptureParams& p, cudaStream_t s) {
+  p = make_params(tris, cfg);
+  const unsigned long long n_leaves = 1ull << (3 * levels);
+  p.cell_lo = sh ? sh->cell_lo : 0ull;
+  p.cell_hi = sh ? sh->cell_hi : n_leaves;
+  if (!sh || sh->n_boxes == 0) {
+    if (do_bin) ctx->n_binned = -1;
+    return FHV_OK;
+  }
+  const long long T = tris->n_tri;
+  if (do_bin) {
+    ctx->n_binned = 0;
+    if (T > 0) {
+      auto* flag = (uint32_t*)scratch(ctx, kTriFlag, (size_t)T * 4);
+      auto* off = (unsigned long long*)scratch(ctx, kTriOff, (size_t)T * 8);
+      auto* idx = (uint32_t*)scratch(ctx, kTriIndex, (size_t)T * 4);
+      auto* boxes = (double*)scratch(ctx, kShardBoxes, sizeof(sh->boxes));
+      if (!flag || !off || !idx || !boxes) return FHV_NOMEM;
+      int rc = check_cuda(ctx, cudaMemcpyAsync(boxes, sh->boxes, (size_t)sh->n_boxes * 6 * sizeof(double),
+                                               cudaMemcpyHostToDevice, s));
+      if (rc) return rc;
+      {
+        LaunchScope L_(ctx, kStJobSetup, s);
+        k_bin_tris<<<grid_for(T, 256), 256, 0, s>>>(tris->pos, T, boxes, sh->n_boxes, sh->margin, flag);
+      }
+      if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+      if ((rc = scan_u32_to_u64(ctx, flag, off, T, s))) return rc;
+      {
+        LaunchScope L_(ctx, kStJobSetup, s);
+        k_compact_tris<<<grid_for(T, 256), 256, 0, s>>>(flag, off, T, idx);
+      }
+      if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+      if ((rc = sync_control(ctx, s))) return rc;
+      ctx->n_binned = (int64_t)ctx->ctl_host->scan_total;
+    }
+  }
+  if (ctx->n_binned < 0) return FHV_BAD_ARGS;
+  p.tri_index = (const uint32_t*)ctx->bufs[kTriIndex].ptr;
+  p.n_tri = ctx->n_binned;
+  p.n_jobs = (cfg->strategy == 1 || cfg->strategy == 2) ? 3 * p.n_tri : p.n_tri;
   return FHV_OK;
 }
 
-extern "C" int fhv_pofa_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
-                                const uint32_t* counts, const uint32_t* offsets, fhv_pool_t* pool, int32_t flags,
-                                void* stream) {
-  if (!ctx || !counts || !offsets || !pool) return FHV_BAD_ARGS;
+}  // namespace
+
+extern "C" int fhv_pofa_shard_count(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
+                                    int32_t levels, const fhv_shard_t* shard, uint32_t* counts_local,
+                                    int64_t* local_total, void* stream) {
+  if (!ctx || !counts_local || levels < 1 || levels > 10 || !shard_ok(shard, levels)) return FHV_BAD_ARGS;
   int rc = validate(tris, cfg);
   if (rc) return rc;
-  if (ctx->pass1_levels != levels || ctx->pass1_tris != tris->n_tri) return FHV_BAD_ARGS;
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->pass1_levels = -1;
+  CaptureParams p;
+  if ((rc = reset_control(ctx, s))) return rc;
+  if ((rc = shard_params(ctx, tris, cfg, levels, shard, true, p, s))) return rc;
+  const unsigned long long n_local = p.cell_hi - p.cell_lo;
+  if ((rc = plan(ctx, p, s))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(counts_local, 0, (size_t)n_local * 4, s)))) return rc;
+  if ((rc = count(ctx, p, true, levels, counts_local, s))) return rc;
+  if ((rc = sync_control(ctx, s))) return rc;
+  const long long frags = (long long)ctx->ctl_host->scan_total;
+  if (frags >= (1LL << 32)) return FHV_TOO_MANY;
+  ctx->pass1_total = frags;
+  ctx->pass1_levels = levels;
+  ctx->pass1_tris = tris->n_tri;
+  ctx->pass1_lo = p.cell_lo;
+  ctx->pass1_hi = p.cell_hi;
+  if (local_total) *local_total = frags;
+  return FHV_OK;
+}
+
+extern "C" int fhv_pofa_shard_directory(fhv_ctx* ctx, int32_t levels, const fhv_shard_t* shard,
+                                        const uint32_t* counts_local, uint32_t* offsets_local, uint8_t* pyramid,
+                                        uint64_t base, void* stream) {
+  if (!ctx || !counts_local || !offsets_local || !pyramid || levels < 1 || levels > 10 || !shard_ok(shard, levels))
+    return FHV_BAD_ARGS;
+  const unsigned long long n_leaves = 1ull << (3 * levels);
+  const unsigned long long lo = shard ? shard->cell_lo : 0ull, hi = shard ? shard->cell_hi : n_leaves;
+  if (ctx->pass1_levels != levels || ctx->pass1_lo != lo || ctx->pass1_hi != hi) return FHV_BAD_ARGS;
+  if (base + (uint64_t)ctx->pass1_total > 0xffffffffull) return FHV_TOO_MANY;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (lo == 0 && hi == n_leaves && base == 0) return scan_leaves_and_pyramid(ctx, counts_local, offsets_local, pyramid,
+                                                                            levels, s);
+  return scan_leaf_range_and_pyramid(ctx, counts_local, offsets_local, pyramid, levels, lo, hi, base, s);
+}
+
+extern "C" int fhv_pofa_shard_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
+                                      int32_t levels, const fhv_shard_t* shard, const uint32_t* counts_local,
+                                      const uint32_t* offsets_local, uint64_t base, fhv_pool_t* pool, int32_t flags,
+                                      void* stream) {
+  if (!ctx || !counts_local || !offsets_local || !pool || !shard_ok(shard, levels)) return FHV_BAD_ARGS;
+  int rc = validate(tris, cfg);
+  if (rc) return rc;
+  const unsigned long long n_leaves = 1ull << (3 * levels);
+  const unsigned long long lo = shard ? shard->cell_lo : 0ull, hi = shard ? shard->cell_hi : n_leaves;
+  if (ctx->pass1_levels != levels || ctx->pass1_tris != tris->n_tri || ctx->pass1_lo != lo || ctx->pass1_hi != hi)
+    return FHV_BAD_ARGS;
   if (pool->capacity < ctx->pass1_total) return FHV_BAD_ARGS;
   cudaStream_t s = (cudaStream_t)stream;
-  const CaptureParams p = make_params(tris, cfg);
-  const long long n_leaves = 1LL << (3 * levels);
-  uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_leaves * 4);
+  CaptureParams p;
+  if ((rc = shard_params(ctx, tris, cfg, levels, shard, false, p, s))) return rc;
+  const unsigned long long n_local = hi - lo;
+  uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_local * 4);
   if (!cursors) return FHV_NOMEM;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_leaves * 4, s)))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_local * 4, s)))) return rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->alloc, 0, 8, s)))) return rc;
   EmitOut o = empty_out();
   set_pool(o, pool);
   o.levels = levels;
-  o.offsets = offsets;
-  o.counts = counts;
+  o.offsets = offsets_local;
+  o.counts = counts_local;
   o.cursors = cursors;
+  o.base = base;
   o.flags = flags;
   if ((rc = emit<kPofa>(ctx, p, o, false, s))) return rc;
   if (flags & FHV_EXACT_ORDER) {
     {
       LaunchScope L_(ctx, kStLeafOrder, s);
-      k_leaf_order<<<grid_for(n_leaves, 128, 32), 128, 0, s>>>(offsets, counts, n_leaves, pool->pos, pool->nrm,
-                                                             pool->mat, pool->obj, pool->prev);
+      k_leaf_order<<<grid_for((long long)n_local, 128, 32), 128, 0, s>>>(offsets_local, counts_local, (long long)n_local,
+                                                                       base, pool->pos, pool->nrm, pool->mat, pool->obj,
+                                                                       pool->prev);
     }
     if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
   }
@@ -935,6 +1115,25 @@ extern "C" int fhv_pofa_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_
   // imply cursors == counts (fhv/storage.py:614-619)
   if ((long long)ctx->ctl_host->alloc != ctx->pass1_total) return FHV_PASS_MISMATCH;
   return FHV_OK;
+}
+
+extern "C" int fhv_pofa_count(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
+                              uint32_t* counts, uint32_t* offsets, uint8_t* pyramid, int64_t* total, void* stream) {
+  if (!ctx || !counts || !offsets || !pyramid || levels < 1 || levels > 10) return FHV_BAD_ARGS;
+  int64_t frags = 0;
+  int rc = fhv_pofa_shard_count(ctx, tris, cfg, levels, nullptr, counts, &frags, stream);
+  if (rc) return rc;
+  if ((rc = fhv_pofa_shard_directory(ctx, levels, nullptr, counts, offsets, pyramid, 0, stream))) return rc;
+  if ((rc = sync_control(ctx, (cudaStream_t)stream))) return rc;
+  if ((long long)ctx->ctl_host->scan_total != frags) return FHV_PASS_MISMATCH;
+  if (total) *total = frags;
+  return FHV_OK;
+}
+
+extern "C" int fhv_pofa_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
+                                const uint32_t* counts, const uint32_t* offsets, fhv_pool_t* pool, int32_t flags,
+                                void* stream) {
+  return fhv_pofa_shard_scatter(ctx, tris, cfg, levels, nullptr, counts, offsets, 0, pool, flags, stream);
 }
 
 extern "C" int fhv_face_normals(fhv_ctx* ctx, int64_t n_tri, const double* pos, double* fnrm, void* stream) {

@@ -62,6 +62,8 @@ struct fhv_ctx {
   int64_t n_jobs = 0, n_items = 0, pass1_total = 0;
   int32_t pass1_levels = -1;
   int64_t pass1_tris = -1;
+  uint64_t pass1_lo = 0, pass1_hi = 0;
+  int64_t n_binned = -1;  // triangles kept by the last shard binning (-1: no binning)
   int last_cuda_error = 0;
 };
 
@@ -69,7 +71,8 @@ namespace fhv {
 
 enum BufId {
   kJobs = 0, kJobItems, kJobItemOff, kItemJob, kItemP0, kItemCnt, kItemOff, kScanStatus,
-  kCursors, kChainScratch, kSplatKey, kSplatWin, kSplatBox, kRays, kTmp0, kTmp1, kNumBufs
+  kCursors, kChainScratch, kSplatKey, kSplatWin, kSplatBox, kRays, kTmp0, kTmp1, kTriFlag, kTriOff, kTriIndex,
+  kShardBoxes, kNumBufs
 };
 
 // Counts a launch and, when profiling is on, brackets it with CUDA events on
@@ -94,6 +97,12 @@ int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, i
 // POFA directory: offsets = excl-scan(counts), pyramid level L-1 from counts > 0, then upper levels
 int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
                             int levels, cudaStream_t s);
+// leaves per directory tile (4096 for L = 4, 32768 for L >= 5, 0 below): shard ranges are multiples
+long long dir_tile_leaves(int levels);
+// shard variant: counts/offsets cover leaves [lo, hi) (multiples of dir_tile_leaves); stored offsets get
+// + base; the pyramid must be zeroed by the caller and receives this shard's occupancy only
+int scan_leaf_range_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
+                                int levels, uint64_t lo, uint64_t hi, uint64_t base, cudaStream_t s);
 int pyramid_from_heads(fhv_ctx* ctx, const int32_t* heads, uint8_t* pyramid, int levels, cudaStream_t s);
 int pyramid_upper_levels(fhv_ctx* ctx, uint8_t* pyramid, int levels, cudaStream_t s);
 

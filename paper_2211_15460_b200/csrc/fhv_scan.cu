@@ -165,82 +165,97 @@ __global__ void __launch_bounds__(BLOCK) k_scan_leaves(const uint4* __restrict__
   if (threadIdx.x == 0 && tile == n_tiles - 1) ctl->scan_total = prefix_s + total_s;
 }
 
-// Directory tiles for L >= 4: one CTA = one level-(L-4) subtree = 4096
-// leaves (4 warps x 4 iterations x 32 lanes x 8 leaves).  A lane owns one
+// Directory tiles: one CTA = one subtree of 8^K leaves (WARPS warps x ITERS
+// iterations x 32 lanes x 8 leaves; K = 4 or 5).  A lane owns one
 // level-(L-1) node (8 consecutive leaves, two 16-B loads) per iteration, so
-// the tile writes pyramid levels L-1 (lane masks), L-2 (warp ballots), L-3
-// (ballot pairs) and L-4 (the tile root) from registers, and for POFA also
-// offsets = exclusive scan of counts (warp running scan + tile look-back).
-// The last tile to finish builds the remaining levels L-5..0 from the
-// level-(L-4) bytes.  One pass over the directory: 8 B/leaf (POFA) or
-// 4 B/leaf (POFL heads) of HBM plus 8^L/7 pyramid bytes.
-constexpr int kDirWarps = 4, kDirIters = 4;
-constexpr int kDirThreads = 32 * kDirWarps;
-constexpr long long kDirTileLeaves = 8LL * 32 * kDirWarps * kDirIters;  // 4096 = 8^4
+// the tile writes pyramid level L-1 (lane masks), L-2 (warp ballots), L-3
+// (ballot pairs) from registers and the levels up to its root (L-K) through
+// shared memory; for POFA it also writes offsets = base + exclusive scan of
+// counts (warp running scan + decoupled tile look-back).  The last tile to
+// finish builds levels L-K-1..0 from the tile roots.  One pass over the
+// directory: 8 B/leaf (POFA) or 4 B/leaf (POFL heads) of HBM plus 8^L/7
+// pyramid bytes.  Bigger tiles shorten the look-back chain (one L2 round
+// trip per 32 tiles on the critical path).
+template <int WARPS, int ITERS>
+struct DirTile {
+  static constexpr int kThreads = 32 * WARPS;
+  static constexpr long long kLeaves = 8LL * 32 * WARPS * ITERS;
+  static constexpr int kL3 = WARPS * ITERS / 2;  // level-(L-3) nodes per tile
+  static constexpr int kK = kLeaves == 4096 ? 4 : (kLeaves == 32768 ? 5 : -1);
+  static_assert(kK > 0, "tile must be a whole octree subtree");
+};
+using DirSmall = DirTile<4, 4>;   // 8^4 leaves
+using DirBig = DirTile<16, 8>;    // 8^5 leaves
 
-template <bool kScan>
-__global__ void __launch_bounds__(kDirThreads) k_dir_tiles(const uint4* __restrict__ counts,
-                                                           uint4* __restrict__ offsets,
-                                                           const int4* __restrict__ heads, uint8_t* __restrict__ pyr,
-                                                           int levels, uint64_t* status, Control* ctl,
-                                                           unsigned n_tiles) {
+template <bool kScan, int WARPS, int ITERS>
+__global__ void __launch_bounds__(32 * WARPS) k_dir_tiles(const uint4* __restrict__ counts,
+                                                          uint4* __restrict__ offsets,
+                                                          const int4* __restrict__ heads, uint8_t* __restrict__ pyr,
+                                                          int levels, uint64_t* status, Control* ctl,
+                                                          unsigned n_tiles, unsigned tile0, uint64_t base) {
+  using T = DirTile<WARPS, ITERS>;
   __shared__ unsigned tile_s;
-  __shared__ uint64_t warp_tot[kDirWarps];
+  __shared__ uint64_t warp_tot[WARPS];
   __shared__ uint64_t prefix_s;
-  __shared__ uint8_t l3[2 * kDirWarps];
+  __shared__ uint8_t lvl_s[2][T::kL3];
   __shared__ int last_s;
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) tile_s = kScan ? atomicAdd(&ctl->tile_counter, 1u) : blockIdx.x;
   __syncthreads();
-  const unsigned tile = tile_s;
+  const unsigned tile = tile_s;        // tile within the range (scan order)
+  const unsigned gtile = tile0 + tile;  // level-(L-K) node in the whole tree
   uint8_t* lv1 = pyr + pyr_level_offset(levels - 1);
   uint8_t* lv2 = pyr + pyr_level_offset(levels - 2);
   uint8_t* lv3 = pyr + pyr_level_offset(levels - 3);
-  uint8_t* lv4 = pyr + pyr_level_offset(levels - 4);
-  const long long node0 = (long long)tile * (kDirTileLeaves / 8) + (long long)warp * (32 * kDirIters);
-  uint32_t c[kDirIters][8];
-  unsigned ballots[kDirIters];
+  // local node index (counts / offsets / heads) and global node index (pyramid)
+  const long long node0 = (long long)tile * (T::kLeaves / 8) + (long long)warp * (32 * ITERS);
+  const long long gnode0 = (long long)gtile * (T::kLeaves / 8) + (long long)warp * (32 * ITERS);
+  uint32_t c[ITERS][8];
+  unsigned ballots[ITERS];
 #pragma unroll
-  for (int i = 0; i < kDirIters; ++i) {
+  for (int i = 0; i < ITERS; ++i) {
     const long long n = node0 + i * 32 + lane;
-    unsigned m = 0;
     if (kScan) {
       const uint4 a = __ldg(&counts[2 * n]), b = __ldg(&counts[2 * n + 1]);
       c[i][0] = a.x; c[i][1] = a.y; c[i][2] = a.z; c[i][3] = a.w;
       c[i][4] = b.x; c[i][5] = b.y; c[i][6] = b.z; c[i][7] = b.w;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) m |= (c[i][k] != 0u ? 1u : 0u) << k;
     } else {
       const int4 a = __ldcs(&heads[2 * n]), b = __ldcs(&heads[2 * n + 1]);
       const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int k = 0; k < 8; ++k) m |= (v[k] >= 0 ? 1u : 0u) << k;
+      for (int k = 0; k < 8; ++k) c[i][k] = v[k] >= 0 ? 1u : 0u;
     }
-    lv1[n] = (uint8_t)m;
-    ballots[i] = __ballot_sync(0xffffffffu, m != 0);
   }
-  // level L-2: lane g < 4 of iteration i writes node (node0 + 32 i) / 8 + g
 #pragma unroll
-  for (int i = 0; i < kDirIters; ++i)
-    if (lane < 4) lv2[(node0 + 32 * i) / 8 + lane] = (uint8_t)((ballots[i] >> (8 * lane)) & 0xffu);
-  // level L-3: iterations (2j, 2j+1) -> one node; bit g = L-2 node g non-empty
-  if (lane < kDirIters / 2) {
-    const unsigned b0 = ballots[0], b1 = ballots[1], b2 = ballots[2], b3 = ballots[3];
-    const unsigned lo = lane == 0 ? b0 : b2, hi = lane == 0 ? b1 : b3;
+  for (int i = 0; i < ITERS; ++i) {
     unsigned m = 0;
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      m |= (((lo >> (8 * g)) & 0xffu) != 0 ? 1u : 0u) << g;
-      m |= (((hi >> (8 * g)) & 0xffu) != 0 ? 1u : 0u) << (g + 4);
+    for (int k = 0; k < 8; ++k) m |= (c[i][k] != 0u ? 1u : 0u) << k;
+    lv1[gnode0 + i * 32 + lane] = (uint8_t)m;
+    ballots[i] = __ballot_sync(0xffffffffu, m != 0);
+    // level L-2: lane g < 4 writes node (gnode0 + 32 i) / 8 + g
+    if (lane < 4) lv2[(gnode0 + 32 * i) / 8 + lane] = (uint8_t)((ballots[i] >> (8 * lane)) & 0xffu);
+  }
+  // level L-3: iterations (2j, 2j+1) -> one node; bit g = L-2 node g non-empty
+#pragma unroll
+  for (int j = 0; j < ITERS / 2; ++j) {
+    if (lane == (unsigned)j) {
+      const unsigned lo = ballots[2 * j], hi = ballots[2 * j + 1];
+      unsigned m = 0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        m |= (((lo >> (8 * g)) & 0xffu) != 0 ? 1u : 0u) << g;
+        m |= (((hi >> (8 * g)) & 0xffu) != 0 ? 1u : 0u) << (g + 4);
+      }
+      lv3[gnode0 / 64 + j] = (uint8_t)m;
+      lvl_s[0][warp * (ITERS / 2) + j] = (uint8_t)m;
     }
-    lv3[node0 / 64 + lane] = (uint8_t)m;
-    l3[2 * warp + lane] = (uint8_t)m;
   }
   if (kScan) {
-    uint64_t excl[kDirIters];
+    uint64_t excl[ITERS];
     uint64_t carry = 0;
 #pragma unroll
-    for (int i = 0; i < kDirIters; ++i) {
+    for (int i = 0; i < ITERS; ++i) {
       uint64_t sum = 0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) sum += c[i][k];
@@ -258,7 +273,7 @@ __global__ void __launch_bounds__(kDirThreads) k_dir_tiles(const uint4* __restri
     if (warp == 0) {
       uint64_t t = 0;
 #pragma unroll
-      for (int w = 0; w < kDirWarps; ++w) t += warp_tot[w];
+      for (int w = 0; w < WARPS; ++w) t += warp_tot[w];
       const uint64_t pf = lookback_warp(status, tile, t);
       if (lane == 0) {
         prefix_s = pf;
@@ -266,10 +281,10 @@ __global__ void __launch_bounds__(kDirThreads) k_dir_tiles(const uint4* __restri
       }
     }
     __syncthreads();
-    uint64_t wbase = prefix_s;
+    uint64_t wbase = prefix_s + base;
     for (unsigned w = 0; w < warp; ++w) wbase += warp_tot[w];
 #pragma unroll
-    for (int i = 0; i < kDirIters; ++i) {
+    for (int i = 0; i < ITERS; ++i) {
       const long long n = node0 + i * 32 + lane;
       uint64_t run = wbase + excl[i];
       uint32_t o[8];
@@ -284,12 +299,23 @@ __global__ void __launch_bounds__(kDirThreads) k_dir_tiles(const uint4* __restri
   } else {
     __syncthreads();
   }
-  // tile root (level L-4)
-  if (threadIdx.x == 0) {
-    unsigned m = 0;
+  // levels L-4 .. L-K (the tile root) through shared memory
+  int cur = 0, n_cur = T::kL3, lvl = levels - 3;
+  while (n_cur > 1) {
+    const int n_up = n_cur / 8;
+    --lvl;
+    if ((int)threadIdx.x < n_up) {
+      unsigned m = 0;
 #pragma unroll
-    for (int k = 0; k < 2 * kDirWarps; ++k) m |= (l3[k] != 0 ? 1u : 0u) << k;
-    lv4[tile] = (uint8_t)m;
+      for (int b = 0; b < 8; ++b) m |= (lvl_s[cur][8 * threadIdx.x + b] != 0 ? 1u : 0u) << b;
+      lvl_s[cur ^ 1][threadIdx.x] = (uint8_t)m;
+      pyr[pyr_level_offset(lvl) + (long long)gtile * n_up + threadIdx.x] = (uint8_t)m;
+    }
+    cur ^= 1;
+    n_cur = n_up;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     __threadfence();
     const unsigned long long done = atomicAdd(&ctl->spare[1], 1ull);
     last_s = done == (unsigned long long)n_tiles - 1;
@@ -297,7 +323,7 @@ __global__ void __launch_bounds__(kDirThreads) k_dir_tiles(const uint4* __restri
   __syncthreads();
   if (!last_s) return;
   __threadfence();
-  for (int k = levels - 5; k >= 0; --k) {
+  for (int k = levels - T::kK - 1; k >= 0; --k) {
     const long long nn = 1ll << (3 * k);
     const uint8_t* below = pyr + pyr_level_offset(k + 1);
     uint8_t* out = pyr + pyr_level_offset(k);
@@ -387,9 +413,31 @@ int pyramid_upper_levels(fhv_ctx* ctx, uint8_t* pyramid, int levels, cudaStream_
   return check_cuda(ctx, cudaGetLastError());
 }
 
+// leaves per directory tile at depth `levels` (0: no tile kernel)
+long long dir_tile_leaves(int levels) { return levels >= 5 ? DirBig::kLeaves : (levels == 4 ? DirSmall::kLeaves : 0); }
+
+template <class T>
+static void launch_dir(bool scan, unsigned tiles, unsigned tile0, const uint32_t* counts, uint32_t* offsets,
+                       const int32_t* heads, uint8_t* pyramid, int levels, uint64_t* st, Control* ctl, uint64_t base,
+                       cudaStream_t s) {
+  constexpr int W = T::kThreads / 32, I = (int)(T::kLeaves / (8LL * T::kThreads));
+  if (scan)
+    k_dir_tiles<true, W, I><<<tiles, T::kThreads, 0, s>>>(reinterpret_cast<const uint4*>(counts),
+                                                          reinterpret_cast<uint4*>(offsets), nullptr, pyramid, levels,
+                                                          st, ctl, tiles, tile0, base);
+  else
+    k_dir_tiles<false, W, I><<<tiles, T::kThreads, 0, s>>>(nullptr, nullptr, reinterpret_cast<const int4*>(heads),
+                                                           pyramid, levels, nullptr, ctl, tiles, 0u, 0ull);
+}
+
 static int launch_dir_tiles(fhv_ctx* ctx, bool scan, const uint32_t* counts, uint32_t* offsets, const int32_t* heads,
-                            uint8_t* pyramid, int levels, cudaStream_t s) {
-  const unsigned tiles = (unsigned)(1ll << (3 * (levels - 4)));
+                            uint8_t* pyramid, int levels, cudaStream_t s, uint64_t lo = 0, uint64_t hi = 0,
+                            uint64_t base = 0) {
+  const long long tl = dir_tile_leaves(levels);
+  if (hi == 0) hi = 1ull << (3 * levels);
+  const unsigned tiles = (unsigned)((hi - lo) / (uint64_t)tl);
+  const unsigned tile0 = (unsigned)(lo / (uint64_t)tl);
+  if (tiles == 0) return FHV_OK;
   uint64_t* st = nullptr;
   if (scan) {
     st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)tiles * sizeof(uint64_t));
@@ -403,13 +451,10 @@ static int launch_dir_tiles(fhv_ctx* ctx, bool scan, const uint32_t* counts, uin
   if (rc) return rc;
   {
     LaunchScope L_(ctx, scan ? kStScanLeaves : kStPyramid, s);
-    if (scan)
-      k_dir_tiles<true><<<tiles, kDirThreads, 0, s>>>(reinterpret_cast<const uint4*>(counts),
-                                                      reinterpret_cast<uint4*>(offsets), nullptr, pyramid, levels, st,
-                                                      ctx->ctl, tiles);
+    if (tl == DirBig::kLeaves)
+      launch_dir<DirBig>(scan, tiles, tile0, counts, offsets, heads, pyramid, levels, st, ctx->ctl, base, s);
     else
-      k_dir_tiles<false><<<tiles, kDirThreads, 0, s>>>(nullptr, nullptr, reinterpret_cast<const int4*>(heads), pyramid,
-                                                       levels, nullptr, ctx->ctl, tiles);
+      launch_dir<DirSmall>(scan, tiles, tile0, counts, offsets, heads, pyramid, levels, st, ctx->ctl, base, s);
   }
   return check_cuda(ctx, cudaGetLastError());
 }
@@ -434,6 +479,14 @@ int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offs
   rc = check_cuda(ctx, cudaGetLastError());
   if (rc) return rc;
   return pyramid_upper_levels(ctx, pyramid, levels, s);
+}
+
+int scan_leaf_range_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
+                                int levels, uint64_t lo, uint64_t hi, uint64_t base, cudaStream_t s) {
+  const long long tl = dir_tile_leaves(levels);
+  if (tl == 0 || lo % (uint64_t)tl || hi % (uint64_t)tl || hi < lo || hi > (1ull << (3 * levels))) return FHV_BAD_ARGS;
+  if (hi == lo) return check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->scan_total, 0, 8, s));
+  return launch_dir_tiles(ctx, true, counts, offsets, nullptr, pyramid, levels, s, lo, hi, base);
 }
 
 int pyramid_from_heads(fhv_ctx* ctx, const int32_t* heads, uint8_t* pyramid, int levels, cudaStream_t s) {

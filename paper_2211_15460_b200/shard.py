@@ -1,0 +1,386 @@
+"""Multi-GPU partition of the hot path by Morton range.
+
+The reference is single-process (no distribution at all, SURVEY.md section 2
+row 13); this module is the B200 build's scale-out of its POFA capture
+(``pofa_build``, fhv/storage.py:590-621) and splat reconstruction
+(``splat_render``, fhv/render.py:249-320) across the GPUs of one box:
+
+* **Capture.**  Rank r owns the contiguous leaf range ``[lo_r, hi_r)`` of the
+  Morton order (whole directory tiles of 8^5 leaves).  It rasterises only the
+  triangles whose f64 AABB meets its range's world-space cover (binning on the
+  device), keeps only fragments of its own leaves, and builds its slice of the
+  directory.  The single exchange is one ``all_gather`` of a fragment total
+  per rank: ``base_r`` = sum of the lower ranks' totals turns local offsets
+  into global ones.  Leaf order inside the Morton range equals the global
+  order restricted to it, so the concatenation of the ranks' pools and
+  directory slices IS the 1-GPU ``pofa_build`` (bit-identical with
+  ``exact_order=True``; the tests check it).
+* **Splat.**  Each rank z-tests its own fragments into a full-frame int64
+  depth-key buffer; ``all_reduce(MIN)`` composites the ranks by depth; the
+  tie-break pass finds each pixel's lowest global pool index among the
+  fragments at the global depth, ``all_reduce(MIN)``; each rank shades the
+  pixels whose winner it owns (-0.0 elsewhere, the exact neutral element of
+  addition) and ``all_reduce(SUM)`` assembles the frame.  Identical to
+  ``splat_render`` over the whole pool.
+
+``Comm`` is the exchange: ``TorchComm`` (torch.distributed, NCCL over
+NVLink on the box, gloo on CPU) or ``ThreadComm`` (N ranks as threads of one
+process sharing one GPU -- a loopback used by the tests).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceShading, capture_cfg, device_scene, host_f64
+from .lights import ImageBuffer
+from .raster import CaptureStrategy, RasterConfig, capture_plan
+from .scene import Camera, SceneError
+from .storage import FhvError, FragmentPool, OccupancyPyramid, PofaDirectory, _check_levels, morton_decode
+
+__all__ = ["Comm", "FhvPofaShard", "ThreadComm", "TorchComm", "fragment_weights", "pofa_build_shard",
+           "range_boxes", "shard_ranges", "splat_render_shard", "tile_leaves"]
+
+MAX_BOXES = 64
+BIN_MARGIN = 1e-5  # world units; fragments lie within 1 f32 ulp of the triangle's AABB
+
+
+# ---------------------------------------------------------------------------
+# partition
+
+
+def tile_leaves(levels: int) -> int:
+    """Leaves per directory tile = the granularity of a shard range."""
+    if levels >= 5:
+        return 8 ** 5
+    if levels == 4:
+        return 8 ** 4
+    raise FhvError("sharded capture needs levels >= 4")
+
+
+def shard_ranges(levels: int, world: int, weights: np.ndarray | None = None) -> list:
+    """Contiguous Morton ranges [lo, hi), one per rank, cut at tile bounds.
+    ``weights`` (one per tile, e.g. :func:`fragment_weights`) balances the
+    expected fragments per rank; otherwise the tiles are split evenly."""
+    _check_levels(levels)
+    tl = tile_leaves(levels)
+    n_tiles = 8 ** levels // tl
+    if world < 1 or world > n_tiles:
+        raise FhvError(f"cannot split {n_tiles} directory tiles across {world} ranks")
+    if weights is None:
+        cuts = [round(r * n_tiles / world) for r in range(world + 1)]
+    else:
+        w = np.asarray(weights, dtype=np.float64)
+        if w.shape != (n_tiles,):
+            raise FhvError("weights must have one entry per directory tile")
+        cum = np.concatenate(([0.0], np.cumsum(w)))
+        total = cum[-1]
+        cuts = [0]
+        for r in range(1, world):
+            c = int(np.searchsorted(cum, total * r / world, side="left"))
+            c = min(max(c, cuts[-1] + 1), n_tiles - (world - r))  # every rank keeps >= 1 tile
+            cuts.append(c)
+        cuts.append(n_tiles)
+    return [(cuts[r] * tl, cuts[r + 1] * tl) for r in range(world)]
+
+
+def range_boxes(lo: int, hi: int, levels: int) -> np.ndarray:
+    """World-space cover of leaves [lo, hi): the range split into aligned
+    Morton blocks (each an octree node, i.e. a cube).  Falls back to the
+    blocks' bounding box beyond MAX_BOXES blocks."""
+    boxes = []
+    while lo < hi:
+        k = 0
+        while k < levels and lo % (8 ** (k + 1)) == 0 and lo + 8 ** (k + 1) <= hi:
+            k += 1
+        lvl = levels - k
+        x, y, z = morton_decode(lo >> (3 * k), lvl) if lvl > 0 else (0, 0, 0)
+        size = 1.0 / (1 << lvl)
+        boxes.append((x * size, y * size, z * size, (x + 1) * size, (y + 1) * size, (z + 1) * size))
+        lo += 8 ** k
+    b = np.asarray(boxes, dtype=np.float64).reshape(-1, 6)
+    if len(b) > MAX_BOXES:
+        b = np.concatenate((b[:, :3].min(axis=0), b[:, 3:].max(axis=0)))[None, :]
+    return b
+
+
+def fragment_weights(scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int) -> np.ndarray:
+    """Expected fragments per directory tile, for balanced ranges: each
+    triangle's area / pitch^2 (x3 for the three-axis strategies) binned by its
+    centroid.  Host NumPy, cached on the scene (planning, not the hot path)."""
+    key = ("fragment_weights", strategy.kind, cfg.resolution, cfg.extent, levels)
+    cache = scene.__dict__.setdefault("_shard_cache", {})
+    if key in cache:
+        return cache[key]
+    tl = tile_leaves(levels)
+    tlev = levels - int(round(np.log(tl) / np.log(8)))  # octree level of a tile
+    pos = np.asarray(scene.positions, dtype=np.float64)
+    cen = np.clip(pos.mean(axis=1), 0.0, 1.0)
+    side = 1 << tlev
+    idx = np.clip(np.floor(cen * side).astype(np.int64), 0, side - 1)
+    from .storage import morton_encode
+    code = morton_encode(idx[:, 0], idx[:, 1], idx[:, 2], tlev) if tlev > 0 else np.zeros(len(pos), np.int64)
+    e1, e2 = pos[:, 1] - pos[:, 0], pos[:, 2] - pos[:, 0]
+    area = 0.5 * np.linalg.norm(np.cross(e1, e2), axis=1)
+    pitch = cfg.extent / cfg.resolution[1]
+    w = area / (pitch * pitch) * (3.0 if strategy.kind in ("three_separate", "three_way_geometry") else 1.0)
+    out = np.bincount(code, weights=w + 1.0, minlength=8 ** tlev).astype(np.float64)
+    cache[key] = out
+    return out
+
+
+# ---------------------------------------------------------------------------
+# exchange
+
+
+class Comm:
+    rank: int = 0
+    world: int = 1
+    device: torch.device | None = None
+
+    def all_gather_int(self, v: int) -> list:
+        raise NotImplementedError
+
+    def all_reduce_(self, t: torch.Tensor, op: str) -> torch.Tensor:
+        raise NotImplementedError
+
+
+class TorchComm(Comm):
+    """torch.distributed over the default (or given) process group.  NCCL
+    operates on the CUDA tensors directly (NVLink / NVSwitch); gloo on CPU
+    copies."""
+
+    _OPS = {"min": "MIN", "max": "MAX", "sum": "SUM"}
+
+    def __init__(self, group=None, device: torch.device | None = None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.backend = dist.get_backend(group)
+        self.device = device
+
+    def _dev(self):
+        return self.device if self.backend == "nccl" else torch.device("cpu")
+
+    def all_gather_int(self, v: int) -> list:
+        t = torch.tensor([int(v)], dtype=torch.int64, device=self._dev())
+        out = torch.empty(self.world, dtype=torch.int64, device=self._dev())
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        return [int(x) for x in out.cpu().tolist()]
+
+    def all_reduce_(self, t: torch.Tensor, op: str) -> torch.Tensor:
+        rop = getattr(self.dist.ReduceOp, self._OPS[op])
+        if self.backend != "nccl" and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=rop, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, op=rop, group=self.group)
+        return t
+
+
+class _ThreadHub:
+    def __init__(self, world: int):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+
+class ThreadComm(Comm):
+    """``world`` ranks as host threads of one process (loopback on one GPU).
+    Every rank reduces the published tensors in rank order, so all ranks get
+    bitwise the same result."""
+
+    def __init__(self, hub: _ThreadHub, rank: int, device: torch.device | None = None):
+        self.hub, self.rank, self.world, self.device = hub, rank, hub.world, device
+
+    @staticmethod
+    def group(world: int, device: torch.device | None = None) -> list:
+        hub = _ThreadHub(world)
+        return [ThreadComm(hub, r, device) for r in range(world)]
+
+    def _exchange(self, v):
+        h = self.hub
+        h.slots[self.rank] = v
+        h.barrier.wait()
+        got = list(h.slots)
+        h.barrier.wait()
+        return got
+
+    def all_gather_int(self, v: int) -> list:
+        return [int(x) for x in self._exchange(int(v))]
+
+    def all_reduce_(self, t: torch.Tensor, op: str) -> torch.Tensor:
+        if t.is_cuda:
+            torch.cuda.synchronize(t.device)
+        parts = self._exchange(t)
+        fn = {"min": torch.minimum, "max": torch.maximum, "sum": torch.add}[op]
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc = fn(acc, p)
+        if t.is_cuda:
+            torch.cuda.synchronize(t.device)
+        self._exchange(None)  # every rank has read every part before any rank overwrites its own
+        t.copy_(acc)
+        return t
+
+
+# ---------------------------------------------------------------------------
+# sharded capture
+
+
+@dataclass
+class FhvPofaShard:
+    """One rank's slice of a POFA volume: leaves [cell_lo, cell_hi), pool
+    records with global indices [base, base + pool.capacity)."""
+    directory: PofaDirectory   # counts / offsets of the owned leaves (offsets are global)
+    pyramid: OccupancyPyramid  # this shard's occupancy (see gather_pyramid)
+    pool: FragmentPool
+    capture_resolution: int
+    cell_lo: int
+    cell_hi: int
+    base: int
+    total: int
+    rank: int
+    world: int
+    stats: object = None
+    materials: list | None = None
+    layout = "POFA"
+
+    @property
+    def levels(self) -> int:
+        return self.directory.levels
+
+    def gather_pyramid(self, comm: Comm) -> OccupancyPyramid:
+        """The global occupancy pyramid: MAX over ranks is exact at and below
+        the tile level (each node inside one rank's range); the few levels
+        above are recomputed."""
+        data = self.pyramid.data.clone()
+        comm.all_reduce_(data, "max")
+        L = self.levels
+        k_tile = L - int(round(np.log(tile_leaves(L)) / np.log(8)))
+        off = [((1 << (3 * k)) - 1) // 7 for k in range(L + 1)]
+        bit = (1 << torch.arange(8, device=data.device, dtype=torch.int32))
+        for k in range(k_tile - 1, -1, -1):
+            below = data[off[k + 1]:off[k + 2]].to(torch.int32).reshape(-1, 8)
+            data[off[k]:off[k + 1]] = ((below != 0).to(torch.int32) * bit).sum(dim=1).to(torch.uint8)
+        return OccupancyPyramid(L, data)
+
+
+def _shard_struct(lo: int, hi: int, levels: int) -> _lib.Shard:
+    sh = _lib.Shard()
+    sh.cell_lo, sh.cell_hi = lo, hi
+    full = lo == 0 and hi == 8 ** levels
+    boxes = np.zeros((0, 6)) if full else range_boxes(lo, hi, levels)
+    sh.n_boxes = len(boxes)
+    sh.margin = BIN_MARGIN
+    for i, b in enumerate(boxes):
+        for k in range(6):
+            sh.boxes[i][k] = float(b[k])
+    return sh
+
+
+def pofa_build_shard(scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int, comm: Comm,
+                     ranges: list | None = None, balance: bool = True, exact_order: bool = False,
+                     device=None) -> FhvPofaShard:
+    """This rank's share of ``pofa_build(scene, strategy, cfg, levels)``."""
+    if levels < 4:
+        raise FhvError("sharded capture needs levels >= 4")
+    if levels > 11:
+        raise FhvError(f"levels {levels}: dense POFA directories beyond L=11 exceed device memory")
+    if ranges is None:
+        w = fragment_weights(scene, strategy, cfg, levels) if balance else None
+        ranges = shard_ranges(levels, comm.world, w)
+    lo, hi = ranges[comm.rank]
+    plan = capture_plan(scene, strategy, cfg)
+    ds = device_scene(scene, device)
+    dev = ds.device
+    n_local = hi - lo
+    counts = torch.empty(n_local, dtype=torch.uint32, device=dev)
+    offsets = torch.empty(n_local, dtype=torch.uint32, device=dev)
+    pyr = OccupancyPyramid(levels, device=dev)  # zeros: only this shard's occupancy is written
+    lib = _lib.load()
+    tris, c = ds.struct(), capture_cfg(plan)
+    sh = _shard_struct(lo, hi, levels)
+    cx, st = _lib.ctx(dev), _lib.stream_ptr(dev)
+    local = ctypes.c_int64(0)
+    rc = lib.fhv_pofa_shard_count(cx, tris, c, levels, sh, _lib.ptr(counts), local, st)
+    _lib.check(rc, "pofa_build_shard pass 1")
+    totals = comm.all_gather_int(local.value)
+    base, total = sum(totals[:comm.rank]), sum(totals)
+    if total >= 1 << 32:
+        raise FhvError("fragment count exceeds the 32-bit offset range")
+    rc = lib.fhv_pofa_shard_directory(cx, levels, sh, _lib.ptr(counts), _lib.ptr(offsets), _lib.ptr(pyr.data), base,
+                                      st)
+    _lib.check(rc, "pofa_build_shard directory")
+    pool = FragmentPool(int(local.value), dev, fill_prev=False)
+    rc = lib.fhv_pofa_shard_scatter(cx, tris, c, levels, sh, _lib.ptr(counts), _lib.ptr(offsets), base, pool.struct(),
+                                    _lib.FHV_EXACT_ORDER if exact_order else 0, st)
+    _lib.check(rc, "pofa_build_shard pass 2")
+    pool.next_free = pool.capacity
+    return FhvPofaShard(PofaDirectory(levels, offsets, counts), pyr, pool, int(cfg.resolution[1]), lo, hi, base, total,
+                        comm.rank, comm.world, plan.stats(total), scene.materials)
+
+
+# ---------------------------------------------------------------------------
+# sharded splat
+
+
+class SplatBuffers:
+    """Per-view int64 key / winner buffers (reusable across frames)."""
+
+    def __init__(self, width: int, height: int, device):
+        self.keys = torch.empty(width * height, dtype=torch.int64, device=device)
+        self.winners = torch.empty(width * height, dtype=torch.int64, device=device)
+
+
+def splat_render_shard(vol: FhvPofaShard, camera: Camera, lights, splat_radius_world: float, materials, comm: Comm,
+                       background=(0.0, 0.0, 0.0, 0.0), *, out: ImageBuffer | None = None,
+                       shading: DeviceShading | None = None, buffers: SplatBuffers | None = None) -> ImageBuffer:
+    """``splat_render`` of the union of all ranks' pools; every rank returns
+    the full frame."""
+    if splat_radius_world <= 0.0:
+        raise SceneError("splat radius must be > 0")
+    pool = vol.pool
+    dev = pool.device
+    w, h = camera.resolution
+    if out is None:
+        out = ImageBuffer(w, h, torch.empty((h, w, 4), dtype=torch.float64, device=dev),
+                          torch.empty((h, w), dtype=torch.float64, device=dev))
+    if shading is None:
+        shading = DeviceShading(materials, lights, dev)
+    if buffers is None:
+        buffers = SplatBuffers(w, h, dev)
+    n = pool.stored_count
+    cam = host_f64(camera.scalars())
+    bg = host_f64(background)
+    lib = _lib.load()
+    cx, st = _lib.ctx(dev), _lib.stream_ptr(dev)
+    r = float(splat_radius_world)
+    fp = (ctypes.c_int64 * 2)()
+    rc = lib.fhv_splat_shard_keys(cx, n, _lib.ptr(pool.position), cam.ctypes.data, r, _lib.ptr(buffers.keys), fp, st)
+    _lib.check(rc, "splat_render_shard keys")
+    ext = torch.tensor([fp[0], fp[1]], dtype=torch.int64, device=dev)
+    comm.all_reduce_(ext, "max")
+    kx, ky = (int(v) for v in ext.cpu().tolist())
+    if kx * ky > 4096:
+        _lib.check(_lib.FHV_SPLAT_BIG, "splat_render_shard")
+    comm.all_reduce_(buffers.keys, "min")
+    rc = lib.fhv_splat_shard_winners(cx, n, _lib.ptr(pool.position), cam.ctypes.data, r, _lib.ptr(buffers.keys),
+                                     vol.base, _lib.ptr(buffers.winners), st)
+    _lib.check(rc, "splat_render_shard winners")
+    comm.all_reduce_(buffers.winners, "min")
+    rc = lib.fhv_splat_shard_resolve(cx, n, _lib.ptr(pool.position), _lib.ptr(pool.normal), _lib.ptr(pool.material_id),
+                                     cam.ctypes.data, r, shading.struct(), _lib.ptr(buffers.keys),
+                                     _lib.ptr(buffers.winners), vol.base, 1 if comm.rank == 0 else 0, bg.ctypes.data,
+                                     _lib.ptr(out.pixels), _lib.ptr(out.depth), st)
+    _lib.check(rc, "splat_render_shard resolve")
+    comm.all_reduce_(out.pixels, "sum")
+    comm.all_reduce_(out.depth, "sum")
+    return out
