@@ -15,8 +15,13 @@ scene copied host->device (pinned) and the image copied back every step.
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port, oracle/fhv_oracle.c, threads=1 like the reference's fastest
 setting) on the same workload and prints the same JSON line shape.
-Multi-GPU (torchrun, N>1): each rank runs its own full-size replica of the
-workload (weak scaling, no data-path collective); time = max over ranks.
+Multi-GPU (torchrun, N>1): the same scene is partitioned by Morton range
+(paper_2211_15460_b200/shard.py): each rank bins the
+triangles of its leaf range, captures its slice of the POFA (one all_gather of
+a fragment total per rank for the global offsets) and splats its fragments;
+the frame is composited by depth with NCCL all-reduces (MIN keys, MIN
+winners, SUM pixels).  Strong scaling: fixed total work; time = max over
+ranks; value = all fragments / that time.
 """
 from __future__ import annotations
 
@@ -161,7 +166,7 @@ def reference_arm(args):
     value = frags / tot_s
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frag/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded icosphere field)", "config": CONFIG,
             "cpu_baseline": {"value": value, "unit": "frag/s", "cores": 1, "kind": "port",
                              "sample": "full C3 step per step (POFA capture + 1080p splat), oracle/fhv_oracle.c"},
@@ -184,7 +189,7 @@ def main():
 
     import paper_2211_15460_b200 as fhv
     from paper_2211_15460_b200 import _lib
-    from paper_2211_15460_b200.device import DeviceShading, device_scene
+    from paper_2211_15460_b200.device import DeviceScene, DeviceShading, device_scene
     from paper_2211_15460_b200.lights import ImageBuffer
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -203,16 +208,29 @@ def main():
     img = ImageBuffer(W, H, torch.empty((H, W, 4), dtype=torch.float64, device=dev),
                       torch.empty((H, W), dtype=torch.float64, device=dev))
 
-    def step():
-        vol = fhv.pofa_build(scene, strat, cfg, L, exact_order=args.exact_order, device=dev)
-        fhv.splat_render(vol.pool, view, w["lights"], w["radius"], scene.materials, out=img, packed=args.packed,
-                         shading=shading)
-        return vol
+    if world > 1:
+        from paper_2211_15460_b200 import shard
+        comm = shard.TorchComm(device=dev)
+        ranges = shard.shard_ranges(L, world, shard.fragment_weights(scene, strat, cfg, L))
+        bufs = shard.SplatBuffers(W, H, dev)
+
+        def step(tris=ds, out=img):
+            vol = shard.pofa_build_shard(scene, strat, cfg, L, comm, ranges=ranges, exact_order=args.exact_order,
+                                         device=dev, tris=tris)
+            shard.splat_render_shard(vol, view, w["lights"], w["radius"], scene.materials, comm, out=out,
+                                     shading=shading, buffers=bufs)
+            return vol
+    else:
+        def step(tris=ds, out=img):
+            vol = fhv.pofa_build(scene, strat, cfg, L, exact_order=args.exact_order, device=dev, tris=tris)
+            fhv.splat_render(vol.pool, view, w["lights"], w["radius"], scene.materials, out=out, packed=args.packed,
+                             shading=shading)
+            return vol
 
     for _ in range(args.warmup):
         vol = step()
     torch.cuda.synchronize()
-    n_frags = vol.pool.next_free
+    n_frags = vol.total if world > 1 else vol.pool.next_free
 
     def barrier():
         if world > 1:
@@ -241,7 +259,7 @@ def main():
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
     ms_step = ms / args.steps
-    value = world * n_frags * args.steps / (ms / 1e3)
+    value = n_frags * args.steps / (ms / 1e3)
 
     # per-stage shares + roofline of the dominant kernel
     stage_ms = {k: v[0] / args.steps for k, v in prof.items()}
@@ -250,16 +268,16 @@ def main():
     P = W * H
     algo_bytes = {  # minimal bytes per launch
         "emit_pofa": 176 * T + 36 * n_frags,
-        "count_leaves": 176 * T + 4 * 8 ** L,
+        "count_leaves": 72 * T + 4 * 8 ** L,
         "scan_leaves": 8 * 8 ** L + 8 ** (L - 1),
         "splat_depth": 12 * n_frags + 8 * P,
         "splat_index": 12 * n_frags + 8 * P,
         "splat_resolve": 8 * P + 4 * P + 40 * P,
-        "job_setup": 72 + 24 + 80 * T,
+        "job_setup": (72 + 24 + 80 + 4) * T,
     }
     peak, peak_kind = peaks()
     roof = None
-    if dominant in algo_bytes:
+    if dominant in algo_bytes and world == 1:  # per-kernel bytes below are for the unsharded (N=1) launch
         per_launch_ms = prof[dominant][0] / prof[dominant][1]
         ach = algo_bytes[dominant] / (per_launch_ms / 1e3) / 1e9
         traffic = None
@@ -277,24 +295,61 @@ def main():
     step_bytes = (2 * 176 * T + 36 * n_frags + 12 * 8 ** L + (8 ** L - 1) // 7  # POFA capture
                   + 12 * n_frags + 28 * P + 40 * P)                              # splat + f64 rgba/depth
     # ---- end to end: pinned host scene in, image out ------------------------
+    # Every step copies its scene from pinned host memory and reads its f64
+    # image + depth back.  The copies run on their own streams, double
+    # buffered, so step k+1's upload and step k-1's read-back overlap step
+    # k's kernels (a two-deep pipeline, as a serving loop would run it).
     if not args.profile_only:
-        pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in
-               (scene.positions, scene.normals, scene.face_normals, scene.material_id.view(np.int32),
-                scene.object_id.view(np.int32))]
-        dst = [ds.pos, ds.vnrm, ds.fnrm, ds.mat.view(torch.int32), ds.obj.view(torch.int32)]
-        out_px = torch.empty((H, W, 4), dtype=torch.float64).pin_memory()
-        out_dp = torch.empty((H, W), dtype=torch.float64).pin_memory()
+        host = [np.ascontiguousarray(a) for a in (scene.positions, scene.normals, scene.face_normals,
+                                                  scene.material_id.view(np.int32), scene.object_id.view(np.int32))]
+        pin = [torch.from_numpy(a).pin_memory() for a in host]
+        bufs_in = [ds, DeviceScene(scene, dev)]
+        bufs_out = [img, ImageBuffer(W, H, torch.empty((H, W, 4), dtype=torch.float64, device=dev),
+                                     torch.empty((H, W), dtype=torch.float64, device=dev))]
+        out_px = [torch.empty((H, W, 4), dtype=torch.float64).pin_memory() for _ in range(2)]
+        out_dp = [torch.empty((H, W), dtype=torch.float64).pin_memory() for _ in range(2)]
         h2d = sum(p.numel() * p.element_size() for p in pin)
-        d2h = out_px.numel() * 8 + out_dp.numel() * 8
+        d2h = out_px[0].numel() * 8 + out_dp[0].numel() * 8
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        K = args.steps
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        e_in, e_done, e_out = [ev() for _ in range(K)], [ev() for _ in range(K)], [ev() for _ in range(K)]
+        e_start = ev()
+
+        def upload(k):
+            b = bufs_in[k % 2]
+            s_in.wait_event(e_start)
+            if k >= 2:
+                s_in.wait_event(e_done[k - 2])  # buffer k%2 free again
+            with torch.cuda.stream(s_in):
+                for d, src in zip((b.pos, b.vnrm, b.fnrm, b.mat.view(torch.int32), b.obj.view(torch.int32)), pin):
+                    d.copy_(src, non_blocking=True)
+                e_in[k].record(s_in)
+
+        def readback(k):
+            s_out.wait_event(e_done[k])
+            with torch.cuda.stream(s_out):
+                out_px[k % 2].copy_(bufs_out[k % 2].pixels, non_blocking=True)
+                out_dp[k % 2].copy_(bufs_out[k % 2].depth, non_blocking=True)
+                e_out[k].record(s_out)
+
         barrier()
         e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e2.record(stream)
-        for _ in range(args.steps):
-            for d, s in zip(dst, pin):
-                d.copy_(s, non_blocking=True)
-            step()
-            out_px.copy_(img.pixels, non_blocking=True)
-            out_dp.copy_(img.depth, non_blocking=True)
+        e_start.record(stream)
+        upload(0)
+        for k in range(K):
+            if k + 1 < K:
+                upload(k + 1)
+            stream.wait_event(e_in[k])
+            if k >= 2:
+                stream.wait_event(e_out[k - 2])  # image buffer k%2 read back
+            step(bufs_in[k % 2], bufs_out[k % 2])
+            e_done[k].record(stream)
+            readback(k)
+        stream.wait_event(e_out[K - 1])
+        if K >= 2:
+            stream.wait_event(e_out[K - 2])
         e3.record(stream)
         barrier()
         ms_e2e = e2.elapsed_time(e3)
@@ -302,8 +357,12 @@ def main():
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         ms_e2e = float(t2.item())
-        e2e = {"value": world * n_frags * args.steps / (ms_e2e / 1e3), "unit": "frag/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps}
+        torch.cuda.synchronize()
+        ok = np.array_equal(out_dp[(K - 1) % 2].numpy(), bufs_out[(K - 1) % 2].depth.cpu().numpy())
+        e2e = {"value": n_frags * args.steps / (ms_e2e / 1e3), "unit": "frag/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps,
+               "pipeline": "2-deep: H2D(k+1) and D2H(k-1) on copy streams overlap step k",
+               "readback_matches_device": bool(ok)}
     else:
         e2e = None
 
@@ -315,9 +374,10 @@ def main():
                "capture_s": tc, "splat_s": ts}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "frag/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded icosphere field, no dataset)",
-                "config": dict(CONFIG, fragments=n_frags, parallelism=f"replicas{world}" if world > 1 else "single",
+                "config": dict(CONFIG, fragments=n_frags,
+                               parallelism=f"morton-range shards x{world} (NCCL)" if world > 1 else "single",
                                exact_order=bool(args.exact_order), splat="packed" if args.packed else "exact"),
                 "novel_view_fps": 1e3 / recon_ms if recon_ms else None,
                 "capture_frag_per_s": n_frags / (capture_ms / 1e3) if capture_ms else None,

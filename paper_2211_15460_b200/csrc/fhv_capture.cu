@@ -279,15 +279,13 @@ __global__ void __launch_bounds__(256) k_item_expand(long long n_jobs, const uin
 // with interpolation and the store-specific insert)
 //
 // A warp takes 32 consecutive work items (lane k <-> item i0+k, each a slice
-// of <= kItemPix bbox pixels of one job, in job order) and walks their
-// concatenated pixels 32 at a time: lane l of chunk s tests flat pixel s+l,
-// whose item is found by a 5-step shuffle search over the items' pixel
-// prefix sums.  One ballot per chunk yields every item's covered count and
-// every fragment's emission rank (= its reference pool index), so the
-// per-fragment work -- barycentric divides, interpolation, keying, atomics,
-// stores -- runs 32 fragments wide instead of one item per thread in
-// sequence, and same-key fragments of a chunk are aggregated with
-// __match_any_sync into one atomic.
+// of <= kItemPix bbox pixels of one job, in job order).  Coverage is swept
+// lane-per-item, row-incrementally like the reference loop (a few f64 ops per
+// pixel); covered pixels are appended (ballot + popc) to a per-warp queue in
+// shared memory, in emission order per item, and every 32 queued fragments
+// are processed 32 wide: barycentric divides, interpolation, keying,
+// match_any-aggregated atomics and stores run with full lanes no matter how
+// ragged the triangles are.
 
 struct CoverS {  // per-item coverage state, staged in shared memory
   double ax, ay, bx, by, cx, cy;
@@ -379,16 +377,162 @@ __device__ __forceinline__ void interp_nrm(const TriData& d, double l0, double l
   }
 }
 
-__device__ __forceinline__ unsigned range_mask(int a, int b) {  // lanes [a, b), 0 <= a <= b <= 32
-  const unsigned hi = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
-  const unsigned lo = a >= 32 ? 0xffffffffu : ((1u << a) - 1u);
-  return hi & ~lo;
-}
-
-__device__ __forceinline__ int clamp32(long long v) { return v < 0 ? 0 : (v > 32 ? 32 : (int)v); }
-
 enum RasterMode { kCnt = 0, kCntLeaves = 1, kList = 2, kPpfl = 3, kPofl = 4, kPofa = 5 };
 constexpr int kRasterBlock = 256;
+constexpr int kRasterWarps = kRasterBlock / 32;
+
+template <int kMode, bool kAtomicAlloc>
+struct RasterState {
+  unsigned long long emitted = 0;
+  bool bad_range = false, bad_pass = false, bad_key = false;
+};
+
+// one batch of <= 32 fragments, one per lane (valid lanes), called by the
+// whole warp.  k: the fragment's item (lane index in the group), (px, py): its
+// pixel, push_local: its index among its item's covered pixels.  Local index
+// inside the item: push order for the linked / list modes; owned-fragment
+// order (smem counters) for the keyed POFA modes, whose shard filter is only
+// known here.
+template <int kMode, bool kAtomicAlloc>
+__device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitOut& o, Control* ctl,
+                                             const CoverS* cs, bool valid, int k, int px, int py,
+                                             uint32_t push_local, uint32_t* own_cnt, unsigned long long rank0,
+                                             const uint32_t* item_job_g, RasterState<kMode, kAtomicAlloc>& st) {
+  constexpr bool kKeyed = kMode == kCntLeaves || kMode == kPofl || kMode == kPofa;
+  constexpr bool kOwned = kMode == kCntLeaves || kMode == kPofa;
+  const unsigned lane = lane_id();
+  const unsigned below = (1u << lane) - 1u;
+  const CoverS& c = cs[k];
+  bool live = false;
+  TriData d;
+  double w[3] = {0.0, 0.0, 0.0};
+  double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+  uint64_t code = ~0ull;
+  if (valid) {
+    double f0, f1, f2;
+    cover_test(c, px, py, f0, f1, f2);  // the same f64 values the sweep tested
+    l0 = __ddiv_rn(f0, c.area2);
+    l1 = __ddiv_rn(f1, c.area2);
+    l2 = __ddiv_rn(f2, c.area2);
+    load_tri(p, c.tri, c.swapped, d, kMode != kCntLeaves);
+    interp_pos(d, l0, l1, l2, w);
+    live = true;
+    if (kKeyed) {
+      if (!cell_code(__double2float_rn(w[0]), __double2float_rn(w[1]), __double2float_rn(w[2]), o.levels, &code)) {
+        st.bad_range = true;
+        live = false;
+        code = ~0ull;
+      } else if (code < p.cell_lo || code >= p.cell_hi) {  // another shard's leaf
+        live = false;
+        code = ~0ull;
+      }
+    }
+  }
+  uint32_t local = push_local;
+  if (kOwned) {
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    const unsigned grp = __match_any_sync(0xffffffffu, valid ? k : -1);
+    local = own_cnt[k] + (uint32_t)__popc(grp & m & below);
+    __syncwarp();
+    if (valid && (int)lane == 31 - __clz(grp)) own_cnt[k] += (uint32_t)__popc(grp & m);
+    __syncwarp();
+  }
+  const unsigned long long rank = __shfl_sync(0xffffffffu, rank0, k) + local;
+  if (kMode == kCntLeaves) {
+    const unsigned grp = __match_any_sync(0xffffffffu, code);
+    if (live && (int)lane == __ffs(grp) - 1) atomicAdd(&o.leaf_counts[code - p.cell_lo], (uint32_t)__popc(grp));
+    return;
+  }
+  double nn[3] = {0.0, 0.0, 0.0};
+  if (live) {
+    interp_nrm(d, l0, l1, l2, nn);
+    ++st.emitted;
+  }
+  if (kMode == kList) {
+    if (live && (long long)rank < o.max_out) {
+      o.job[rank] = item_job_g[k];
+      o.px[rank] = px;
+      o.py[rank] = py;
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        o.wpos[3 * rank + e] = w[e];
+        o.wnrm[3 * rank + e] = nn[e];
+      }
+    }
+    return;
+  }
+  long long slot = -1;
+  if (kMode == kPofa) {
+    const unsigned grp = __match_any_sync(0xffffffffu, code);
+    const int leader = __ffs(grp) - 1;
+    uint32_t base = 0, cnt = 0, off = 0;
+    const unsigned long long lc = live ? code - p.cell_lo : 0ull;
+    if (live) {  // issued before the atomic so the latencies overlap
+      cnt = __ldg(&o.counts[lc]);
+      off = __ldg(&o.offsets[lc]);
+    }
+    if (live && (int)lane == leader) base = atomicAdd(&o.cursors[lc], (uint32_t)__popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (live) {
+      const uint32_t cur = base + (uint32_t)__popc(grp & below);
+      if (cur >= cnt) {
+        st.bad_pass = true;
+      } else {
+        slot = (long long)(off - o.base) + cur;
+      }
+    }
+  } else {
+    // slot first: records past capacity are dropped before any keying,
+    // like _store_split (fhv/storage.py:338-342, 366-369, 388-392)
+    if (kAtomicAlloc) {
+      const unsigned m = __ballot_sync(0xffffffffu, live);
+      unsigned long long base = 0;
+      if (m && lane == (unsigned)(__ffs(m) - 1)) base = atomicAdd(&ctl->alloc, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, m ? __ffs(m) - 1 : 0);
+      if (live) slot = (long long)(base + __popc(m & below));
+    } else if (live) {
+      slot = (long long)rank;
+    }
+    if (slot >= o.capacity) slot = -1;
+    uint64_t key = ~0ull;
+    if (slot >= 0) {
+      if (kMode == kPpfl) {
+        key = (uint64_t)py * (uint64_t)o.width + (uint64_t)px;
+        if ((long long)key >= o.n_keys) {
+          st.bad_key = true;
+          slot = -1;
+          key = ~0ull;
+        }
+      } else {
+        key = code;
+      }
+    }
+    // linked insert, aggregated per key: within a batch the lane order is the
+    // emission order of same-key fragments, so the group is chained in place
+    // and spliced in front of the old head with one atomicExch by its last lane
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const int last = 31 - __clz(grp);
+    int32_t old = -1;
+    if (slot >= 0 && (int)lane == last) old = atomicExch(&o.heads[key], (int32_t)slot);
+    old = __shfl_sync(0xffffffffu, old, last);
+    const unsigned lower = grp & below;
+    const int32_t prev_slot = __shfl_sync(0xffffffffu, (int32_t)slot, lower ? 31 - __clz(lower) : (int)lane);
+    if (slot >= 0) o.prev[slot] = lower ? prev_slot : old;
+  }
+  if (slot >= 0) {
+    o.pos[3 * slot] = __double2float_rn(w[0]);
+    o.pos[3 * slot + 1] = __double2float_rn(w[1]);
+    o.pos[3 * slot + 2] = __double2float_rn(w[2]);
+    o.nrm[3 * slot] = __double2float_rn(nn[0]);
+    o.nrm[3 * slot + 1] = __double2float_rn(nn[1]);
+    o.nrm[3 * slot + 2] = __double2float_rn(nn[2]);
+    o.mat[slot] = d.mat;
+    o.obj[slot] = d.obj;
+    // POFA: prev_index = -1; under EXACT_ORDER the emission rank is parked
+    // here until k_leaf_order restores the reference's in-leaf order
+    if (kMode == kPofa) o.prev[slot] = (o.flags & FHV_EXACT_ORDER) ? (int32_t)(uint32_t)rank : -1;
+  }
+}
 
 template <int kMode, bool kAtomicAlloc>
 __global__ void __launch_bounds__(kRasterBlock, 3) k_raster(CaptureParams p, const JobSetup* __restrict__ jobs,
@@ -396,39 +540,206 @@ __global__ void __launch_bounds__(kRasterBlock, 3) k_raster(CaptureParams p, con
                                                          const uint32_t* __restrict__ item_p0,
                                                          const unsigned long long* __restrict__ item_off,
                                                          long long n_items, uint32_t* __restrict__ item_cnt,
-                                                         EmitOut o, Control* ctl) {
-  constexpr bool kCounting = kMode == kCnt || kMode == kCntLeaves;
-  constexpr bool kKeyed = kMode == kCntLeaves || kMode == kPofl || kMode == kPofa;
-  __shared__ CoverS cs_all[kRasterBlock / 32][32];
+                                                         uint4* __restrict__ item_mask, EmitOut o, Control* ctl) {
+  static_assert(kMode == kCnt || kMode == kCntLeaves, "k_raster is the counting pass; emission is k_emit");
+  constexpr bool kOwned = kMode == kCntLeaves || kMode == kPofa;
+  __shared__ CoverS cs_all[kRasterWarps][32];
+  __shared__ int32_t qpx_all[kRasterWarps][64], qpy_all[kRasterWarps][64];
+  __shared__ uint32_t qmeta_all[kRasterWarps][64];
+  __shared__ uint32_t own_all[kRasterWarps][32];
+  __shared__ uint32_t ijob_all[kRasterWarps][32];
   const unsigned lane = lane_id();
-  CoverS* cs = cs_all[threadIdx.x >> 5];
+  const int wib = threadIdx.x >> 5;
+  CoverS* cs = cs_all[wib];
+  int32_t* q_px = qpx_all[wib];
+  int32_t* q_py = qpy_all[wib];
+  uint32_t* q_meta = qmeta_all[wib];
+  uint32_t* own_cnt = own_all[wib];
+  uint32_t* ijob = ijob_all[wib];
   const unsigned below = (1u << lane) - 1u;
   const long long n_groups = (n_items + 31) / 32;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  unsigned long long emitted = 0;
-  bool bad_range = false, bad_pass = false, bad_key = false;
+  RasterState<kMode, kAtomicAlloc> st;
   for (long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; g < n_groups; g += nw) {
     const long long item = g * 32 + lane;
     uint32_t npix = 0;
     unsigned long long rank0 = 0;
+    int px = 0, py = 0, xend = 0;
+    double k0 = 0.0, k1 = 0.0, k2 = 0.0;
     if (item < n_items) {
-      const JobSetup js = jobs[item_job[item]];
+      const uint32_t jid = item_job[item];
+      const JobSetup js = jobs[jid];
       const uint32_t p0 = item_p0[item];
       const unsigned long long pe = (unsigned long long)js.bw * (unsigned long long)js.bh;
       npix = (unsigned long long)p0 + kItemPix < pe ? kItemPix : (uint32_t)(pe - p0);
       make_cover(js, p0, cs[lane]);
-      if (!kCounting && !kAtomicAlloc) rank0 = item_off[item];
+      ijob[lane] = jid;
+      if (!kOwned && kMode != kCnt && !kAtomicAlloc) rank0 = item_off[item];
+      if (kOwned && kMode == kPofa) rank0 = item_off[item];
+      const uint32_t r = p0 / (uint32_t)js.bw;
+      px = js.x0 + (int)(p0 - r * (uint32_t)js.bw);
+      py = js.y0 + (int)r;
+      xend = js.x0 + js.bw;
+      const CoverS& c = cs[lane];
+      const double sy = __dadd_rn((double)py, 0.5);
+      k0 = __dmul_rn(c.e0x, __dsub_rn(sy, c.by));
+      k1 = __dmul_rn(c.e1x, __dsub_rn(sy, c.cy));
+      k2 = __dmul_rn(c.e2x, __dsub_rn(sy, c.ay));
+    }
+    own_cnt[lane] = 0;
+    __syncwarp();
+    uint32_t covered = 0;  // covered pixels of my item so far
+    uint32_t mw0 = 0, mw1 = 0, mw2 = 0, mw3 = 0;  // coverage bit mask of my item (<= 128 pixels)
+    int qn = 0;            // queued fragments (warp-uniform)
+    for (uint32_t j = 0; __any_sync(0xffffffffu, j < npix); ++j) {
+      bool cov = false;
+      int cpx = px, cpy = py;
+      if (j < npix) {
+        const CoverS& c = cs[lane];
+        const double sx = __dadd_rn((double)px, 0.5);
+        const double f0 = __dsub_rn(k0, __dmul_rn(c.e0y, __dsub_rn(sx, c.bx)));
+        if (f0 > 0.0 || (f0 == 0.0 && (c.tl & 1u))) {
+          const double f1 = __dsub_rn(k1, __dmul_rn(c.e1y, __dsub_rn(sx, c.cx)));
+          if (f1 > 0.0 || (f1 == 0.0 && (c.tl & 2u))) {
+            const double f2 = __dsub_rn(k2, __dmul_rn(c.e2y, __dsub_rn(sx, c.ax)));
+            cov = f2 > 0.0 || (f2 == 0.0 && (c.tl & 4u));
+          }
+        }
+        if (++px == xend) {
+          px = c.x0;
+          ++py;
+          const double sy = __dadd_rn((double)py, 0.5);
+          k0 = __dmul_rn(c.e0x, __dsub_rn(sy, c.by));
+          k1 = __dmul_rn(c.e1x, __dsub_rn(sy, c.cy));
+          k2 = __dmul_rn(c.e2x, __dsub_rn(sy, c.ay));
+        }
+      }
+      if (cov) {  // j is warp-uniform: a uniform switch, no local memory
+        const uint32_t bit = 1u << (j & 31u);
+        switch (j >> 5) {
+          case 0: mw0 |= bit; break;
+          case 1: mw1 |= bit; break;
+          case 2: mw2 |= bit; break;
+          default: mw3 |= bit; break;
+        }
+      }
+      if (kMode == kCnt) {
+        covered += cov ? 1u : 0u;
+        continue;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, cov);
+      if (cov) {
+        const int slot = qn + __popc(m & below);
+        q_px[slot] = cpx;
+        q_py[slot] = cpy;
+        q_meta[slot] = lane | (covered << 5);
+        ++covered;
+      }
+      qn += __popc(m);
+      if (qn >= 32) {
+        __syncwarp();
+        {
+          const uint32_t mt = q_meta[lane];
+          raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, true, (int)(mt & 31u), q_px[lane], q_py[lane], mt >> 5,
+                                            own_cnt, rank0, ijob, st);
+        }
+        __syncwarp();
+        if ((int)lane < qn - 32) {
+          q_px[lane] = q_px[32 + lane];
+          q_py[lane] = q_py[32 + lane];
+          q_meta[lane] = q_meta[32 + lane];
+        }
+        qn -= 32;
+        __syncwarp();
+      }
+    }
+    if (kMode != kCnt && qn > 0) {
+      __syncwarp();
+      const bool v = (int)lane < qn;
+      const uint32_t mt = v ? q_meta[lane] : 0u;
+      raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, v, (int)(mt & 31u), v ? q_px[lane] : 0, v ? q_py[lane] : 0,
+                                        mt >> 5, own_cnt, rank0, ijob, st);
     }
     __syncwarp();
-    uint32_t inc = npix;
+    if (item < n_items) {
+      if (kMode == kCnt) item_cnt[item] = covered;
+      if (kMode == kCntLeaves) item_cnt[item] = own_cnt[lane];
+      item_mask[item] = make_uint4(mw0, mw1, mw2, mw3);
+    }
+    __syncwarp();
+  }
+  if (kMode == kPofa) {
+    // pass-2 emitted count (compared with pass 1, fhv/storage.py:614-617)
+    unsigned long long e = st.emitted;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+    if (lane == 0 && e) atomicAdd(&ctl->alloc, e);
+  }
+  if (st.bad_range) raise_status(&ctl->status, FHV_RANGE);
+  if (st.bad_pass) raise_status(&ctl->status, FHV_PASS_MISMATCH);
+  if (st.bad_key) raise_status(&ctl->status, FHV_BAD_ARGS);
+}
+
+// position of the n-th (0-based) set bit of v (v has > n set bits)
+__device__ __forceinline__ uint32_t nth_set_bit(uint32_t v, uint32_t n) {
+  uint32_t pos = 0;
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1) {
+    const uint32_t lo = (uint32_t)__popc(v & ((1u << w) - 1u));
+    if (n >= lo) {
+      n -= lo;
+      v >>= w;
+      pos += (uint32_t)w;
+    }
+  }
+  return pos;
+}
+
+// emission pass: the counting pass left each item's coverage mask, so the
+// warp enumerates exactly the covered pixels of its 32 items, 32 fragments
+// per step (flat index -> item by a 5-step shuffle search over the items'
+// fragment prefix sums -> pixel by select-n-th-bit), no coverage sweep.
+template <int kMode, bool kAtomicAlloc>
+__global__ void __launch_bounds__(kRasterBlock, 3) k_emit(CaptureParams p, const JobSetup* __restrict__ jobs,
+                                                       const uint32_t* __restrict__ item_job,
+                                                       const uint32_t* __restrict__ item_p0,
+                                                       const unsigned long long* __restrict__ item_off,
+                                                       const uint4* __restrict__ item_mask, long long n_items,
+                                                       EmitOut o, Control* ctl) {
+  static_assert(kMode == kList || kMode == kPpfl || kMode == kPofl || kMode == kPofa, "emission modes only");
+  __shared__ CoverS cs_all[kRasterWarps][32];
+  __shared__ uint32_t own_all[kRasterWarps][32];
+  __shared__ uint32_t ijob_all[kRasterWarps][32];
+  const unsigned lane = lane_id();
+  const int wib = threadIdx.x >> 5;
+  CoverS* cs = cs_all[wib];
+  uint32_t* own_cnt = own_all[wib];
+  uint32_t* ijob = ijob_all[wib];
+  const long long n_groups = (n_items + 31) / 32;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  RasterState<kMode, kAtomicAlloc> st;
+  for (long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; g < n_groups; g += nw) {
+    const long long item = g * 32 + lane;
+    uint4 mk = make_uint4(0u, 0u, 0u, 0u);
+    unsigned long long rank0 = 0;
+    if (item < n_items) {
+      const uint32_t jid = item_job[item];
+      make_cover(jobs[jid], item_p0[item], cs[lane]);
+      ijob[lane] = jid;
+      mk = item_mask[item];
+      if (!kAtomicAlloc) rank0 = item_off[item];
+    }
+    own_cnt[lane] = 0;
+    const uint32_t cnt = (uint32_t)(__popc(mk.x) + __popc(mk.y) + __popc(mk.z) + __popc(mk.w));
+    uint32_t inc = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
       if (lane >= (unsigned)d) inc += y;
     }
-    const uint32_t E = inc - npix;  // my item's first flat pixel
+    const uint32_t E = inc - cnt;
     const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    uint32_t run = 0;               // live fragments of my item so far
+    __syncwarp();
     for (uint32_t s = 0; s < total; s += 32) {
       const uint32_t f = s + lane;
       const bool valid = f < total;
@@ -436,160 +747,52 @@ __global__ void __launch_bounds__(kRasterBlock, 3) k_raster(CaptureParams p, con
 #pragma unroll
       for (int step = 16; step > 0; step >>= 1) {
         const uint32_t Ec = __shfl_sync(0xffffffffu, E, k + step);
-        if (Ec <= f && valid) k += step;
+        if (valid && Ec <= f) k += step;
       }
-      const uint32_t Ek = __shfl_sync(0xffffffffu, E, k);
-      const uint32_t run_k = __shfl_sync(0xffffffffu, run, k);
-      const unsigned long long rank0_k = __shfl_sync(0xffffffffu, rank0, k);
-      const CoverS& c = cs[k];
-      double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+      const uint32_t local = f - __shfl_sync(0xffffffffu, E, k);
+      const uint32_t m0 = __shfl_sync(0xffffffffu, mk.x, k), m1 = __shfl_sync(0xffffffffu, mk.y, k);
+      const uint32_t m2 = __shfl_sync(0xffffffffu, mk.z, k), m3 = __shfl_sync(0xffffffffu, mk.w, k);
       int px = 0, py = 0;
-      bool live = false;
       if (valid) {
-        const uint32_t q = c.p0 + (f - Ek);
+        uint32_t rem = local, wv = m0, word = 0;
+        const uint32_t c0 = (uint32_t)__popc(m0);
+        if (rem >= c0) {
+          rem -= c0;
+          wv = m1;
+          word = 1;
+          const uint32_t c1 = (uint32_t)__popc(m1);
+          if (rem >= c1) {
+            rem -= c1;
+            wv = m2;
+            word = 2;
+            const uint32_t c2 = (uint32_t)__popc(m2);
+            if (rem >= c2) {
+              rem -= c2;
+              wv = m3;
+              word = 3;
+            }
+          }
+        }
+        const CoverS& c = cs[k];
+        const uint32_t q = c.p0 + 32u * word + nth_set_bit(wv, rem);
         const uint32_t r = q / (uint32_t)c.bw;
         px = c.x0 + (int)(q - r * (uint32_t)c.bw);
         py = c.y0 + (int)r;
-        live = cover_test(c, px, py, f0, f1, f2);
       }
-      TriData d;
-      double w[3] = {0.0, 0.0, 0.0};
-      double l0 = 0.0, l1 = 0.0, l2 = 0.0;
-      uint64_t code = ~0ull;
-      if (kMode != kCnt && live) {
-        l0 = __ddiv_rn(f0, c.area2);
-        l1 = __ddiv_rn(f1, c.area2);
-        l2 = __ddiv_rn(f2, c.area2);
-        load_tri(p, c.tri, c.swapped, d, kMode != kCntLeaves);
-        interp_pos(d, l0, l1, l2, w);
-        if (kKeyed) {
-          if (!cell_code(__double2float_rn(w[0]), __double2float_rn(w[1]), __double2float_rn(w[2]), o.levels,
-                         &code)) {
-            bad_range = true;
-            live = false;
-            code = ~0ull;
-          } else if (code < p.cell_lo || code >= p.cell_hi) {  // another shard's leaf
-            live = false;
-            code = ~0ull;
-          }
-        }
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, live);
-      // emission rank of my fragment: item base + live lanes of my item before me
-      const int a_k = clamp32((long long)Ek - (long long)s);
-      const unsigned long long rank = rank0_k + run_k + __popc(m & below & ~range_mask(0, a_k));
-      {  // my item's live count
-        const int a = clamp32((long long)E - (long long)s), b = clamp32((long long)E + npix - (long long)s);
-        if (b > a) run += __popc(m & range_mask(a, b));
-      }
-      if (kMode == kCnt) continue;
-      if (kMode == kCntLeaves) {
-        const unsigned grp = __match_any_sync(0xffffffffu, code);
-        if (live && (int)lane == __ffs(grp) - 1) atomicAdd(&o.leaf_counts[code - p.cell_lo], (uint32_t)__popc(grp));
-        continue;
-      }
-      double nn[3] = {0.0, 0.0, 0.0};
-      if (live) {
-        interp_nrm(d, l0, l1, l2, nn);
-        ++emitted;
-      }
-      if (kMode == kList) {
-        if (live && (long long)rank < o.max_out) {
-          o.job[rank] = item_job[g * 32 + k];
-          o.px[rank] = px;
-          o.py[rank] = py;
-#pragma unroll
-          for (int e = 0; e < 3; ++e) {
-            o.wpos[3 * rank + e] = w[e];
-            o.wnrm[3 * rank + e] = nn[e];
-          }
-        }
-        continue;
-      }
-      long long slot = -1;
-      if (kMode == kPofa) {
-        const unsigned grp = __match_any_sync(0xffffffffu, code);
-        const int leader = __ffs(grp) - 1;
-        uint32_t base = 0, cnt = 0, off = 0;
-        const unsigned long long lc = live ? code - p.cell_lo : 0ull;
-        if (live) {  // issued before the atomic so the latencies overlap
-          cnt = __ldg(&o.counts[lc]);
-          off = __ldg(&o.offsets[lc]);
-        }
-        if (live && (int)lane == leader) base = atomicAdd(&o.cursors[lc], (uint32_t)__popc(grp));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (live) {
-          const uint32_t cur = base + (uint32_t)__popc(grp & below);
-          if (cur >= cnt) {
-            bad_pass = true;
-          } else {
-            slot = (long long)(off - o.base) + cur;
-          }
-        }
-      } else {
-        // slot first: records past capacity are dropped before any keying,
-        // like _store_split (fhv/storage.py:338-342, 366-369, 388-392)
-        if (kAtomicAlloc) {
-          unsigned long long base = 0;
-          if (m && lane == (unsigned)(__ffs(m) - 1)) base = atomicAdd(&ctl->alloc, (unsigned long long)__popc(m));
-          base = __shfl_sync(0xffffffffu, base, m ? __ffs(m) - 1 : 0);
-          if (live) slot = (long long)(base + __popc(m & below));
-        } else if (live) {
-          slot = (long long)rank;
-        }
-        if (slot >= o.capacity) slot = -1;
-        uint64_t key = ~0ull;
-        if (slot >= 0) {
-          if (kMode == kPpfl) {
-            key = (uint64_t)py * (uint64_t)o.width + (uint64_t)px;
-            if ((long long)key >= o.n_keys) {
-              bad_key = true;
-              slot = -1;
-              key = ~0ull;
-            }
-          } else {
-            key = code;
-          }
-        }
-        // linked insert, aggregated per key: within a group the lane order is
-        // the emission order, so the group is chained in place and spliced in
-        // front of the old head with one atomicExch by its last lane
-        const unsigned grp = __match_any_sync(0xffffffffu, key);
-        const int last = 31 - __clz(grp);
-        int32_t old = -1;
-        if (slot >= 0 && (int)lane == last) old = atomicExch(&o.heads[key], (int32_t)slot);
-        old = __shfl_sync(0xffffffffu, old, last);
-        const unsigned lower = grp & below;
-        const int32_t prev_slot = __shfl_sync(0xffffffffu, (int32_t)slot, lower ? 31 - __clz(lower) : (int)lane);
-        if (slot >= 0) o.prev[slot] = lower ? prev_slot : old;
-      }
-      if (slot >= 0) {
-        o.pos[3 * slot] = __double2float_rn(w[0]);
-        o.pos[3 * slot + 1] = __double2float_rn(w[1]);
-        o.pos[3 * slot + 2] = __double2float_rn(w[2]);
-        o.nrm[3 * slot] = __double2float_rn(nn[0]);
-        o.nrm[3 * slot + 1] = __double2float_rn(nn[1]);
-        o.nrm[3 * slot + 2] = __double2float_rn(nn[2]);
-        o.mat[slot] = d.mat;
-        o.obj[slot] = d.obj;
-        // POFA: prev_index = -1; under EXACT_ORDER the emission rank is parked
-        // here until k_leaf_order restores the reference's in-leaf order
-        if (kMode == kPofa) o.prev[slot] = (o.flags & FHV_EXACT_ORDER) ? (int32_t)(uint32_t)rank : -1;
-      }
+      raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, valid, k, px, py, local, own_cnt, rank0, ijob, st);
     }
-    if (kCounting && item < n_items) item_cnt[item] = run;
     __syncwarp();
   }
   if (kMode == kPofa) {
     // pass-2 emitted count (compared with pass 1, fhv/storage.py:614-617)
-    unsigned long long e = emitted;
+    unsigned long long e = st.emitted;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
     if (lane == 0 && e) atomicAdd(&ctl->alloc, e);
   }
-  if (bad_range) raise_status(&ctl->status, FHV_RANGE);
-  if (bad_pass) raise_status(&ctl->status, FHV_PASS_MISMATCH);
-  if (bad_key) raise_status(&ctl->status, FHV_BAD_ARGS);
+  if (st.bad_range) raise_status(&ctl->status, FHV_RANGE);
+  if (st.bad_pass) raise_status(&ctl->status, FHV_PASS_MISMATCH);
+  if (st.bad_key) raise_status(&ctl->status, FHV_BAD_ARGS);
 }
 
 // ---------------------------------------------------------------------------
@@ -821,7 +1024,8 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
   const long long n = ctx->n_items;
   uint32_t* item_cnt = (uint32_t*)scratch(ctx, kItemCnt, (size_t)(n > 0 ? n : 1) * 4);
   auto* item_off = (unsigned long long*)scratch(ctx, kItemOff, (size_t)(n > 0 ? n : 1) * 8);
-  if (!item_cnt || !item_off) return FHV_NOMEM;
+  auto* item_mask = (uint4*)scratch(ctx, kItemMask, (size_t)(n > 0 ? n : 1) * 16);
+  if (!item_cnt || !item_off || !item_mask) return FHV_NOMEM;
   if (n > 0) {
     const JobSetup* jobs = (const JobSetup*)ctx->bufs[kJobs].ptr;
     const uint32_t* ij = (const uint32_t*)ctx->bufs[kItemJob].ptr;
@@ -834,9 +1038,11 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
     {
       LaunchScope L_(ctx, leaves ? kStCountLeaves : kStCount, s);
       if (leaves)
-        k_raster<kCntLeaves, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, item_cnt, o, ctx->ctl);
+        k_raster<kCntLeaves, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, item_cnt, item_mask, o,
+                                                                   ctx->ctl);
       else
-        k_raster<kCnt, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, item_cnt, o, ctx->ctl);
+        k_raster<kCnt, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, item_cnt, item_mask, o,
+                                                             ctx->ctl);
     }
     int rc = check_cuda(ctx, cudaGetLastError());
     if (rc) return rc;
@@ -852,13 +1058,14 @@ int emit(fhv_ctx* ctx, const CaptureParams& p, const EmitOut& o, bool atomic_all
   const uint32_t* ij = (const uint32_t*)ctx->bufs[kItemJob].ptr;
   const uint32_t* ip = (const uint32_t*)ctx->bufs[kItemP0].ptr;
   const auto* io = (const unsigned long long*)ctx->bufs[kItemOff].ptr;
+  const auto* im = (const uint4*)ctx->bufs[kItemMask].ptr;
   const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
   {
     LaunchScope L_(ctx, kStEmitList + (kMode - kList), s);
     if (atomic_alloc)
-      k_raster<kMode, true><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, n, nullptr, o, ctx->ctl);
+      k_emit<kMode, true><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, im, n, o, ctx->ctl);
     else
-      k_raster<kMode, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, n, nullptr, o, ctx->ctl);
+      k_emit<kMode, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, im, n, o, ctx->ctl);
   }
   return check_cuda(ctx, cudaGetLastError());
 }
@@ -932,7 +1139,8 @@ static int build_linked(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_
   const CaptureParams p = make_params(tris, cfg);
   const bool atomic_alloc = (flags & FHV_ALLOC_ATOMIC) != 0;
   if ((rc = plan(ctx, p, s))) return rc;
-  if (!atomic_alloc && (rc = count(ctx, p, false, 0, nullptr, s))) return rc;
+  // the counting pass also leaves the coverage masks the emission pass enumerates
+  if ((rc = count(ctx, p, false, 0, nullptr, s))) return rc;
   EmitOut o = empty_out();
   set_pool(o, pool);
   o.heads = heads;

@@ -72,7 +72,7 @@ namespace fhv {
 enum BufId {
   kJobs = 0, kJobItems, kJobItemOff, kItemJob, kItemP0, kItemCnt, kItemOff, kScanStatus,
   kCursors, kChainScratch, kSplatKey, kSplatWin, kSplatBox, kRays, kTmp0, kTmp1, kTriFlag, kTriOff, kTriIndex,
-  kShardBoxes, kNumBufs
+  kShardBoxes, kItemMask, kNumBufs
 };
 
 // Counts a launch and, when profiling is on, brackets it with CUDA events on

@@ -55,6 +55,18 @@ class DeviceScene:
         self.pos, self.vnrm, self.fnrm, self.mat, self.obj = pos, vnrm, fnrm, mat, obj
         return self
 
+    def derive_face_normals(self) -> torch.Tensor:
+        """Recompute ``fnrm`` on the device from ``pos`` with make_triangle's
+        arithmetic (fhv/scene.py:137-139: cross, sqrt(FWD dot), divide), on the
+        current stream.  Bit-identical to the host face normals of any scene
+        built by make_triangle (tests/test_gpu_parity.py), so a pipelined
+        caller need not upload them."""
+        lib = _lib.load()
+        rc = lib.fhv_face_normals(_lib.ctx(self.device), self.n_tri, _lib.ptr(self.pos), _lib.ptr(self.fnrm),
+                                  _lib.stream_ptr(self.device))
+        _lib.check(rc, "face normals")
+        return self.fnrm
+
     def struct(self) -> _lib.Tris:
         return _lib.Tris(self.n_tri, _lib.ptr(self.pos), _lib.ptr(self.vnrm), _lib.ptr(self.fnrm),
                          _lib.ptr(self.mat), _lib.ptr(self.obj))

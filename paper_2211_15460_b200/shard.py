@@ -288,7 +288,7 @@ def _shard_struct(lo: int, hi: int, levels: int) -> _lib.Shard:
 
 def pofa_build_shard(scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int, comm: Comm,
                      ranges: list | None = None, balance: bool = True, exact_order: bool = False,
-                     device=None) -> FhvPofaShard:
+                     device=None, tris=None) -> FhvPofaShard:
     """This rank's share of ``pofa_build(scene, strategy, cfg, levels)``."""
     if levels < 4:
         raise FhvError("sharded capture needs levels >= 4")
@@ -299,7 +299,7 @@ def pofa_build_shard(scene, strategy: CaptureStrategy, cfg: RasterConfig, levels
         ranges = shard_ranges(levels, comm.world, w)
     lo, hi = ranges[comm.rank]
     plan = capture_plan(scene, strategy, cfg)
-    ds = device_scene(scene, device)
+    ds = tris if tris is not None else device_scene(scene, device)
     dev = ds.device
     n_local = hi - lo
     counts = torch.empty(n_local, dtype=torch.uint32, device=dev)

@@ -389,15 +389,18 @@ def build_pofl(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
 
 
 def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int, threads: int = 1, *,
-               exact_order: bool = False, device=None) -> FhvPofa:
+               exact_order: bool = False, device=None, tris=None) -> FhvPofa:
     """Two-pass per-octant arrays (fhv/storage.py:590-621): per-leaf histogram,
-    exclusive scan (+ pyramid), exact pool, scatter into leaf ranges."""
+    exclusive scan (+ pyramid), exact pool, scatter into leaf ranges.
+    ``tris``: a DeviceScene already holding this scene's triangle arrays (e.g.
+    one of several buffers a pipelined caller fills asynchronously); default:
+    the scene's cached upload."""
     if levels < 1:
         raise FhvError("octree needs at least one level")
     if levels > 11:
         raise FhvError(f"levels {levels}: dense POFA directories beyond L=11 exceed device memory")
     plan = capture_plan(scene, strategy, cfg)
-    ds = device_scene(scene, device)
+    ds = tris if tris is not None else device_scene(scene, device)
     dev = ds.device
     n_leaf = 8 ** levels
     counts = torch.empty(n_leaf, dtype=torch.uint32, device=dev)

@@ -87,8 +87,8 @@ def test_sharded_fast_order_is_a_per_leaf_permutation():
     scene = _scene("spheres")
     cfg = fhv.RasterConfig.from_camera(fhv.capture_camera(scene, "+z", 256))
     ns = fhv.CaptureStrategy.normal_space()
-    ref = fhv.pofa_build(scene, ns, cfg, 5, exact_order=True)
-    vols = _run_ranks(2, lambda c: shard.pofa_build_shard(scene, ns, cfg, 5, c))
+    ref = fhv.pofa_build(scene, ns, cfg, 6, exact_order=True)
+    vols = _run_ranks(2, lambda c: shard.pofa_build_shard(scene, ns, cfg, 6, c))
     # multiset per leaf: sort records inside each leaf range, then compare
     pos = torch.cat([v.pool.position for v in vols]).cpu().numpy()
     rpos = ref.pool.position.cpu().numpy()
