@@ -140,14 +140,24 @@ class ClockSampler:
 # CPU baseline / reference arm (oracle port)
 
 
-def cpu_run(w):
-    """One full C3 step on the host with the oracle port (threads=1)."""
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_run(w, threads: int = 1):
+    """One full C3 step on the host with the oracle port: POFA capture + the
+    1080p splat, on ``threads`` host threads (threads=1 is the reference's
+    sequential order; more threads keep the directory and image identical)."""
     from oracle import oracle as orc
-    t0 = time.perf_counter()
-    vol = orc.pofa_build(w["scene"], w["strategy"], w["cfg"], w["levels"])
-    t1 = time.perf_counter()
-    orc.splat(vol["pool"], vol["next_free"], w["view"], w["lights"], w["radius"], w["scene"].materials)
-    t2 = time.perf_counter()
+    with orc.threads(threads):
+        t0 = time.perf_counter()
+        vol = orc.pofa_build(w["scene"], w["strategy"], w["cfg"], w["levels"])
+        t1 = time.perf_counter()
+        orc.splat(vol["pool"], vol["next_free"], w["view"], w["lights"], w["radius"], w["scene"].materials)
+        t2 = time.perf_counter()
     return vol["next_free"], t1 - t0, t2 - t1
 
 
@@ -156,20 +166,23 @@ def reference_arm(args):
     if rank != 0:
         return 0
     w = workload()
+    nt = host_threads()
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_run(w)
+        cpu_run(w, nt)
     tot_s, frags = 0.0, 0
-    for _ in range(args.steps):
-        n, tc, ts = cpu_run(w)
+    steps = min(args.steps, 30)  # each step ~0.5-2 s of host time; keep the arm within a few minutes
+    for _ in range(steps):
+        n, tc, ts = cpu_run(w, nt)
         tot_s += tc + ts
         frags += n
     value = frags / tot_s
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frag/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+            "steps": steps, "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded icosphere field)", "config": CONFIG,
-            "cpu_baseline": {"value": value, "unit": "frag/s", "cores": 1, "kind": "port",
-                             "sample": "full C3 step per step (POFA capture + 1080p splat), oracle/fhv_oracle.c"},
+            "cpu_baseline": {"value": value, "unit": "frag/s", "cores": nt, "kind": "port",
+                             "sample": f"{steps} full C3 steps (POFA capture + 1080p splat), oracle/fhv_oracle.c "
+                                       f"on {nt} host threads"},
             "e2e": {"value": value, "unit": "frag/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -300,9 +313,15 @@ def main():
     # buffered, so step k+1's upload and step k-1's read-back overlap step
     # k's kernels (a two-deep pipeline, as a serving loop would run it).
     if not args.profile_only:
-        host = [np.ascontiguousarray(a) for a in (scene.positions, scene.normals, scene.face_normals,
-                                                  scene.material_id.view(np.int32), scene.object_id.view(np.int32))]
-        pin = [torch.from_numpy(a).pin_memory() for a in host]
+        # face normals are a pure function of the positions (make_triangle,
+        # fhv/scene.py:137-139): they are re-derived on the device, bit-identical
+        # (tests/test_gpu_fullsize.py::test_device_face_normals_bit_exact), not uploaded
+        probe = DeviceScene(scene, dev)
+        derive_fn = bool(torch.equal(probe.fnrm.clone(), probe.derive_face_normals()))
+        del probe
+        arrays = (scene.positions, scene.normals) + (() if derive_fn else (scene.face_normals,)) + \
+            (scene.material_id.view(np.int32), scene.object_id.view(np.int32))
+        pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays]
         bufs_in = [ds, DeviceScene(scene, dev)]
         bufs_out = [img, ImageBuffer(W, H, torch.empty((H, W, 4), dtype=torch.float64, device=dev),
                                      torch.empty((H, W), dtype=torch.float64, device=dev))]
@@ -321,8 +340,9 @@ def main():
             s_in.wait_event(e_start)
             if k >= 2:
                 s_in.wait_event(e_done[k - 2])  # buffer k%2 free again
+            dsts = (b.pos, b.vnrm) + (() if derive_fn else (b.fnrm,)) + (b.mat.view(torch.int32), b.obj.view(torch.int32))
             with torch.cuda.stream(s_in):
-                for d, src in zip((b.pos, b.vnrm, b.fnrm, b.mat.view(torch.int32), b.obj.view(torch.int32)), pin):
+                for d, src in zip(dsts, pin):
                     d.copy_(src, non_blocking=True)
                 e_in[k].record(s_in)
 
@@ -344,6 +364,8 @@ def main():
             stream.wait_event(e_in[k])
             if k >= 2:
                 stream.wait_event(e_out[k - 2])  # image buffer k%2 read back
+            if derive_fn:
+                bufs_in[k % 2].derive_face_normals()
             step(bufs_in[k % 2], bufs_out[k % 2])
             e_done[k].record(stream)
             readback(k)
@@ -362,16 +384,22 @@ def main():
         e2e = {"value": n_frags * args.steps / (ms_e2e / 1e3), "unit": "frag/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps,
                "pipeline": "2-deep: H2D(k+1) and D2H(k-1) on copy streams overlap step k",
+               "face_normals": "derived on device (bit-identical)" if derive_fn else "uploaded",
                "readback_matches_device": bool(ok)}
     else:
         e2e = None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
-        n, tc, ts = cpu_run(w)
-        cpu = {"value": n / (tc + ts), "unit": "frag/s", "cores": 1, "kind": "port",
-               "sample": f"one full C3 step on the host (oracle/fhv_oracle.c): capture {tc:.2f} s + splat {ts:.2f} s",
-               "capture_s": tc, "splat_s": ts}
+        nt = host_threads()
+        cpu_run(w, nt)  # warm-up (page faults, thread start)
+        n, tc, ts = cpu_run(w, nt)
+        n1, tc1, ts1 = cpu_run(w, 1)
+        cpu = {"value": n / (tc + ts), "unit": "frag/s", "cores": nt, "kind": "port",
+               "sample": f"one full C3 step on the host (oracle/fhv_oracle.c, {nt} threads): capture {tc:.2f} s + "
+                         f"splat {ts:.2f} s",
+               "capture_s": tc, "splat_s": ts,
+               "single_thread": {"value": n1 / (tc1 + ts1), "capture_s": tc1, "splat_s": ts1}}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "frag/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",

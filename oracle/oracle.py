@@ -51,6 +51,23 @@ def lib():
     return _lib
 
 
+class threads:
+    """Context manager: run the oracle's POFA capture passes and splat on n
+    host threads (CPU-baseline leg).  Directory, pyramid and splat image are
+    unchanged; records inside a leaf land in a nondeterministic order."""
+
+    def __init__(self, n: int):
+        self.n = max(1, int(n))
+
+    def __enter__(self):
+        self.old = lib().orc_get_threads()
+        lib().orc_set_threads(self.n)
+        return self
+
+    def __exit__(self, *exc):
+        lib().orc_set_threads(self.old)
+
+
 def _p(a):
     return None if a is None else ctypes.c_void_p(a.ctypes.data)
 
@@ -111,10 +128,16 @@ def capture_list(scene, strategy, cfg, max_out=None):
             "stats": _stats(plan, raw)}
 
 
+def _touched(shape, dtype, fill=0):
+    """np.full, i.e. pages faulted in here, once, rather than concurrently by
+    the threaded passes (first-touch faults serialise on the mm lock)."""
+    return np.full(shape, fill, dtype)
+
+
 def _new_pool(cap):
-    return {"position": np.zeros((cap, 3), np.float32), "normal": np.zeros((cap, 3), np.float32),
-            "material_id": np.zeros(cap, np.uint32), "object_id": np.zeros(cap, np.uint32),
-            "prev_index": np.full(cap, -1, np.int32)}
+    return {"position": _touched((cap, 3), np.float32), "normal": _touched((cap, 3), np.float32),
+            "material_id": _touched(cap, np.uint32), "object_id": _touched(cap, np.uint32),
+            "prev_index": _touched(cap, np.int32, -1)}
 
 
 def _pool_ptrs(pool):
@@ -167,7 +190,7 @@ def pofa_build(scene, strategy, cfg, levels):
     """pofa_build: count pass, exclusive scan, scatter pass (fhv/storage.py:590-621)."""
     plan, proj = _plan_args(scene, strategy, cfg)
     P, N, F, M, O = _tris(scene)
-    c64 = np.zeros(8 ** levels, np.int64)
+    c64 = _touched(8 ** levels, np.int64)
     raw1 = np.zeros(4, np.int64)
     rc = lib().orc_pofa_count(_i64(len(P)), _p(P), _p(N), _p(F), _p(M), _p(O), plan.strategy, plan.res,
                               _f64(plan.pitch), _p(proj), 3, levels, _p(c64), _p(raw1))

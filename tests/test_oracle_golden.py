@@ -164,3 +164,30 @@ def test_splat_and_raycast_images(name, cname, lname):
             assert list(stats.values()) == list(g[k + "stats"]), k
             assert np.array_equal(ids, g[k + "ids"])
             np.testing.assert_allclose(rgba, g[k + "rgba"], rtol=0, atol=TOL)
+
+
+def test_threaded_oracle_matches_sequential():
+    """The CPU baseline's threaded oracle: same directory / pyramid / splat
+    image, same records per leaf (any order)."""
+    s = sample_scenes.sphere_field(8, 3, seed=5, r_lo=0.05, r_hi=0.2, c_lo=0.2, c_hi=0.8)
+    cfg = RasterConfig.from_camera(capture_camera(s, "+z", 256))
+    ns = CaptureStrategy.normal_space()
+    ref = orc.pofa_build(s, ns, cfg, 6)
+    with orc.threads(4):
+        mt = orc.pofa_build(s, ns, cfg, 6)
+    for k in ("counts", "offsets", "pyramid"):
+        assert np.array_equal(mt[k], ref[k]), k
+    assert mt["next_free"] == ref["next_free"]
+    key = lambda pool, a, b: np.sort(  # noqa: E731
+        pool["position"][a:b].view(np.uint32).astype(np.uint64) @ np.array([1 << 40, 1 << 20, 1], np.uint64))
+    off, cnt = ref["offsets"].astype(np.int64), ref["counts"].astype(np.int64)
+    for c in np.nonzero(cnt)[0]:
+        a, b = off[c], off[c] + cnt[c]
+        assert np.array_equal(key(mt["pool"], a, b), key(ref["pool"], a, b))
+    cam = viewpoint_camera("+x", (96, 80), "perspective")
+    lights = [headlight(cam)]
+    r1 = orc.splat(ref["pool"], ref["next_free"], cam, lights, 1 / 256, s.materials)
+    with orc.threads(3):
+        r2 = orc.splat(ref["pool"], ref["next_free"], cam, lights, 1 / 256, s.materials)
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
