@@ -411,6 +411,7 @@ def main():
                 "capture_frag_per_s": n_frags / (capture_ms / 1e3) if capture_ms else None,
                 "step_gbs": step_bytes / (ms_step / 1e3) / 1e9, "step_bytes": step_bytes,
                 "stage_ms": {k: round(v, 4) for k, v in sorted(stage_ms.items(), key=lambda kv: -kv[1])},
+                "gap_ms_per_step": round(ms_step - sum(stage_ms.values()), 4),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

@@ -51,6 +51,7 @@ enum {
   FHV_NOMEM = 7,          /* MemoryError */
   FHV_TOO_MANY = 8,       /* FhvError: >= 2^32 fragments (fhv/storage.py:604-606) */
   FHV_SPLAT_BIG = 9,      /* SceneError: splat footprint > 4096 px (fhv/render.py:285-286) */
+  FHV_NEED_POOL = 10,     /* fhv_pofa_build: pool smaller than the exact count; *total says how big */
 };
 
 /* capture flags */
@@ -196,6 +197,16 @@ int fhv_pofa_count(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t
 int fhv_pofa_scatter(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg,
                      int32_t levels, const uint32_t *counts, const uint32_t *offsets, fhv_pool_t *pool,
                      int32_t flags, void *stream);
+
+/* pofa_build in one call (fhv/storage.py:590-621): pass 1 + directory +
+   pass 2 with the syncs inside the library.  pool may be NULL or smaller
+   than the exact count: then *total is set, nothing is scattered and
+   FHV_NEED_POOL is returned -- allocate a pool of *total records and finish
+   with fhv_pofa_scatter (the pass-1 state stays in ctx).  A pool larger than
+   *total receives records [0, *total) only. */
+int fhv_pofa_build(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int32_t levels,
+                   uint32_t *counts, uint32_t *offsets, uint8_t *pyramid, fhv_pool_t *pool, int32_t flags,
+                   int64_t *total, void *stream);
 
 /* Sharded pofa_build (one rank; the caller exchanges totals between the
    calls, e.g. one all_gather of a u64 per rank):

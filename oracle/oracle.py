@@ -309,3 +309,76 @@ def raycast(vol, camera, lights, radius, mode="transparency", cutoff=1.0, shadow
     stats = dict(zip(("visited_leaves", "tested_fragments", "hits", "early_terminations"),
                      (int(c) for c in counters)))
     return rgba.reshape(h, w, 4), stats, (None if ids is None else ids.reshape(h, w))
+
+
+def deferred(scene, camera, lights, background=(0.0, 0.0, 0.0, 0.0)):
+    """deferred_baseline (fhv/render.py:327-382) -> dict of rgba f64[h,w,4],
+    depth f64[h,w], G-buffer gpos/gnrm f64[h,w,3], gmat/gobj i32[h,w],
+    valid bool[h,w], and the fragment count."""
+    from paper_2211_15460_b200.raster import RasterConfig
+    w, h = camera.resolution
+    M = np.ascontiguousarray(RasterConfig.from_camera(camera).projection, dtype=np.float64)
+    pos, vn, fn, mat, obj = _tris(scene)
+    lk, lv, lc, la = pack_lights(lights)
+    md, ms, msh, ma = pack_materials(scene.materials)
+    out = {"rgba": np.zeros((h, w, 4)), "depth": np.zeros((h, w)), "gpos": np.zeros((h, w, 3)),
+           "gnrm": np.zeros((h, w, 3)), "gmat": np.zeros((h, w), np.int32), "gobj": np.zeros((h, w), np.int32),
+           "valid": np.zeros((h, w), np.uint8)}
+    eye = np.ascontiguousarray(camera.eye, dtype=np.float64)
+    bg = np.asarray(background, dtype=np.float64)
+    n = ctypes.c_int64(0)
+    rc = lib().orc_deferred(_i64(scene.n_triangles), _p(pos), _p(vn), _p(fn), _p(mat), _p(obj), _p(M), _i64(w),
+                            _i64(h), _p(eye), len(lights), _p(lk), _p(lv), _p(lc), _p(la), _p(md), _p(ms), _p(msh),
+                            _p(ma), _p(bg), _p(out["rgba"]), _p(out["depth"]), _p(out["gpos"]), _p(out["gnrm"]),
+                            _p(out["gmat"]), _p(out["gobj"]), _p(out["valid"]), ctypes.byref(n))
+    if rc:
+        raise OracleError(rc, "deferred")
+    out["valid"] = out["valid"].astype(bool)
+    out["emitted"] = int(n.value)
+    return out
+
+
+_SNAP_HEADER = "<4s4sIIIIQ"  # magic, layout, levels, w, h, record size, count (fhv/storage.py:722-723)
+
+
+def snapshot_bytes(vol):
+    """FHV1 snapshot of an oracle volume dict (fhv/storage.py:725-755): header,
+    directory, pyramid levels, packed 36-byte records of the stored prefix."""
+    import struct
+    from paper_2211_15460_b200.storage import RECORD_DTYPE
+    n = min(vol["next_free"], vol["capacity"])
+    if vol["layout"] == "PPFL":
+        parts = [struct.pack(_SNAP_HEADER, b"FHV1", b"PPFL", 0, vol["width"], vol["height"], 36, n),
+                 vol["heads"].astype("<i4").tobytes()]
+    else:
+        r = vol["capture_resolution"]
+        parts = [struct.pack(_SNAP_HEADER, b"FHV1", vol["layout"].encode(), vol["levels"], r, r, 36, n)]
+        if vol["layout"] == "POFL":
+            parts.append(vol["heads"].astype("<i4").tobytes())
+        else:
+            parts += [vol["offsets"].astype("<u4").tobytes(), vol["counts"].astype("<u4").tobytes()]
+        parts.append(vol["pyramid"].tobytes())
+    rec = np.empty(n, dtype=RECORD_DTYPE)
+    for k in RECORD_DTYPE.names:
+        rec[k] = vol["pool"][k][:n]
+    parts.append(rec.tobytes())
+    return b"".join(parts)
+
+
+def rebuild_pofl_as_pofa(vol):
+    """rebuild_pofl_as_pofa (fhv/storage.py:624-652) of an oracle POFL dict:
+    leaf codes of the f32 positions (cell_code), stable counting sort by leaf
+    (emission = pool order inside a leaf), directory, pyramid; prev = -1."""
+    L = vol["levels"]
+    n = min(vol["next_free"], vol["capacity"])
+    codes = cell_codes(vol["pool"]["position"][:n], L)
+    counts = np.bincount(codes, minlength=8 ** L).astype(np.uint32)
+    offsets = np.zeros(8 ** L, np.uint32)
+    offsets[1:] = np.cumsum(counts[:-1], dtype=np.int64).astype(np.uint32)
+    perm = np.argsort(codes, kind="stable")
+    pool = _new_pool(n)
+    for k in ("position", "normal", "material_id", "object_id"):
+        pool[k][:] = vol["pool"][k][:n][perm]
+    return {"layout": "POFA", "pool": pool, "offsets": offsets, "counts": counts,
+            "pyramid": pyramid_from_occupancy(counts > 0, L), "levels": L, "next_free": n, "capacity": n,
+            "overflowed": False, "capture_resolution": vol["capture_resolution"]}

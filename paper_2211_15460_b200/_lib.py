@@ -13,12 +13,13 @@ import threading
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfhv_b200.so")
+LIB_PATH = os.environ.get("FHV_LIB") or os.path.join(HERE, "libfhv_b200.so")  # FHV_LIB: experiment variants
 
 c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 
 FHV_OK, FHV_OVERFLOW, FHV_PASS_MISMATCH, FHV_BAD_ARGS, FHV_CUDA_ERROR = 0, 1, 2, 3, 4
 FHV_RANGE, FHV_BASIS, FHV_NOMEM, FHV_TOO_MANY, FHV_SPLAT_BIG = 5, 6, 7, 8, 9
+FHV_NEED_POOL = 10
 FHV_ALLOC_ATOMIC, FHV_EXACT_ORDER = 1, 2
 FHV_SPLAT_PACKED = 1
 
@@ -71,6 +72,8 @@ _SIGS = {
     "fhv_build_pofl": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, _P(Pool), c_vp, c_vp, c_i32,
                                       _P(c_i64), c_vp]),
     "fhv_pofa_count": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, c_vp, c_vp, c_vp, _P(c_i64), c_vp]),
+    "fhv_pofa_build": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, c_vp, c_vp, c_vp, _P(Pool), c_i32,
+                                      _P(c_i64), c_vp]),
     "fhv_pofa_scatter": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, c_vp, c_vp, _P(Pool), c_i32,
                                         c_vp]),
     "fhv_pofa_shard_count": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, _P(Shard), c_vp, _P(c_i64),

@@ -39,16 +39,23 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile the library (default: in-tree libfhv_b200.so).  ``out`` +
+    ``defines`` build an experiment variant (e.g. a launch-bounds sweep) that
+    ``FHV_LIB=<path>`` selects at load time."""
+    if out is None and not force and up_to_date():
         return OUT
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", OUT] + [os.path.join(HERE, "csrc", f) for f in SOURCES]
+    out = out or OUT
+    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out] + \
+        [os.path.join(HERE, "csrc", f) for f in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True, cwd=HERE)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(OUT)
+    args = sys.argv[1:]
+    o = args[args.index("--out") + 1] if "--out" in args else None
+    defs = [args[i + 1] for i, a in enumerate(args) if a == "-D"]
+    print(build(force="--force" in args, verbose="-v" in args, out=o, defines=defs))

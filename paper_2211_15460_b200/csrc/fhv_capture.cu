@@ -318,11 +318,11 @@ __device__ __forceinline__ void make_cover(const JobSetup& js, uint32_t p0, Cove
 __device__ __forceinline__ bool cover_test(const CoverS& c, int px, int py, double& f0, double& f1, double& f2) {
   const double sy = __dadd_rn((double)py, 0.5), sx = __dadd_rn((double)px, 0.5);
   f0 = __dsub_rn(__dmul_rn(c.e0x, __dsub_rn(sy, c.by)), __dmul_rn(c.e0y, __dsub_rn(sx, c.bx)));
-  if (!(f0 > 0.0 || (f0 == 0.0 && (c.tl & 1u)))) return false;
   f1 = __dsub_rn(__dmul_rn(c.e1x, __dsub_rn(sy, c.cy)), __dmul_rn(c.e1y, __dsub_rn(sx, c.cx)));
-  if (!(f1 > 0.0 || (f1 == 0.0 && (c.tl & 2u)))) return false;
   f2 = __dsub_rn(__dmul_rn(c.e2x, __dsub_rn(sy, c.ay)), __dmul_rn(c.e2y, __dsub_rn(sx, c.ax)));
-  return f2 > 0.0 || (f2 == 0.0 && (c.tl & 4u));
+  const bool in0 = f0 > 0.0 || (f0 == 0.0 && (c.tl & 1u));
+  const bool in1 = f1 > 0.0 || (f1 == 0.0 && (c.tl & 2u));
+  return in0 & in1 & (f2 > 0.0 || (f2 == 0.0 && (c.tl & 4u)));
 }
 
 // triangle vertex data in winding order
@@ -378,6 +378,9 @@ __device__ __forceinline__ void interp_nrm(const TriData& d, double l0, double l
 }
 
 enum RasterMode { kCnt = 0, kCntLeaves = 1, kList = 2, kPpfl = 3, kPofl = 4, kPofa = 5 };
+#ifndef FHV_RASTER_MINB
+#define FHV_RASTER_MINB 3  // resident CTAs per SM the raster kernels are register-budgeted for
+#endif
 constexpr int kRasterBlock = 256;
 constexpr int kRasterWarps = kRasterBlock / 32;
 
@@ -535,7 +538,7 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
 }
 
 template <int kMode, bool kAtomicAlloc>
-__global__ void __launch_bounds__(kRasterBlock, 3) k_raster(CaptureParams p, const JobSetup* __restrict__ jobs,
+__global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(CaptureParams p, const JobSetup* __restrict__ jobs,
                                                          const uint32_t* __restrict__ item_job,
                                                          const uint32_t* __restrict__ item_p0,
                                                          const unsigned long long* __restrict__ item_off,
@@ -597,14 +600,15 @@ __global__ void __launch_bounds__(kRasterBlock, 3) k_raster(CaptureParams p, con
       if (j < npix) {
         const CoverS& c = cs[lane];
         const double sx = __dadd_rn((double)px, 0.5);
+        // the three edge functions as independent chains (no early-out
+        // branches: ILP instead of divergence; same values either way)
         const double f0 = __dsub_rn(k0, __dmul_rn(c.e0y, __dsub_rn(sx, c.bx)));
-        if (f0 > 0.0 || (f0 == 0.0 && (c.tl & 1u))) {
-          const double f1 = __dsub_rn(k1, __dmul_rn(c.e1y, __dsub_rn(sx, c.cx)));
-          if (f1 > 0.0 || (f1 == 0.0 && (c.tl & 2u))) {
-            const double f2 = __dsub_rn(k2, __dmul_rn(c.e2y, __dsub_rn(sx, c.ax)));
-            cov = f2 > 0.0 || (f2 == 0.0 && (c.tl & 4u));
-          }
-        }
+        const double f1 = __dsub_rn(k1, __dmul_rn(c.e1y, __dsub_rn(sx, c.cx)));
+        const double f2 = __dsub_rn(k2, __dmul_rn(c.e2y, __dsub_rn(sx, c.ax)));
+        const bool in0 = f0 > 0.0 || (f0 == 0.0 && (c.tl & 1u));
+        const bool in1 = f1 > 0.0 || (f1 == 0.0 && (c.tl & 2u));
+        const bool in2 = f2 > 0.0 || (f2 == 0.0 && (c.tl & 4u));
+        cov = in0 & in1 & in2;
         if (++px == xend) {
           px = c.x0;
           ++py;
@@ -700,7 +704,7 @@ __device__ __forceinline__ uint32_t nth_set_bit(uint32_t v, uint32_t n) {
 // per step (flat index -> item by a 5-step shuffle search over the items'
 // fragment prefix sums -> pixel by select-n-th-bit), no coverage sweep.
 template <int kMode, bool kAtomicAlloc>
-__global__ void __launch_bounds__(kRasterBlock, 3) k_emit(CaptureParams p, const JobSetup* __restrict__ jobs,
+__global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureParams p, const JobSetup* __restrict__ jobs,
                                                        const uint32_t* __restrict__ item_job,
                                                        const uint32_t* __restrict__ item_p0,
                                                        const unsigned long long* __restrict__ item_off,
@@ -1238,6 +1242,37 @@ int shard_params(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* 
 
 }  // namespace
 
+namespace {
+
+// pass 1 up to the per-leaf histogram, no sync after the counting kernel: the
+// item scan's total is parked in ctl->frags_total for the caller's next sync
+int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
+                     const fhv_shard_t* shard, uint32_t* counts_local, cudaStream_t s, CaptureParams& p) {
+  ctx->pass1_levels = -1;
+  int rc;
+  if ((rc = reset_control(ctx, s))) return rc;
+  if ((rc = shard_params(ctx, tris, cfg, levels, shard, true, p, s))) return rc;
+  const unsigned long long n_local = p.cell_hi - p.cell_lo;
+  if ((rc = plan(ctx, p, s))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(counts_local, 0, (size_t)n_local * 4, s)))) return rc;
+  if ((rc = count(ctx, p, true, levels, counts_local, s))) return rc;
+  return check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total, sizeof(unsigned long long),
+                                         cudaMemcpyDeviceToDevice, s));
+}
+
+int pofa_count_done(fhv_ctx* ctx, const fhv_tris_t* tris, int32_t levels, const CaptureParams& p) {
+  const long long frags = (long long)ctx->ctl_host->frags_total;
+  if (frags >= (1LL << 32)) return FHV_TOO_MANY;
+  ctx->pass1_total = frags;
+  ctx->pass1_levels = levels;
+  ctx->pass1_tris = tris->n_tri;
+  ctx->pass1_lo = p.cell_lo;
+  ctx->pass1_hi = p.cell_hi;
+  return FHV_OK;
+}
+
+}  // namespace
+
 extern "C" int fhv_pofa_shard_count(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
                                     int32_t levels, const fhv_shard_t* shard, uint32_t* counts_local,
                                     int64_t* local_total, void* stream) {
@@ -1245,23 +1280,11 @@ extern "C" int fhv_pofa_shard_count(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   int rc = validate(tris, cfg);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  ctx->pass1_levels = -1;
   CaptureParams p;
-  if ((rc = reset_control(ctx, s))) return rc;
-  if ((rc = shard_params(ctx, tris, cfg, levels, shard, true, p, s))) return rc;
-  const unsigned long long n_local = p.cell_hi - p.cell_lo;
-  if ((rc = plan(ctx, p, s))) return rc;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(counts_local, 0, (size_t)n_local * 4, s)))) return rc;
-  if ((rc = count(ctx, p, true, levels, counts_local, s))) return rc;
+  if ((rc = pofa_count_async(ctx, tris, cfg, levels, shard, counts_local, s, p))) return rc;
   if ((rc = sync_control(ctx, s))) return rc;
-  const long long frags = (long long)ctx->ctl_host->scan_total;
-  if (frags >= (1LL << 32)) return FHV_TOO_MANY;
-  ctx->pass1_total = frags;
-  ctx->pass1_levels = levels;
-  ctx->pass1_tris = tris->n_tri;
-  ctx->pass1_lo = p.cell_lo;
-  ctx->pass1_hi = p.cell_hi;
-  if (local_total) *local_total = frags;
+  if ((rc = pofa_count_done(ctx, tris, levels, p))) return rc;
+  if (local_total) *local_total = ctx->pass1_total;
   return FHV_OK;
 }
 
@@ -1278,6 +1301,11 @@ extern "C" int fhv_pofa_shard_directory(fhv_ctx* ctx, int32_t levels, const fhv_
   if (lo == 0 && hi == n_leaves && base == 0) return scan_leaves_and_pyramid(ctx, counts_local, offsets_local, pyramid,
                                                                             levels, s);
   return scan_leaf_range_and_pyramid(ctx, counts_local, offsets_local, pyramid, levels, lo, hi, base, s);
+}
+
+static int fhv_pofa_shard_directory_nocheck(fhv_ctx* ctx, int32_t levels, const uint32_t* counts,
+                                            uint32_t* offsets, uint8_t* pyramid, cudaStream_t s) {
+  return scan_leaves_and_pyramid(ctx, counts, offsets, pyramid, levels, s);
 }
 
 extern "C" int fhv_pofa_shard_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
@@ -1328,14 +1356,27 @@ extern "C" int fhv_pofa_shard_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, cons
 extern "C" int fhv_pofa_count(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
                               uint32_t* counts, uint32_t* offsets, uint8_t* pyramid, int64_t* total, void* stream) {
   if (!ctx || !counts || !offsets || !pyramid || levels < 1 || levels > 10) return FHV_BAD_ARGS;
-  int64_t frags = 0;
-  int rc = fhv_pofa_shard_count(ctx, tris, cfg, levels, nullptr, counts, &frags, stream);
+  int rc = validate(tris, cfg);
   if (rc) return rc;
-  if ((rc = fhv_pofa_shard_directory(ctx, levels, nullptr, counts, offsets, pyramid, 0, stream))) return rc;
-  if ((rc = sync_control(ctx, (cudaStream_t)stream))) return rc;
-  if ((long long)ctx->ctl_host->scan_total != frags) return FHV_PASS_MISMATCH;
-  if (total) *total = frags;
+  cudaStream_t s = (cudaStream_t)stream;
+  CaptureParams p;
+  // histogram and directory back to back; one sync reads both totals
+  if ((rc = pofa_count_async(ctx, tris, cfg, levels, nullptr, counts, s, p))) return rc;
+  if ((rc = fhv_pofa_shard_directory_nocheck(ctx, levels, counts, offsets, pyramid, s))) return rc;
+  if ((rc = sync_control(ctx, s))) return rc;
+  if ((rc = pofa_count_done(ctx, tris, levels, p))) return rc;
+  if ((long long)ctx->ctl_host->scan_total != ctx->pass1_total) return FHV_PASS_MISMATCH;
+  if (total) *total = ctx->pass1_total;
   return FHV_OK;
+}
+
+extern "C" int fhv_pofa_build(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
+                              uint32_t* counts, uint32_t* offsets, uint8_t* pyramid, fhv_pool_t* pool, int32_t flags,
+                              int64_t* total, void* stream) {
+  int rc = fhv_pofa_count(ctx, tris, cfg, levels, counts, offsets, pyramid, total, stream);
+  if (rc) return rc;
+  if (!pool || pool->capacity < ctx->pass1_total) return FHV_NEED_POOL;
+  return fhv_pofa_shard_scatter(ctx, tris, cfg, levels, nullptr, counts, offsets, 0, pool, flags, stream);
 }
 
 extern "C" int fhv_pofa_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,

@@ -273,15 +273,23 @@ class Camera:
         [persp, eye3, r3, u3, f3, w, h, half_w, half_h, tan(fov/2), aspect,
         near, far, extent].  Every derived scalar is computed with the same
         Python expression the reference uses (fhv/render.py:211-242,
-        fhv/raycast.py:148-172)."""
+        fhv/raycast.py:148-172).  Cached per camera state (read-only array)."""
+        key = (self.kind, self.eye.tobytes(), self.view_dir.tobytes(), self.up.tobytes(), self.extent_or_fov,
+               self.resolution, self.near, self.far)
+        hit = self.__dict__.get("_scalars")
+        if hit is not None and hit[0] == key:
+            return hit[1]
         r, u, f = self.basis()
         w, h = self.resolution
         persp = self.kind == "perspective"
         half_h = self.extent_or_fov / 2.0
         half_w = half_h * self.aspect
         t = math.tan(math.radians(self.extent_or_fov) / 2.0) if persp else 0.0
-        return np.array([1.0 if persp else 0.0, *self.eye, *r, *u, *f, w, h, half_w, half_h, t,
-                         self.aspect, self.near, self.far, self.extent_or_fov], dtype=np.float64)
+        out = np.array([1.0 if persp else 0.0, *self.eye, *r, *u, *f, w, h, half_w, half_h, t,
+                        self.aspect, self.near, self.far, self.extent_or_fov], dtype=np.float64)
+        out.flags.writeable = False
+        self.__dict__["_scalars"] = (key, out)
+        return out
 
 
 def normalize_scene(scene: Scene, margin: float = 0.0):

@@ -149,14 +149,36 @@ class FragmentPool:
         dev = default_device(device)
         self.capacity = int(capacity)
         self.device = dev
-        self.position = torch.empty((capacity, 3), dtype=torch.float32, device=dev)
-        self.normal = torch.empty((capacity, 3), dtype=torch.float32, device=dev)
-        self.material_id = torch.empty(capacity, dtype=torch.uint32, device=dev)
-        self.object_id = torch.empty(capacity, dtype=torch.uint32, device=dev)
-        self.prev_index = (torch.full((capacity,), -1, dtype=torch.int32, device=dev) if fill_prev
-                           else torch.empty(capacity, dtype=torch.int32, device=dev))
+        # one allocation carved into the five SoA arrays (each 256-B aligned)
+        c = self.capacity
+        sizes = [12 * c, 12 * c, 4 * c, 4 * c, 4 * c]
+        offs, o = [], 0
+        for b in sizes:
+            offs.append(o)
+            o += (b + 255) // 256 * 256
+        buf = torch.empty(max(o, 1), dtype=torch.uint8, device=dev)
+        seg = [buf[a:a + b] for a, b in zip(offs, sizes)]
+        self.position = seg[0].view(torch.float32).view(c, 3)
+        self.normal = seg[1].view(torch.float32).view(c, 3)
+        self.material_id = seg[2].view(torch.uint32)
+        self.object_id = seg[3].view(torch.uint32)
+        self.prev_index = seg[4].view(torch.int32)
+        if fill_prev:
+            self.prev_index.fill_(-1)
         self.next_free = 0
         self.overflowed = False
+
+    def narrow(self, n: int) -> "FragmentPool":
+        """The first ``n`` records as a pool of capacity ``n`` (views, no copy)."""
+        if not 0 <= n <= self.capacity:
+            raise FhvError(f"cannot narrow a pool of {self.capacity} records to {n}")
+        out = FragmentPool.__new__(FragmentPool)
+        out.capacity, out.device = int(n), self.device
+        out.position, out.normal = self.position[:n], self.normal[:n]
+        out.material_id, out.object_id, out.prev_index = self.material_id[:n], self.object_id[:n], self.prev_index[:n]
+        out.next_free = min(self.next_free, n)
+        out.overflowed = False
+        return out
 
     @property
     def stored_count(self) -> int:
@@ -345,14 +367,14 @@ def build_ppfl(scene: Scene, cfg: RasterConfig, strategy: CaptureStrategy | None
     w, h = cfg.resolution
     if capacity is None:
         capacity = int(w * h * overalloc)
-    plan = capture_plan(scene, strategy, cfg)
+    plan, c = _plan_cfg(scene, strategy, cfg)
     ds = device_scene(scene, device)
     dev = ds.device
     pool = FragmentPool(capacity, dev)
     heads = torch.full((w * h,), -1, dtype=torch.int32, device=dev)
     nf = ctypes_i64()
     lib = _lib.load()
-    tris, c, p = ds.struct(), capture_cfg(plan), pool.struct()
+    tris, p = ds.struct(), pool.struct()
     rc = lib.fhv_build_ppfl(_lib.ctx(dev), tris, c, w, p, _lib.ptr(heads), _flags(alloc, exact_order), nf,
                             _lib.stream_ptr(dev))
     _lib.check(rc, "build_ppfl", allow=(_lib.FHV_OK, _lib.FHV_OVERFLOW))
@@ -371,7 +393,7 @@ def build_pofl(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     w, h = cfg.resolution
     if capacity is None:
         capacity = int(w * h * overalloc)
-    plan = capture_plan(scene, strategy, cfg)
+    plan, c = _plan_cfg(scene, strategy, cfg)
     ds = device_scene(scene, device)
     dev = ds.device
     pool = FragmentPool(capacity, dev)
@@ -379,7 +401,7 @@ def build_pofl(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     pyr = OccupancyPyramid(levels, device=dev)
     nf = ctypes_i64()
     lib = _lib.load()
-    tris, c, p = ds.struct(), capture_cfg(plan), pool.struct()
+    tris, p = ds.struct(), pool.struct()
     rc = lib.fhv_build_pofl(_lib.ctx(dev), tris, c, levels, p, _lib.ptr(heads), _lib.ptr(pyr.data),
                             _flags(alloc, exact_order), nf, _lib.stream_ptr(dev))
     _lib.check(rc, "build_pofl", allow=(_lib.FHV_OK, _lib.FHV_OVERFLOW))
@@ -399,7 +421,7 @@ def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
         raise FhvError("octree needs at least one level")
     if levels > 11:
         raise FhvError(f"levels {levels}: dense POFA directories beyond L=11 exceed device memory")
-    plan = capture_plan(scene, strategy, cfg)
+    plan, c = _plan_cfg(scene, strategy, cfg)
     ds = tris if tris is not None else device_scene(scene, device)
     dev = ds.device
     n_leaf = 8 ** levels
@@ -407,20 +429,44 @@ def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     offsets = torch.empty(n_leaf, dtype=torch.uint32, device=dev)
     pyr = OccupancyPyramid(levels, device=dev)
     lib = _lib.load()
-    tris, c = ds.struct(), capture_cfg(plan)
     total = ctypes_i64()
     cx = _lib.ctx(dev)
     st = _lib.stream_ptr(dev)
-    rc = lib.fhv_pofa_count(cx, tris, c, levels, _lib.ptr(counts), _lib.ptr(offsets), _lib.ptr(pyr.data), total, st)
-    _lib.check(rc, "pofa_build pass 1")
-    pool = FragmentPool(int(total.value), dev, fill_prev=False)  # pass 2 writes every prev_index
-    p = pool.struct()
-    rc = lib.fhv_pofa_scatter(cx, tris, c, levels, _lib.ptr(counts), _lib.ptr(offsets), p,
-                              _lib.FHV_EXACT_ORDER if exact_order else 0, st)
-    _lib.check(rc, "pofa_build pass 2")
-    pool.next_free = pool.capacity
+    flags = _lib.FHV_EXACT_ORDER if exact_order else 0
+    # the exact pool size is data dependent: start from the last total seen for
+    # this (scene, plan, levels) so count + directory + scatter run in ONE call
+    # with the syncs inside the library; a miss costs a second call
+    guesses = ds.__dict__.setdefault("_pofa_totals", {})
+    gkey = (plan.key, levels)
+    guess = guesses.get(gkey)
+    pool = FragmentPool(guess, dev, fill_prev=False) if guess is not None else None  # pass 2 writes every prev
+    tr = ds.struct()
+    rc = lib.fhv_pofa_build(cx, tr, c, levels, _lib.ptr(counts), _lib.ptr(offsets), _lib.ptr(pyr.data),
+                            pool.struct() if pool is not None else None, flags, total, st)
+    n = int(total.value)
+    if rc == _lib.FHV_NEED_POOL:
+        pool = FragmentPool(n, dev, fill_prev=False)
+        rc = lib.fhv_pofa_scatter(cx, tr, c, levels, _lib.ptr(counts), _lib.ptr(offsets), pool.struct(), flags, st)
+    _lib.check(rc, "pofa_build")
+    guesses[gkey] = n
+    if pool.capacity != n:
+        pool = pool.narrow(n)
+    pool.next_free = n
     return FhvPofa(PofaDirectory(levels, offsets, counts), pyr, pool, int(cfg.resolution[1]),
                    plan.stats(pool.next_free), scene.materials)
+
+
+def _plan_cfg(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig):
+    """capture_plan + its C struct, cached on the scene per (strategy, config)."""
+    key = (strategy.kind, getattr(strategy, "axis", None), tuple(cfg.resolution), cfg.extent,
+           np.asarray(cfg.projection).tobytes())
+    cache = scene.__dict__.setdefault("_plan_cache", {})
+    hit = cache.get(key)
+    if hit is None:
+        plan = capture_plan(scene, strategy, cfg)
+        plan.key = key
+        hit = cache[key] = (plan, capture_cfg(plan))
+    return hit
 
 
 def ctypes_i64():
