@@ -208,6 +208,32 @@ int fhv_pofa_build(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t
                    uint32_t *counts, uint32_t *offsets, uint8_t *pyramid, fhv_pool_t *pool, int32_t flags,
                    int64_t *total, void *stream);
 
+/* rebuild_pofl_as_pofa (fhv/storage.py:624-652): repack the first n records
+   of a linked-list pool into per-leaf contiguous ranges (Morton order, pool
+   order inside a leaf), counts / offsets [8^L], pyramid from counts > 0;
+   dst->prev_index = -1.  FHV_RANGE if a position lies outside [0,1]^3.
+   Synchronises. */
+int fhv_rebuild_pofa(fhv_ctx *ctx, int32_t levels, const fhv_pool_t *src, int64_t n, uint32_t *counts,
+                     uint32_t *offsets, uint8_t *pyramid, fhv_pool_t *dst, void *stream);
+
+/* FHV1 snapshot records (fhv/storage.py:725-808): pack the first n pool
+   records into `out` as packed little-endian 36-byte RECORD_DTYPE rows
+   (device memory, 4-byte aligned), or unpack such rows into a pool.  Async. */
+int fhv_pack_records(fhv_ctx *ctx, const fhv_pool_t *pool, int64_t n, void *out, void *stream);
+int fhv_unpack_records(fhv_ctx *ctx, const void *in, int64_t n, fhv_pool_t *pool, void *stream);
+
+/* deferred_baseline (fhv/render.py:327-382) -- the paper's DS comparison
+   renderer: every triangle rasterised through the camera projection `proj`
+   (4x4 row-major world->clip, RasterConfig.from_camera) at width x height,
+   nearest (f64 depth, triangle index) per pixel kept in the f64 G-buffer
+   (all five planes required; written for every pixel: winners, or the
+   GBuffer.new defaults), then Blinn-Phong with eye[3] into out_rgba
+   [H][W][4] (background where empty) and out_depth [H][W] (+inf where
+   empty).  *emitted = fragments rasterised.  Synchronises. */
+int fhv_deferred(fhv_ctx *ctx, const fhv_tris_t *tris, const double *proj, int32_t width, int32_t height,
+                 const double *eye, const fhv_shading_t *shading, const double *background, double *out_rgba,
+                 double *out_depth, const fhv_gbuffer_t *gb, int64_t *emitted, void *stream);
+
 /* Sharded pofa_build (one rank; the caller exchanges totals between the
    calls, e.g. one all_gather of a u64 per rank):
    1. fhv_pofa_shard_count: bin triangles, rasterise, histogram the owned

@@ -13,7 +13,7 @@ from .lights import (GBuffer, ImageBuffer, Light, composite_over, front_to_back_
 from .raster import (CaptureStats, CaptureStrategy, FragmentBatch, RasterConfig, capture_plan, ortho_projection,
                      perspective_projection, tangent_basis, world_pixel_footprint)
 from .raycast import RaycastConfig, RaycastStats, default_raycast_config, primary_rays, render_raycast
-from .render import splat_render
+from .render import deferred_baseline, splat_render
 from .scene import (Aabb, Camera, Material, Scene, SceneError, SceneLoadError, Triangle, Vertex, capture_camera,
                     make_quad, make_triangle, normalize_scene, viewpoint_camera)
 from .storage import (FhvError, FhvPofa, FhvPofl, FhvPpfl, FragmentPool, FragmentRecord, OccupancyPyramid,

@@ -40,8 +40,21 @@ static_assert(sizeof(JobSetup) == 80, "JobSetup layout");
 
 constexpr uint32_t kItemPix = 128;
 
+// per-job screen data of the deferred pass (strategy kScreen): clip w and
+// ndc z of the vertices in winding order, and whether the job's batch holds
+// exactly one fragment (numpy's gemv takes the ddot path then)
+struct JobPersp {
+  double w[3], z[3];
+  uint32_t n1, pad;
+};
+
+constexpr int kScreen = 4;  // deferred_baseline: one camera, W x H, any projection
+
 struct CaptureParams {
   int strategy, res;
+  int width, height;   // raster size (res x res for the capture strategies)
+  int ortho;           // projection row 3 == (0, 0, 0, 1) (RasterConfig.is_orthographic)
+  JobPersp* persp;     // kScreen only
   double pitch;
   double proj[3][16];
   long long n_tri, n_jobs;
@@ -80,6 +93,10 @@ struct EmitOut {
   double* wpos;
   double* wnrm;
   int flags;
+  // deferred_baseline (kScreen): per-pixel depth keys, winning job, G-buffer
+  unsigned long long* ds_key;
+  uint32_t* ds_win;
+  fhv_gbuffer_t gb;
 };
 
 // ---------------------------------------------------------------------------
@@ -136,22 +153,46 @@ __device__ __forceinline__ bool finish_setup(const double xr[3], const double yr
   return true;
 }
 
-// _raster_screen for an orthographic capture axis (fhv/raster.py:184-209)
-__device__ __forceinline__ void setup_screen(const CaptureParams& p, long long t, int axis, JobSetup& js) {
+// _raster_screen (fhv/raster.py:184-209): clip = dgemm (FWD) + P[:,3]; the
+// capture axes are orthographic; the deferred camera (kScreen) may be
+// perspective: a triangle with any clip w <= 1e-9 is skipped
+__device__ __forceinline__ void setup_screen(const CaptureParams& p, long long j, long long t, int axis,
+                                             JobSetup& js) {
   const double* M = p.proj[axis];
   const double* P = p.pos + 9 * t;
-  double xr[3], yr[3];
+  double xr[3], yr[3], cw[3], nz[3];
+  bool behind = false;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const double X = P[3 * i], Y = P[3 * i + 1], Z = P[3 * i + 2];
     const double c0 = __dadd_rn(fwd3(X, Y, Z, M[0], M[1], M[2]), M[3]);
     const double c1 = __dadd_rn(fwd3(X, Y, Z, M[4], M[5], M[6]), M[7]);
     const double c3 = __dadd_rn(fwd3(X, Y, Z, M[12], M[13], M[14]), M[15]);
+    if (p.strategy == kScreen) {
+      const double c2 = __dadd_rn(fwd3(X, Y, Z, M[8], M[9], M[10]), M[11]);
+      nz[i] = __ddiv_rn(c2, c3);
+      cw[i] = c3;
+      behind = behind || (!p.ortho && c3 <= 1e-9);
+    }
     const double nx = __ddiv_rn(c0, c3), ny = __ddiv_rn(c1, c3);
-    xr[i] = __dmul_rn(__dmul_rn(__dadd_rn(nx, 1.0), 0.5), (double)p.res);
-    yr[i] = __dmul_rn(__dmul_rn(__dsub_rn(1.0, ny), 0.5), (double)p.res);
+    xr[i] = __dmul_rn(__dmul_rn(__dadd_rn(nx, 1.0), 0.5), (double)p.width);
+    yr[i] = __dmul_rn(__dmul_rn(__dsub_rn(1.0, ny), 0.5), (double)p.height);
   }
-  finish_setup(xr, yr, p.res, p.res, js);
+  if (behind) {  // "behind the eye; this rasterizer does not clip"
+    js.bw = 0;
+    js.bh = 0;
+    return;
+  }
+  finish_setup(xr, yr, p.width, p.height, js);
+  if (p.strategy == kScreen) {
+    JobPersp jp;
+    const int o1 = js.swapped ? 2 : 1, o2 = js.swapped ? 1 : 2;
+    jp.w[0] = cw[0]; jp.w[1] = cw[o1]; jp.w[2] = cw[o2];
+    jp.z[0] = nz[0]; jp.z[1] = nz[o1]; jp.z[2] = nz[o2];
+    jp.n1 = 0;
+    jp.pad = 0;
+    p.persp[j] = jp;
+  }
 }
 
 // _raster_tangent (fhv/raster.py:212-242) with tangent_basis (:147-163)
@@ -227,7 +268,7 @@ __global__ void k_job_setup(CaptureParams p, JobSetup* __restrict__ jobs, uint32
     if (p.strategy == 3)
       setup_tangent(p, t, js, status);
     else
-      setup_screen(p, t, axis, js);
+      setup_screen(p, j, t, axis, js);
     const unsigned long long pix = (unsigned long long)js.bw * (unsigned long long)js.bh;
     unsigned long long items = (pix + kItemPix - 1) / kItemPix;
     if (items > 0xFFFFFFFFull) {
@@ -333,25 +374,32 @@ struct TriData {
   uint32_t mat, obj;
 };
 
-__device__ __forceinline__ void load_tri(const CaptureParams& p, uint32_t tri, uint32_t swapped, TriData& d,
-                                         bool normals) {
+__device__ __forceinline__ void load_tri_pos(const CaptureParams& p, uint32_t tri, uint32_t swapped, TriData& d) {
   const double* P = p.pos + 9 * (long long)tri;
-  const double* N = p.vnrm + 9 * (long long)tri;
   const int o[3] = {0, swapped ? 2 : 1, swapped ? 1 : 2};
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int k = 0; k < 3; ++k) d.v[i][k] = __ldg(&P[3 * o[i] + k]);
-  if (normals) {
+}
+
+__device__ __forceinline__ void load_tri_nrm(const CaptureParams& p, uint32_t tri, uint32_t swapped, TriData& d) {
+  const double* N = p.vnrm + 9 * (long long)tri;
+  const int o[3] = {0, swapped ? 2 : 1, swapped ? 1 : 2};
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) d.n[i][k] = __ldg(&N[3 * o[i] + k]);
+    for (int k = 0; k < 3; ++k) d.n[i][k] = __ldg(&N[3 * o[i] + k]);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) d.f[k] = __ldg(&p.fnrm[3 * (long long)tri + k]);
-    d.mat = __ldg(&p.mat[tri]);
-    d.obj = __ldg(&p.obj[tri]);
-  }
+  for (int k = 0; k < 3; ++k) d.f[k] = __ldg(&p.fnrm[3 * (long long)tri + k]);
+  d.mat = __ldg(&p.mat[tri]);
+  d.obj = __ldg(&p.obj[tri]);
+}
+
+__device__ __forceinline__ void load_tri(const CaptureParams& p, uint32_t tri, uint32_t swapped, TriData& d,
+                                         bool normals) {
+  load_tri_pos(p, tri, swapped, d);
+  if (normals) load_tri_nrm(p, tri, swapped, d);
 }
 
 // lam @ V (dgemm FWD chain), fhv/raster.py:168
@@ -377,7 +425,8 @@ __device__ __forceinline__ void interp_nrm(const TriData& d, double l0, double l
   }
 }
 
-enum RasterMode { kCnt = 0, kCntLeaves = 1, kList = 2, kPpfl = 3, kPofl = 4, kPofa = 5 };
+enum RasterMode { kCnt = 0, kCntLeaves = 1, kList = 2, kPpfl = 3, kPofl = 4, kPofa = 5, kDsDepth = 6, kDsIndex = 7,
+                  kDsWrite = 8 };
 #ifndef FHV_RASTER_MINB
 #define FHV_RASTER_MINB 3  // resident CTAs per SM the raster kernels are register-budgeted for
 #endif
@@ -396,11 +445,63 @@ struct RasterState {
 // inside the item: push order for the linked / list modes; owned-fragment
 // order (smem counters) for the keyed POFA modes, whose shard filter is only
 // known here.
+// one fragment of the deferred geometry pass (fhv/render.py:345-371).
+// depth = lam @ ndc_z (gemv: G102, FWD for a one-fragment batch); the pixel's
+// winner is the smallest (depth, triangle) -- "equal depth keeps first" --
+// found in three sweeps: RED.MIN of the order-preserving depth key, then
+// atomicMin of the job among fragments at that key, then the winner alone
+// interpolates with the perspective-corrected lam (lam / w renormalised,
+// :206-208) and writes the f64 G-buffer.
+template <int kMode>
+__device__ __forceinline__ void ds_fragment(const CaptureParams& p, const EmitOut& o, const CoverS& c, uint32_t job,
+                                            int px, int py) {
+  double f0, f1, f2;
+  cover_test(c, px, py, f0, f1, f2);
+  double l0 = __ddiv_rn(f0, c.area2), l1 = __ddiv_rn(f1, c.area2), l2 = __ddiv_rn(f2, c.area2);
+  const JobPersp& jp = p.persp[job];
+  const double d = jp.n1 ? fwd3(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]) : g102(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]);
+  if (isnan(d)) return;  // np.minimum.at would poison the pixel; no winner either way
+  const unsigned long long key = depth_key(d);
+  const long long pix = (long long)py * p.width + px;
+  if (kMode == kDsDepth) {
+    atomicMin(&o.ds_key[pix], key);
+    return;
+  }
+  if (kMode == kDsIndex) {
+    if (o.ds_key[pix] == key) atomicMin(&o.ds_win[pix], job);
+    return;
+  }
+  if (o.ds_win[pix] != job) return;
+  if (!p.ortho) {
+    const double lw0 = __ddiv_rn(l0, jp.w[0]), lw1 = __ddiv_rn(l1, jp.w[1]), lw2 = __ddiv_rn(l2, jp.w[2]);
+    const double sum = __dadd_rn(__dadd_rn(lw0, lw1), lw2);
+    l0 = __ddiv_rn(lw0, sum);
+    l1 = __ddiv_rn(lw1, sum);
+    l2 = __ddiv_rn(lw2, sum);
+  }
+  TriData td;
+  load_tri(p, c.tri, c.swapped, td, true);
+  double w[3], nn[3];
+  interp_pos(td, l0, l1, l2, w);
+  interp_nrm(td, l0, l1, l2, nn);
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+    o.gb.position[3 * pix + e] = w[e];
+    o.gb.normal[3 * pix + e] = nn[e];
+  }
+  o.gb.material_id[pix] = (int32_t)td.mat;
+  o.gb.object_id[pix] = (int32_t)td.obj;
+}
+
 template <int kMode, bool kAtomicAlloc>
 __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitOut& o, Control* ctl,
                                              const CoverS* cs, bool valid, int k, int px, int py,
                                              uint32_t push_local, uint32_t* own_cnt, unsigned long long rank0,
                                              const uint32_t* item_job_g, RasterState<kMode, kAtomicAlloc>& st) {
+  if constexpr (kMode == kDsDepth || kMode == kDsIndex || kMode == kDsWrite) {
+    if (valid) ds_fragment<kMode>(p, o, cs[k], item_job_g[k], px, py);
+    return;
+  }
   constexpr bool kKeyed = kMode == kCntLeaves || kMode == kPofl || kMode == kPofa;
   constexpr bool kOwned = kMode == kCntLeaves || kMode == kPofa;
   const unsigned lane = lane_id();
@@ -417,7 +518,7 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
     l0 = __ddiv_rn(f0, c.area2);
     l1 = __ddiv_rn(f1, c.area2);
     l2 = __ddiv_rn(f2, c.area2);
-    load_tri(p, c.tri, c.swapped, d, kMode != kCntLeaves);
+    load_tri_pos(p, c.tri, c.swapped, d);
     interp_pos(d, l0, l1, l2, w);
     live = true;
     if (kKeyed) {
@@ -446,8 +547,24 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
     if (live && (int)lane == __ffs(grp) - 1) atomicAdd(&o.leaf_counts[code - p.cell_lo], (uint32_t)__popc(grp));
     return;
   }
+  // POFA: the leaf's cursor atomic (and its range loads) go out BEFORE the
+  // normal interpolation, so their L2/DRAM round trip overlaps the FP64 work
+  unsigned pofa_grp = 0;
+  int pofa_leader = 0;
+  uint32_t pofa_base = 0, pofa_cnt = 0, pofa_off = 0;
+  if (kMode == kPofa) {
+    pofa_grp = __match_any_sync(0xffffffffu, code);
+    pofa_leader = __ffs(pofa_grp) - 1;
+    const unsigned long long lc = live ? code - p.cell_lo : 0ull;
+    if (live) {
+      pofa_cnt = __ldg(&o.counts[lc]);
+      pofa_off = __ldg(&o.offsets[lc]);
+    }
+    if (live && (int)lane == pofa_leader) pofa_base = atomicAdd(&o.cursors[lc], (uint32_t)__popc(pofa_grp));
+  }
   double nn[3] = {0.0, 0.0, 0.0};
   if (live) {
+    load_tri_nrm(p, c.tri, c.swapped, d);
     interp_nrm(d, l0, l1, l2, nn);
     ++st.emitted;
   }
@@ -466,22 +583,13 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   }
   long long slot = -1;
   if (kMode == kPofa) {
-    const unsigned grp = __match_any_sync(0xffffffffu, code);
-    const int leader = __ffs(grp) - 1;
-    uint32_t base = 0, cnt = 0, off = 0;
-    const unsigned long long lc = live ? code - p.cell_lo : 0ull;
-    if (live) {  // issued before the atomic so the latencies overlap
-      cnt = __ldg(&o.counts[lc]);
-      off = __ldg(&o.offsets[lc]);
-    }
-    if (live && (int)lane == leader) base = atomicAdd(&o.cursors[lc], (uint32_t)__popc(grp));
-    base = __shfl_sync(0xffffffffu, base, leader);
+    const uint32_t base = __shfl_sync(0xffffffffu, pofa_base, pofa_leader);
     if (live) {
-      const uint32_t cur = base + (uint32_t)__popc(grp & below);
-      if (cur >= cnt) {
+      const uint32_t cur = base + (uint32_t)__popc(pofa_grp & below);
+      if (cur >= pofa_cnt) {
         st.bad_pass = true;
       } else {
-        slot = (long long)(off - o.base) + cur;
+        slot = (long long)(pofa_off - o.base) + cur;
       }
     }
   } else {
@@ -710,7 +818,9 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
                                                        const unsigned long long* __restrict__ item_off,
                                                        const uint4* __restrict__ item_mask, long long n_items,
                                                        EmitOut o, Control* ctl) {
-  static_assert(kMode == kList || kMode == kPpfl || kMode == kPofl || kMode == kPofa, "emission modes only");
+  static_assert(kMode == kList || kMode == kPpfl || kMode == kPofl || kMode == kPofa || kMode == kDsDepth ||
+                    kMode == kDsIndex || kMode == kDsWrite,
+                "emission modes only");
   __shared__ CoverS cs_all[kRasterWarps][32];
   __shared__ uint32_t own_all[kRasterWarps][32];
   __shared__ uint32_t ijob_all[kRasterWarps][32];
@@ -952,6 +1062,104 @@ __global__ void k_compact_tris(const uint32_t* __restrict__ flag, const unsigned
     if (flag[t]) idx[off[t]] = (uint32_t)t;
 }
 
+// rebuild_pofl_as_pofa (fhv/storage.py:624-652): leaf histogram of the f32
+// record positions (cell_code), then a scatter into the leaf ranges with the
+// source index parked in prev_index for k_leaf_order (stable: pool order =
+// emission order inside a leaf)
+__global__ void k_pool_leaf_hist(const float* __restrict__ pos, long long n, int levels, uint32_t* __restrict__ counts,
+                                 int* status) {
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31u); i0 < n;
+       i0 += (long long)gridDim.x * blockDim.x) {
+    const long long i = i0 + lane_id();
+    uint64_t code = ~0ull;
+    if (i < n && !cell_code(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], levels, &code)) {
+      raise_status(status, FHV_RANGE);
+      code = ~0ull;
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, code);
+    if (code != ~0ull && (int)lane_id() == __ffs(grp) - 1) atomicAdd(&counts[code], (uint32_t)__popc(grp));
+  }
+}
+
+__global__ void k_pool_leaf_scatter(const float* __restrict__ spos, const float* __restrict__ snrm,
+                                    const uint32_t* __restrict__ smat, const uint32_t* __restrict__ sobj, long long n,
+                                    int levels, const uint32_t* __restrict__ offsets, uint32_t* __restrict__ cursors,
+                                    float* __restrict__ dpos, float* __restrict__ dnrm, uint32_t* __restrict__ dmat,
+                                    uint32_t* __restrict__ dobj, int32_t* __restrict__ dprev) {
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31u); i0 < n;
+       i0 += (long long)gridDim.x * blockDim.x) {
+    const long long i = i0 + lane_id();
+    uint64_t code = ~0ull;
+    if (i < n && !cell_code(spos[3 * i], spos[3 * i + 1], spos[3 * i + 2], levels, &code)) code = ~0ull;
+    const unsigned grp = __match_any_sync(0xffffffffu, code);
+    const int leader = __ffs(grp) - 1;
+    uint32_t base = 0;
+    if (code != ~0ull && (int)lane_id() == leader) base = atomicAdd(&cursors[code], (uint32_t)__popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (code == ~0ull) continue;
+    const long long d = (long long)offsets[code] + base + __popc(grp & ((1u << lane_id()) - 1u));
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      dpos[3 * d + e] = spos[3 * i + e];
+      dnrm[3 * d + e] = snrm[3 * i + e];
+    }
+    dmat[d] = smat[i];
+    dobj[d] = sobj[i];
+    dprev[d] = (int32_t)i;
+  }
+}
+
+// FHV1 snapshot records (fhv/storage.py:57-66, 725-808): SoA pool <-> packed
+// little-endian 36-byte RECORD_DTYPE rows (pos f32x3, nrm f32x3, material
+// u32, object u32, prev i32), one 4-byte word per thread
+__global__ void k_pack_records(const float* __restrict__ pos, const float* __restrict__ nrm,
+                               const uint32_t* __restrict__ mat, const uint32_t* __restrict__ obj,
+                               const int32_t* __restrict__ prev, long long n, uint32_t* __restrict__ out) {
+  const long long words = 9 * n;
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < words;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long r = w / 9;
+    const int f = (int)(w - 9 * r);
+    uint32_t v;
+    if (f < 3) v = __float_as_uint(pos[3 * r + f]);
+    else if (f < 6) v = __float_as_uint(nrm[3 * r + f - 3]);
+    else if (f == 6) v = mat[r];
+    else if (f == 7) v = obj[r];
+    else v = (uint32_t)prev[r];
+    out[w] = v;
+  }
+}
+
+__global__ void k_unpack_records(const uint32_t* __restrict__ in, long long n, float* __restrict__ pos,
+                                 float* __restrict__ nrm, uint32_t* __restrict__ mat, uint32_t* __restrict__ obj,
+                                 int32_t* __restrict__ prev) {
+  const long long words = 9 * n;
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < words;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long r = w / 9;
+    const int f = (int)(w - 9 * r);
+    const uint32_t v = in[w];
+    if (f < 3) pos[3 * r + f] = __uint_as_float(v);
+    else if (f < 6) nrm[3 * r + f - 3] = __uint_as_float(v);
+    else if (f == 6) mat[r] = v;
+    else if (f == 7) obj[r] = v;
+    else prev[r] = (int32_t)v;
+  }
+}
+
+// deferred pass: flag the jobs whose batch holds exactly one fragment
+__global__ void k_job_n1(long long n_jobs, const uint32_t* __restrict__ job_items,
+                         const unsigned long long* __restrict__ job_item_off, const uint32_t* __restrict__ item_cnt,
+                         JobPersp* __restrict__ persp) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n_jobs;
+       j += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long b = job_item_off[j];
+    unsigned long long n = 0;
+    for (uint32_t k = 0; k < job_items[j] && n < 2; ++k) n += item_cnt[b + k];
+    persp[j].n1 = n == 1 ? 1u : 0u;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host orchestration
 
@@ -968,6 +1176,10 @@ CaptureParams make_params(const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg) 
   CaptureParams p;
   p.strategy = cfg->strategy;
   p.res = cfg->res;
+  p.width = cfg->res;
+  p.height = cfg->res;
+  p.ortho = 1;
+  p.persp = nullptr;
   p.pitch = cfg->pitch;
   std::memcpy(p.proj, cfg->proj, sizeof(p.proj));
   p.n_tri = tris->n_tri;
@@ -1065,7 +1277,7 @@ int emit(fhv_ctx* ctx, const CaptureParams& p, const EmitOut& o, bool atomic_all
   const auto* im = (const uint4*)ctx->bufs[kItemMask].ptr;
   const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
   {
-    LaunchScope L_(ctx, kStEmitList + (kMode - kList), s);
+    LaunchScope L_(ctx, kMode >= kDsDepth ? kStDeferred : kStEmitList + (kMode - kList), s);
     if (atomic_alloc)
       k_emit<kMode, true><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, im, n, o, ctx->ctl);
     else
@@ -1383,6 +1595,127 @@ extern "C" int fhv_pofa_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_
                                 const uint32_t* counts, const uint32_t* offsets, fhv_pool_t* pool, int32_t flags,
                                 void* stream) {
   return fhv_pofa_shard_scatter(ctx, tris, cfg, levels, nullptr, counts, offsets, 0, pool, flags, stream);
+}
+
+// deferred_baseline (fhv/render.py:327-382): every triangle through the
+// camera (_raster_screen), nearest (depth, triangle) per pixel into the f64
+// G-buffer, then one Blinn-Phong pass.  gb must carry all five planes.
+extern "C" int fhv_deferred(fhv_ctx* ctx, const fhv_tris_t* tris, const double* proj, int32_t width, int32_t height,
+                            const double* eye, const fhv_shading_t* shading, const double* background,
+                            double* out_rgba, double* out_depth, const fhv_gbuffer_t* gb, int64_t* emitted,
+                            void* stream) {
+  if (!ctx || !tris || !proj || !eye || !shading || !background || !out_rgba || !out_depth || !gb || width < 1 ||
+      height < 1 || !gb->position || !gb->normal || !gb->material_id || !gb->object_id || !gb->valid)
+    return FHV_BAD_ARGS;
+  if (tris->n_tri < 0 || (tris->n_tri > 0 && (!tris->pos || !tris->vnrm || !tris->fnrm || !tris->mat || !tris->obj)))
+    return FHV_BAD_ARGS;
+  if (tris->n_tri >= (1LL << 32) - 1) return FHV_BAD_ARGS;
+  cudaStream_t s = (cudaStream_t)stream;
+  CaptureParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.strategy = kScreen;
+  p.res = height;
+  p.width = width;
+  p.height = height;
+  p.ortho = proj[12] == 0.0 && proj[13] == 0.0 && proj[14] == 0.0 && proj[15] == 1.0;
+  std::memcpy(p.proj[0], proj, 16 * sizeof(double));
+  p.n_tri = tris->n_tri;
+  p.n_jobs = tris->n_tri;
+  p.pos = tris->pos;
+  p.vnrm = tris->vnrm;
+  p.fnrm = tris->fnrm;
+  p.mat = tris->mat;
+  p.obj = tris->obj;
+  p.cell_hi = ~0ull;
+  const long long P = (long long)width * height;
+  p.persp = (JobPersp*)scratch(ctx, kJobPersp, (size_t)(p.n_jobs > 0 ? p.n_jobs : 1) * sizeof(JobPersp));
+  auto* key = (unsigned long long*)scratch(ctx, kSplatKey, (size_t)P * 8);
+  auto* win = (uint32_t*)scratch(ctx, kSplatWin, (size_t)P * 4);
+  if (!p.persp || !key || !win) return FHV_NOMEM;
+  int rc;
+  if ((rc = plan(ctx, p, s))) return rc;
+  if ((rc = count(ctx, p, false, 0, nullptr, s))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(key, 0xff, (size_t)P * 8, s)))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(win, 0xff, (size_t)P * 4, s)))) return rc;
+  if (ctx->n_items > 0) {
+    {
+      LaunchScope L_(ctx, kStDeferred, s);
+      k_job_n1<<<grid_for(p.n_jobs, 256), 256, 0, s>>>(p.n_jobs, (const uint32_t*)ctx->bufs[kJobItems].ptr,
+                                                       (const unsigned long long*)ctx->bufs[kJobItemOff].ptr,
+                                                       (const uint32_t*)ctx->bufs[kItemCnt].ptr, p.persp);
+    }
+    if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+    EmitOut o = empty_out();
+    o.ds_key = key;
+    o.ds_win = win;
+    o.gb = *gb;
+    if ((rc = emit<kDsDepth>(ctx, p, o, false, s))) return rc;
+    if ((rc = emit<kDsIndex>(ctx, p, o, false, s))) return rc;
+    if ((rc = emit<kDsWrite>(ctx, p, o, false, s))) return rc;
+  }
+  if ((rc = deferred_resolve(ctx, P, shading, eye, key, win, gb, background, out_rgba, out_depth, s))) return rc;
+  rc = sync_control(ctx, s);
+  if (emitted) *emitted = (int64_t)ctx->ctl_host->scan_total;
+  return rc;
+}
+
+extern "C" int fhv_rebuild_pofa(fhv_ctx* ctx, int32_t levels, const fhv_pool_t* src, int64_t n, uint32_t* counts,
+                                uint32_t* offsets, uint8_t* pyramid, fhv_pool_t* dst, void* stream) {
+  if (!ctx || !src || !dst || !counts || !offsets || !pyramid || levels < 1 || levels > 10 || n < 0 ||
+      n > src->capacity || dst->capacity < n || n >= (1LL << 31))
+    return FHV_BAD_ARGS;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long n_leaves = 1LL << (3 * levels);
+  uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_leaves * 4);
+  if (!cursors) return FHV_NOMEM;
+  int rc;
+  if ((rc = reset_control(ctx, s))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(counts, 0, (size_t)n_leaves * 4, s)))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_leaves * 4, s)))) return rc;
+  if (n > 0) {
+    LaunchScope L_(ctx, kStCountLeaves, s);
+    k_pool_leaf_hist<<<grid_for(n, 256), 256, 0, s>>>(src->pos, n, levels, counts, &ctx->ctl->status);
+  }
+  if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  if ((rc = scan_leaves_and_pyramid(ctx, counts, offsets, pyramid, levels, s))) return rc;
+  if (n > 0) {
+    {
+      LaunchScope L_(ctx, kStEmitPofa, s);
+      k_pool_leaf_scatter<<<grid_for(n, 256), 256, 0, s>>>(src->pos, src->nrm, src->mat, src->obj, n, levels, offsets,
+                                                           cursors, dst->pos, dst->nrm, dst->mat, dst->obj, dst->prev);
+    }
+    {
+      LaunchScope L_(ctx, kStLeafOrder, s);
+      k_leaf_order<<<grid_for(n_leaves, 128, 32), 128, 0, s>>>(offsets, counts, n_leaves, 0ull, dst->pos, dst->nrm,
+                                                               dst->mat, dst->obj, dst->prev);
+    }
+    if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  }
+  return sync_control(ctx, s);
+}
+
+extern "C" int fhv_pack_records(fhv_ctx* ctx, const fhv_pool_t* pool, int64_t n, void* out, void* stream) {
+  if (!ctx || !pool || n < 0 || n > pool->capacity || (n > 0 && !out) || ((uintptr_t)out & 3)) return FHV_BAD_ARGS;
+  if (n == 0) return FHV_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    LaunchScope L_(ctx, kStLeafOrder, s);
+    k_pack_records<<<grid_for(9 * n, 256), 256, 0, s>>>(pool->pos, pool->nrm, pool->mat, pool->obj, pool->prev, n,
+                                                        (uint32_t*)out);
+  }
+  return check_cuda(ctx, cudaGetLastError());
+}
+
+extern "C" int fhv_unpack_records(fhv_ctx* ctx, const void* in, int64_t n, fhv_pool_t* pool, void* stream) {
+  if (!ctx || !pool || n < 0 || n > pool->capacity || (n > 0 && !in) || ((uintptr_t)in & 3)) return FHV_BAD_ARGS;
+  if (n == 0) return FHV_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    LaunchScope L_(ctx, kStLeafOrder, s);
+    k_unpack_records<<<grid_for(9 * n, 256), 256, 0, s>>>((const uint32_t*)in, n, pool->pos, pool->nrm, pool->mat,
+                                                          pool->obj, pool->prev);
+  }
+  return check_cuda(ctx, cudaGetLastError());
 }
 
 extern "C" int fhv_face_normals(fhv_ctx* ctx, int64_t n_tri, const double* pos, double* fnrm, void* stream) {

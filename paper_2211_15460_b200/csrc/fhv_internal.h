@@ -39,7 +39,7 @@ namespace fhv {
 enum Stage {
   kStJobSetup = 0, kStScan, kStItemExpand, kStCount, kStCountLeaves, kStEmitList, kStEmitPpfl, kStEmitPofl,
   kStEmitPofa, kStChainOrder, kStLeafOrder, kStScanLeaves, kStPyramid, kStSplatDepth, kStSplatIndex,
-  kStSplatResolve, kStRaycast, kStFaceNormals, kNumStages
+  kStSplatResolve, kStRaycast, kStFaceNormals, kStDeferred, kNumStages
 };
 struct PendingEvent {
   int stage;
@@ -72,7 +72,7 @@ namespace fhv {
 enum BufId {
   kJobs = 0, kJobItems, kJobItemOff, kItemJob, kItemP0, kItemCnt, kItemOff, kScanStatus,
   kCursors, kChainScratch, kSplatKey, kSplatWin, kSplatBox, kRays, kTmp0, kTmp1, kTriFlag, kTriOff, kTriIndex,
-  kShardBoxes, kItemMask, kNumBufs
+  kShardBoxes, kItemMask, kJobPersp, kNumBufs
 };
 
 // Counts a launch and, when profiling is on, brackets it with CUDA events on
@@ -105,5 +105,9 @@ int scan_leaf_range_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* 
                                 int levels, uint64_t lo, uint64_t hi, uint64_t base, cudaStream_t s);
 int pyramid_from_heads(fhv_ctx* ctx, const int32_t* heads, uint8_t* pyramid, int levels, cudaStream_t s);
 int pyramid_upper_levels(fhv_ctx* ctx, uint8_t* pyramid, int levels, cudaStream_t s);
+// deferred_baseline lighting pass over the G-buffer the geometry pass left (fhv_splat.cu)
+int deferred_resolve(fhv_ctx* ctx, long long P, const fhv_shading_t* sh, const double* eye,
+                     const unsigned long long* key, const uint32_t* win, const fhv_gbuffer_t* gb, const double* bg,
+                     double* out_rgba, double* out_depth, cudaStream_t s);
 
 }  // namespace fhv

@@ -15,7 +15,8 @@ from .lights import (GBuffer, ImageBuffer, Light, composite_over, front_to_back_
                      write_float_dump, write_ppm)
 from .scene import Camera, SceneError
 
-__all__ = ["GBuffer", "ImageBuffer", "Light", "composite_over", "front_to_back_accumulate", "headlight",
+__all__ = ["GBuffer", "ImageBuffer", "Light", "composite_over", "deferred_baseline", "front_to_back_accumulate",
+           "headlight",
            "material_arrays", "read_float_dump", "read_ppm", "resolve_over_background", "splat_render",
            "srgb_encode", "write_float_dump", "write_ppm"]
 
@@ -56,6 +57,49 @@ def splat_render(pool, camera: Camera, lights, splat_radius_world: float, materi
                        gb, _lib.FHV_SPLAT_PACKED if packed else 0, _lib.stream_ptr(dev))
     _lib.check(rc, "splat_render")
     return out
+
+
+def deferred_baseline(scene, camera: Camera, lights, background=(0.0, 0.0, 0.0, 0.0), *, device=None,
+                      tris=None, shading: DeviceShading | None = None, out=None):
+    """Two-phase reference renderer (fhv/render.py:327-382) on the device:
+    depth-tested geometry pass into a G-buffer (nearest f64 depth per pixel,
+    equal depths keep the earlier triangle), then one shading pass.
+
+    Returns ``(ImageBuffer, GBuffer)`` of CUDA tensors with the reference's
+    dtypes (f64 pixels / depth / position / normal, int32 ids, bool valid).
+    ``tris``: a DeviceScene already holding the scene; ``shading``: prebuilt
+    DeviceShading; ``out``: a previous ``(ImageBuffer, GBuffer)`` to reuse.
+    """
+    from .device import device_scene
+    from .raster import RasterConfig
+    ds = tris if tris is not None else device_scene(scene, device)
+    dev = ds.device
+    w, h = camera.resolution
+    if out is None:
+        img = ImageBuffer(w, h, torch.empty((h, w, 4), dtype=torch.float64, device=dev),
+                          torch.empty((h, w), dtype=torch.float64, device=dev))
+        gb = GBuffer(torch.empty((h, w, 3), dtype=torch.float64, device=dev),
+                     torch.empty((h, w, 3), dtype=torch.float64, device=dev),
+                     torch.empty((h, w), dtype=torch.int32, device=dev),
+                     torch.empty((h, w), dtype=torch.int32, device=dev),
+                     torch.empty((h, w), dtype=torch.bool, device=dev))
+    else:
+        img, gb = out
+    if shading is None:
+        shading = DeviceShading(scene.materials, lights, dev)
+    proj = host_f64(RasterConfig.from_camera(camera).projection).reshape(16)
+    eye = host_f64(camera.eye)
+    bg = host_f64(background)
+    g = _lib.GBuf(_lib.ptr(gb.position), _lib.ptr(gb.normal), _lib.ptr(gb.material_id), _lib.ptr(gb.object_id),
+                  _lib.ptr(gb.valid))
+    import ctypes
+    n = ctypes.c_int64(0)
+    lib = _lib.load()
+    rc = lib.fhv_deferred(_lib.ctx(dev), ds.struct(), proj.ctypes.data, int(w), int(h), eye.ctypes.data,
+                          shading.struct(), bg.ctypes.data, _lib.ptr(img.pixels), _lib.ptr(img.depth), g,
+                          ctypes.byref(n), _lib.stream_ptr(dev))
+    _lib.check(rc, "deferred_baseline")
+    return img, gb
 
 
 def device_gbuffer(width: int, height: int, device) -> GBuffer:

@@ -475,41 +475,22 @@ def ctypes_i64():
 
 
 def rebuild_pofl_as_pofa(fhv: FhvPofl) -> FhvPofa:
-    """Repack a POFL into POFA (fhv/storage.py:624-652): group by leaf in
-    Morton order, keep emission (pool) order inside each leaf.  Uses device
-    tensor ops (a stable sort by leaf code); not on the timed path."""
+    """Repack a POFL into POFA (fhv/storage.py:624-652) on the device: leaf
+    histogram of the f32 positions, offsets + pyramid (the POFA directory
+    kernel), scatter into leaf ranges, stable in-leaf order restored by pool
+    index.  Records: same bytes as the reference's lexsort repack."""
     pool = fhv.pool
     n, L, dev = pool.stored_count, fhv.levels, pool.device
-    pos = pool.position[:n].to(torch.float64)
-    side = float(1 << L)
-    idx = torch.clamp(torch.floor(pos * side).to(torch.int64), 0, (1 << L) - 1).cpu().numpy()
-    codes = morton_encode(idx[:, 0], idx[:, 1], idx[:, 2], L) if n else np.empty(0, np.int64)
-    counts64 = np.bincount(codes, minlength=8 ** L)
-    counts = counts64.astype(np.uint32)
-    offsets = np.concatenate(([0], np.cumsum(counts[:-1], dtype=np.int64))).astype(np.uint32)
-    perm = torch.from_numpy(np.lexsort((np.arange(n), codes))).to(dev)
-    new = FragmentPool(n, dev)
-    new.position.copy_(pool.position[:n][perm])
-    new.normal.copy_(pool.normal[:n][perm])
-    new.material_id.copy_(pool.material_id[:n].view(torch.int32)[perm].view(torch.uint32))
-    new.object_id.copy_(pool.object_id[:n].view(torch.int32)[perm].view(torch.uint32))
+    counts = torch.empty(8 ** L, dtype=torch.uint32, device=dev)
+    offsets = torch.empty(8 ** L, dtype=torch.uint32, device=dev)
+    pyr = OccupancyPyramid(L, device=dev)
+    new = FragmentPool(n, dev, fill_prev=False)  # every prev is written (-1)
+    lib = _lib.load()
+    rc = lib.fhv_rebuild_pofa(_lib.ctx(dev), L, pool.struct(), n, _lib.ptr(counts), _lib.ptr(offsets),
+                              _lib.ptr(pyr.data), new.struct(), _lib.stream_ptr(dev))
+    _lib.check(rc, "rebuild_pofl_as_pofa")
     new.next_free = n
-    occ = np.repeat(False, 8 ** L) if n == 0 else counts > 0
-    pyr = _pyramid_from_occupancy_host(occ, L, dev)
-    d = PofaDirectory(L, torch.from_numpy(offsets.view(np.int32)).to(dev).view(torch.uint32),
-                      torch.from_numpy(counts.view(np.int32)).to(dev).view(torch.uint32))
-    return FhvPofa(d, pyr, new, fhv.capture_resolution, fhv.stats, fhv.materials)
-
-
-def _pyramid_from_occupancy_host(occ: np.ndarray, L: int, dev) -> OccupancyPyramid:
-    levels = [None] * L
-    bits = 1 << np.arange(8, dtype=np.uint32)
-    cur = np.asarray(occ, dtype=bool)
-    for k in range(L - 1, -1, -1):
-        masks = (cur.reshape(-1, 8).astype(np.uint32) * bits).sum(axis=1).astype(np.uint8)
-        levels[k] = masks
-        cur = masks > 0
-    return OccupancyPyramid(L, torch.from_numpy(np.concatenate(levels)).to(dev))
+    return FhvPofa(PofaDirectory(L, offsets, counts), pyr, new, fhv.capture_resolution, fhv.stats, fhv.materials)
 
 
 # ---------------------------------------------------------------------------
@@ -567,27 +548,35 @@ SNAPSHOT_MAGIC = b"FHV1"
 _HEADER = struct.Struct("<4s4sIIIIQ")
 
 
+def _pack_pool(pool: FragmentPool, n: int) -> torch.Tensor:
+    """The first n records as packed 36-byte RECORD_DTYPE rows, on the device."""
+    out = torch.empty(36 * n, dtype=torch.uint8, device=pool.device)
+    rc = _lib.load().fhv_pack_records(_lib.ctx(pool.device), pool.struct(), n, _lib.ptr(out),
+                                      _lib.stream_ptr(pool.device))
+    _lib.check(rc, "snapshot pack")
+    return out
+
+
 def snapshot_bytes(fhv) -> bytes:
+    """FHV1 snapshot (fhv/storage.py:725-755): header, directory, pyramid
+    levels, packed records.  Assembled in device memory (records packed by a
+    kernel straight from the SoA pool) and read back in ONE copy."""
     pool = fhv.pool
     count = pool.stored_count
-    parts = []
     if fhv.layout == "PPFL":
         d = fhv.directory
-        parts += [_HEADER.pack(SNAPSHOT_MAGIC, b"PPFL", 0, d.width, d.height, RECORD_SIZE_PACKED, count),
-                  d.heads.cpu().numpy().astype("<i4").tobytes()]
+        header = _HEADER.pack(SNAPSHOT_MAGIC, b"PPFL", 0, d.width, d.height, RECORD_SIZE_PACKED, count)
+        planes = [d.heads]
     elif fhv.layout in ("POFL", "POFA"):
         r = fhv.capture_resolution
-        parts.append(_HEADER.pack(SNAPSHOT_MAGIC, fhv.layout.encode(), fhv.levels, r, r, RECORD_SIZE_PACKED, count))
-        if fhv.layout == "POFL":
-            parts.append(fhv.directory.heads.cpu().numpy().astype("<i4").tobytes())
-        else:
-            parts.append(fhv.directory.offsets.cpu().numpy().astype("<u4").tobytes())
-            parts.append(fhv.directory.counts.cpu().numpy().astype("<u4").tobytes())
-        parts.append(fhv.pyramid.data.cpu().numpy().tobytes())
+        header = _HEADER.pack(SNAPSHOT_MAGIC, fhv.layout.encode(), fhv.levels, r, r, RECORD_SIZE_PACKED, count)
+        planes = [fhv.directory.heads] if fhv.layout == "POFL" else [fhv.directory.offsets, fhv.directory.counts]
+        planes.append(fhv.pyramid.data)
     else:
         raise FhvError(f"cannot snapshot layout {fhv.layout!r}")
-    parts.append(pool.to_struct_array().tobytes())
-    return b"".join(parts)
+    planes = [t.contiguous().view(torch.uint8).reshape(-1) for t in planes] + [_pack_pool(pool, count)]
+    body = torch.cat(planes) if planes else torch.empty(0, dtype=torch.uint8)
+    return header + body.cpu().numpy().tobytes()
 
 
 def save_snapshot(fhv, path) -> None:
@@ -616,9 +605,20 @@ def load_snapshot(path, materials=None, device=None):
     def dev32(a):
         return torch.from_numpy(a.view(np.int32)).to(dev)
 
+    def records(n):
+        # validated on the host like the reference (np.frombuffer raises on a
+        # short buffer), then ONE upload of the packed rows, unpacked by a kernel
+        rec = take(RECORD_DTYPE, n)
+        pool = FragmentPool(n, dev, fill_prev=False)
+        raw = torch.from_numpy(rec.view(np.uint8).reshape(-1)).to(dev)
+        rc = _lib.load().fhv_unpack_records(_lib.ctx(dev), _lib.ptr(raw), n, pool.struct(), _lib.stream_ptr(dev))
+        _lib.check(rc, "snapshot unpack")
+        pool.next_free = n
+        return pool
+
     if layout == b"PPFL":
         heads = take("<i4", w * h)
-        pool = FragmentPool.from_struct_array(take(RECORD_DTYPE, count), dev)
+        pool = records(count)
         return FhvPpfl(PixelDirectory(w, h, dev32(heads)), pool, h, materials=materials)
     if layout in (b"POFL", b"POFA"):
         if layout == b"POFL":
@@ -627,7 +627,7 @@ def load_snapshot(path, materials=None, device=None):
             offs = take("<u4", 8 ** levels)
             cnts = take("<u4", 8 ** levels)
         pyr = np.concatenate([take(np.uint8, 8 ** k) for k in range(levels)])
-        pool = FragmentPool.from_struct_array(take(RECORD_DTYPE, count), dev)
+        pool = records(count)
         pyramid = OccupancyPyramid(levels, torch.from_numpy(pyr).to(dev))
         if layout == b"POFL":
             return FhvPofl(PoflDirectory(levels, dev32(heads)), pyramid, pool, h, materials=materials)
