@@ -339,6 +339,17 @@ def main():
         out_px = [torch.empty((H, W, 4), dtype=torch.float64).pin_memory() for _ in range(2)]
         out_dp = [torch.empty((H, W), dtype=torch.float64).pin_memory() for _ in range(2)]
         h2d = sum(p.numel() * p.element_size() for p in pin)
+        # the link itself: the same pinned uploads alone (PCIe bound of the e2e line)
+        torch.cuda.synchronize()
+        el0, el1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        el0.record(stream)
+        for _ in range(3):
+            for d_, src in zip((ds.pos, ds.vnrm) + (() if derive_fn else (ds.fnrm,)) +
+                               (ds.mat.view(torch.int32), ds.obj.view(torch.int32)), pin):
+                d_.copy_(src, non_blocking=True)
+        el1.record(stream)
+        torch.cuda.synchronize()
+        h2d_gbs = 3 * h2d / (el0.elapsed_time(el1) / 1e3) / 1e9
         d2h = out_px[0].numel() * 8 + out_dp[0].numel() * 8
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         K = args.steps
@@ -396,7 +407,7 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps,
                "pipeline": "2-deep: H2D(k+1) and D2H(k-1) on copy streams overlap step k",
                "face_normals": "derived on device (bit-identical)" if derive_fn else "uploaded",
-               "readback_matches_device": bool(ok)}
+               "readback_matches_device": bool(ok), "h2d_link_gbs": round(h2d_gbs, 1)}
     else:
         e2e = None
 

@@ -288,12 +288,17 @@ constexpr uint32_t kExpandSmall = 4;
 
 __global__ void __launch_bounds__(256) k_item_expand(long long n_jobs, const uint32_t* __restrict__ job_items,
                                                      const unsigned long long* __restrict__ job_item_off,
-                                                     uint32_t* __restrict__ item_job, uint32_t* __restrict__ item_p0) {
+                                                     uint32_t* __restrict__ item_job, uint32_t* __restrict__ item_p0,
+                                                     unsigned long long cap, int* status) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long j0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); j0 < n_jobs; j0 += stride) {
     const long long j = j0 + lane_id();
-    const uint32_t n = j < n_jobs ? job_items[j] : 0u;
+    uint32_t n = j < n_jobs ? job_items[j] : 0u;
     const unsigned long long base = j < n_jobs ? job_item_off[j] : 0ull;
+    if (base + n > cap) {  // speculative item buffers too small: the host re-plans with a sync
+      raise_status(status, FHV_RETRY_ITEMS);
+      n = base < cap ? (uint32_t)(cap - base) : 0u;
+    }
     if (n <= kExpandSmall) {
       for (uint32_t k = 0; k < n; ++k) {
         item_job[base + k] = (uint32_t)j;
@@ -436,7 +441,7 @@ constexpr int kRasterWarps = kRasterBlock / 32;
 template <int kMode, bool kAtomicAlloc>
 struct RasterState {
   unsigned long long emitted = 0;
-  bool bad_range = false, bad_pass = false, bad_key = false;
+  bool bad_range = false, bad_pass = false, bad_key = false, short_pool = false;
 };
 
 // one batch of <= 32 fragments, one per lane (valid lanes), called by the
@@ -590,6 +595,10 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
         st.bad_pass = true;
       } else {
         slot = (long long)(pofa_off - o.base) + cur;
+        if (slot >= o.capacity) {  // speculative pool smaller than the exact count
+          st.short_pool = true;
+          slot = -1;
+        }
       }
     }
   } else {
@@ -650,7 +659,8 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
                                                          const uint32_t* __restrict__ item_job,
                                                          const uint32_t* __restrict__ item_p0,
                                                          const unsigned long long* __restrict__ item_off,
-                                                         long long n_items, uint32_t* __restrict__ item_cnt,
+                                                         long long n_items, const unsigned long long* n_dev,
+                                                         uint32_t* __restrict__ item_cnt,
                                                          uint4* __restrict__ item_mask, EmitOut o, Control* ctl) {
   static_assert(kMode == kCnt || kMode == kCntLeaves, "k_raster is the counting pass; emission is k_emit");
   constexpr bool kOwned = kMode == kCntLeaves || kMode == kPofa;
@@ -668,6 +678,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
   uint32_t* own_cnt = own_all[wib];
   uint32_t* ijob = ijob_all[wib];
   const unsigned below = (1u << lane) - 1u;
+  if (n_dev && (long long)*n_dev < n_items) n_items = (long long)*n_dev;  // speculative launch (cap >= count)
   const long long n_groups = (n_items + 31) / 32;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   RasterState<kMode, kAtomicAlloc> st;
@@ -817,7 +828,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
                                                        const uint32_t* __restrict__ item_p0,
                                                        const unsigned long long* __restrict__ item_off,
                                                        const uint4* __restrict__ item_mask, long long n_items,
-                                                       EmitOut o, Control* ctl) {
+                                                       const unsigned long long* n_dev, EmitOut o, Control* ctl) {
   static_assert(kMode == kList || kMode == kPpfl || kMode == kPofl || kMode == kPofa || kMode == kDsDepth ||
                     kMode == kDsIndex || kMode == kDsWrite,
                 "emission modes only");
@@ -829,6 +840,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
   CoverS* cs = cs_all[wib];
   uint32_t* own_cnt = own_all[wib];
   uint32_t* ijob = ijob_all[wib];
+  if (n_dev && (long long)*n_dev < n_items) n_items = (long long)*n_dev;
   const long long n_groups = (n_items + 31) / 32;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   RasterState<kMode, kAtomicAlloc> st;
@@ -907,6 +919,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
   if (st.bad_range) raise_status(&ctl->status, FHV_RANGE);
   if (st.bad_pass) raise_status(&ctl->status, FHV_PASS_MISMATCH);
   if (st.bad_key) raise_status(&ctl->status, FHV_BAD_ARGS);
+  if (st.short_pool) raise_status(&ctl->status, FHV_NEED_POOL);
 }
 
 // ---------------------------------------------------------------------------
@@ -974,13 +987,15 @@ __global__ void k_chain_order(int32_t* __restrict__ heads, int32_t* __restrict__
 // pofa_scatter, fhv/_ckern.pyx:135-142) from the parked ranks, then
 // prev_index = -1 (fhv/storage.py:439)
 __global__ void k_leaf_order(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts,
-                             long long n_leaves, unsigned long long base, float* __restrict__ pos, float* __restrict__ nrm,
-                             uint32_t* __restrict__ mat, uint32_t* __restrict__ obj, int32_t* __restrict__ prev) {
+                             long long n_leaves, unsigned long long base, unsigned long long cap,
+                             float* __restrict__ pos, float* __restrict__ nrm, uint32_t* __restrict__ mat,
+                             uint32_t* __restrict__ obj, int32_t* __restrict__ prev) {
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n_leaves;
        c += (long long)gridDim.x * blockDim.x) {
     const uint32_t n = counts[c];
     if (n == 0) continue;
     const long long off = (long long)(offsets[c] - base);
+    if ((unsigned long long)off + n > cap) continue;  // speculative pool too small: the caller re-scatters
     uint32_t* rk = reinterpret_cast<uint32_t*>(prev + off);
     for (uint32_t i = 1; i < n; ++i) {
       const uint32_t r = rk[i];
@@ -1203,12 +1218,18 @@ int validate(const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg) {
   return FHV_OK;
 }
 
-// job setup + work-item expansion; leaves ctx->n_jobs / n_items (sync #1)
-int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s) {
+// job setup + work-item expansion.  The number of work items is data
+// dependent.  Exact path: sync once, size the item buffers.  Speculative path
+// (allow_spec, same job count as the last exact plan on this ctx): launch on
+// the grow-only buffers of that plan without waiting; every item kernel reads
+// the true count from ctl->items_total, k_item_expand raises FHV_RETRY_ITEMS
+// if it does not fit, and the caller's final sync re-plans exactly.
+int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s, bool allow_spec = false) {
   int rc = reset_control(ctx, s);
   if (rc) return rc;
   ctx->n_jobs = p.n_jobs;
   ctx->n_items = 0;
+  ctx->spec = false;
   if (p.n_jobs == 0) return FHV_OK;
   JobSetup* jobs = (JobSetup*)scratch(ctx, kJobs, (size_t)p.n_jobs * sizeof(JobSetup));
   uint32_t* job_items = (uint32_t*)scratch(ctx, kJobItems, (size_t)p.n_jobs * 4);
@@ -1220,20 +1241,36 @@ int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s) {
   }
   if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
   if ((rc = scan_u32_to_u64(ctx, job_items, job_item_off, p.n_jobs, s))) return rc;
-  if ((rc = sync_control(ctx, s))) return rc;
-  const long long n_items = (long long)ctx->ctl_host->scan_total;
-  ctx->n_items = n_items;
+  if ((rc = check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->items_total, &ctx->ctl->scan_total, sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToDevice, s))))
+    return rc;
+  const bool spec = allow_spec && ctx->last_n_jobs == p.n_jobs && ctx->item_cap > 0;
+  long long n_items;
+  if (spec) {
+    n_items = ctx->item_cap;
+  } else {
+    if ((rc = sync_control(ctx, s))) return rc;
+    n_items = (long long)ctx->ctl_host->scan_total;
+    ctx->last_n_jobs = p.n_jobs;
+    if (n_items > ctx->item_cap) ctx->item_cap = n_items;
+  }
   if (n_items == 0) return FHV_OK;
   if (n_items >= (1LL << 31)) return FHV_NOMEM;
   uint32_t* item_job = (uint32_t*)scratch(ctx, kItemJob, (size_t)n_items * 4);
   uint32_t* item_p0 = (uint32_t*)scratch(ctx, kItemP0, (size_t)n_items * 4);
   if (!item_job || !item_p0) return FHV_NOMEM;
+  ctx->n_items = n_items;
+  ctx->spec = spec;
   {
     LaunchScope L_(ctx, kStItemExpand, s);
-    k_item_expand<<<grid_for(p.n_jobs, 256), 256, 0, s>>>(p.n_jobs, job_items, job_item_off, item_job, item_p0);
+    k_item_expand<<<grid_for(p.n_jobs, 256), 256, 0, s>>>(p.n_jobs, job_items, job_item_off, item_job, item_p0,
+                                                          (unsigned long long)n_items, &ctx->ctl->status);
   }
   return check_cuda(ctx, cudaGetLastError());
 }
+
+// device-side item count of a speculative plan (nullptr: ctx->n_items is exact)
+inline const unsigned long long* items_dev(fhv_ctx* ctx) { return ctx->spec ? &ctx->ctl->items_total : nullptr; }
 
 // counts per item (+ leaf histogram) and their scan (fragment ranks); async
 int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_t* leaf_counts, cudaStream_t s) {
@@ -1242,6 +1279,7 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
   auto* item_off = (unsigned long long*)scratch(ctx, kItemOff, (size_t)(n > 0 ? n : 1) * 8);
   auto* item_mask = (uint4*)scratch(ctx, kItemMask, (size_t)(n > 0 ? n : 1) * 16);
   if (!item_cnt || !item_off || !item_mask) return FHV_NOMEM;
+  const unsigned long long* nd = items_dev(ctx);
   if (n > 0) {
     const JobSetup* jobs = (const JobSetup*)ctx->bufs[kJobs].ptr;
     const uint32_t* ij = (const uint32_t*)ctx->bufs[kItemJob].ptr;
@@ -1254,16 +1292,16 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
     {
       LaunchScope L_(ctx, leaves ? kStCountLeaves : kStCount, s);
       if (leaves)
-        k_raster<kCntLeaves, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, item_cnt, item_mask, o,
-                                                                   ctx->ctl);
+        k_raster<kCntLeaves, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, nd, item_cnt, item_mask,
+                                                                   o, ctx->ctl);
       else
-        k_raster<kCnt, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, item_cnt, item_mask, o,
+        k_raster<kCnt, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, nd, item_cnt, item_mask, o,
                                                              ctx->ctl);
     }
     int rc = check_cuda(ctx, cudaGetLastError());
     if (rc) return rc;
   }
-  return scan_u32_to_u64(ctx, item_cnt, item_off, n, s);
+  return scan_u32_to_u64(ctx, item_cnt, item_off, n, s, nd);
 }
 
 template <int kMode>
@@ -1275,13 +1313,14 @@ int emit(fhv_ctx* ctx, const CaptureParams& p, const EmitOut& o, bool atomic_all
   const uint32_t* ip = (const uint32_t*)ctx->bufs[kItemP0].ptr;
   const auto* io = (const unsigned long long*)ctx->bufs[kItemOff].ptr;
   const auto* im = (const uint4*)ctx->bufs[kItemMask].ptr;
+  const unsigned long long* nd = items_dev(ctx);
   const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
   {
     LaunchScope L_(ctx, kMode >= kDsDepth ? kStDeferred : kStEmitList + (kMode - kList), s);
     if (atomic_alloc)
-      k_emit<kMode, true><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, im, n, o, ctx->ctl);
+      k_emit<kMode, true><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, im, n, nd, o, ctx->ctl);
     else
-      k_emit<kMode, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, im, n, o, ctx->ctl);
+      k_emit<kMode, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, io, im, n, nd, o, ctx->ctl);
   }
   return check_cuda(ctx, cudaGetLastError());
 }
@@ -1354,29 +1393,35 @@ static int build_linked(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_
   cudaStream_t s = (cudaStream_t)stream;
   const CaptureParams p = make_params(tris, cfg);
   const bool atomic_alloc = (flags & FHV_ALLOC_ATOMIC) != 0;
-  if ((rc = plan(ctx, p, s))) return rc;
-  // the counting pass also leaves the coverage masks the emission pass enumerates
-  if ((rc = count(ctx, p, false, 0, nullptr, s))) return rc;
-  EmitOut o = empty_out();
-  set_pool(o, pool);
-  o.heads = heads;
-  o.flags = flags;
-  long long n_keys;
-  if (pofl) {
-    o.levels = levels;
-    n_keys = 1LL << (3 * levels);
-  } else {
-    o.width = width;
-    n_keys = (long long)width * (long long)cfg->res;  // caller's directory is width x res
+  const long long n_keys = pofl ? 1LL << (3 * levels) : (long long)width * (long long)cfg->res;  // width x res
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (attempt > 0) {  // the speculative pass ran on too small item buffers: restore the -1 prefills
+      if ((rc = check_cuda(ctx, cudaMemsetAsync(heads, 0xff, (size_t)n_keys * 4, s)))) return rc;
+      if (pool->capacity > 0 &&
+          (rc = check_cuda(ctx, cudaMemsetAsync(pool->prev, 0xff, (size_t)pool->capacity * 4, s))))
+        return rc;
+    }
+    if ((rc = plan(ctx, p, s, attempt == 0))) return rc;
+    // the counting pass also leaves the coverage masks the emission pass enumerates
+    if ((rc = count(ctx, p, false, 0, nullptr, s))) return rc;
+    EmitOut o = empty_out();
+    set_pool(o, pool);
+    o.heads = heads;
+    o.flags = flags;
+    if (pofl)
+      o.levels = levels;
+    else
+      o.width = width;
+    o.n_keys = n_keys;
+    rc = pofl ? emit<kPofl>(ctx, p, o, atomic_alloc, s) : emit<kPpfl>(ctx, p, o, atomic_alloc, s);
+    if (rc) return rc;
+    if (flags & FHV_EXACT_ORDER) {
+      if ((rc = chain_order(ctx, heads, pool->prev, n_keys, pool->capacity, s))) return rc;
+    }
+    if (pofl && (rc = pyramid_from_heads(ctx, heads, pyramid, levels, s))) return rc;
+    rc = sync_control(ctx, s);
+    if (rc != FHV_RETRY_ITEMS) break;
   }
-  o.n_keys = n_keys;
-  rc = pofl ? emit<kPofl>(ctx, p, o, atomic_alloc, s) : emit<kPpfl>(ctx, p, o, atomic_alloc, s);
-  if (rc) return rc;
-  if (flags & FHV_EXACT_ORDER) {
-    if ((rc = chain_order(ctx, heads, pool->prev, n_keys, pool->capacity, s))) return rc;
-  }
-  if (pofl && (rc = pyramid_from_heads(ctx, heads, pyramid, levels, s))) return rc;
-  rc = sync_control(ctx, s);
   const long long total = (long long)(atomic_alloc ? ctx->ctl_host->alloc : ctx->ctl_host->scan_total);
   if (next_free) *next_free = total;
   if (rc == FHV_OK && total > pool->capacity) rc = FHV_OVERFLOW;
@@ -1459,13 +1504,14 @@ namespace {
 // pass 1 up to the per-leaf histogram, no sync after the counting kernel: the
 // item scan's total is parked in ctl->frags_total for the caller's next sync
 int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
-                     const fhv_shard_t* shard, uint32_t* counts_local, cudaStream_t s, CaptureParams& p) {
+                     const fhv_shard_t* shard, uint32_t* counts_local, cudaStream_t s, CaptureParams& p,
+                     bool spec = false) {
   ctx->pass1_levels = -1;
   int rc;
   if ((rc = reset_control(ctx, s))) return rc;
   if ((rc = shard_params(ctx, tris, cfg, levels, shard, true, p, s))) return rc;
   const unsigned long long n_local = p.cell_hi - p.cell_lo;
-  if ((rc = plan(ctx, p, s))) return rc;
+  if ((rc = plan(ctx, p, s, spec))) return rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(counts_local, 0, (size_t)n_local * 4, s)))) return rc;
   if ((rc = count(ctx, p, true, levels, counts_local, s))) return rc;
   return check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total, sizeof(unsigned long long),
@@ -1515,6 +1561,40 @@ extern "C" int fhv_pofa_shard_directory(fhv_ctx* ctx, int32_t levels, const fhv_
   return scan_leaf_range_and_pyramid(ctx, counts_local, offsets_local, pyramid, levels, lo, hi, base, s);
 }
 
+// pass 2 of a POFA build, enqueued only: cursors, scatter, EXACT_ORDER fix-up
+static int pofa_scatter_async(fhv_ctx* ctx, const CaptureParams& p, int32_t levels, unsigned long long lo,
+                              unsigned long long hi, const uint32_t* counts_local, const uint32_t* offsets_local,
+                              uint64_t base, fhv_pool_t* pool, int32_t flags, cudaStream_t s) {
+  const unsigned long long n_local = hi - lo;
+  uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_local * 4);
+  if (!cursors) return FHV_NOMEM;
+  int rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_local * 4, s)))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->alloc, 0, 8, s)))) return rc;
+  // a retry after a speculative pass leaves its FHV_NEED_POOL behind
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->status, 0, sizeof(int), s)))) return rc;
+  EmitOut o = empty_out();
+  set_pool(o, pool);
+  o.levels = levels;
+  o.offsets = offsets_local;
+  o.counts = counts_local;
+  o.cursors = cursors;
+  o.base = base;
+  o.flags = flags;
+  if ((rc = emit<kPofa>(ctx, p, o, false, s))) return rc;
+  if (flags & FHV_EXACT_ORDER) {
+    {
+      LaunchScope L_(ctx, kStLeafOrder, s);
+      k_leaf_order<<<grid_for((long long)n_local, 128, 32), 128, 0, s>>>(offsets_local, counts_local, (long long)n_local,
+                                                                       base, (unsigned long long)pool->capacity,
+                                                                       pool->pos, pool->nrm, pool->mat, pool->obj,
+                                                                       pool->prev);
+    }
+    if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  }
+  return FHV_OK;
+}
+
 static int fhv_pofa_shard_directory_nocheck(fhv_ctx* ctx, int32_t levels, const uint32_t* counts,
                                             uint32_t* offsets, uint8_t* pyramid, cudaStream_t s) {
   return scan_leaves_and_pyramid(ctx, counts, offsets, pyramid, levels, s);
@@ -1535,29 +1615,7 @@ extern "C" int fhv_pofa_shard_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, cons
   cudaStream_t s = (cudaStream_t)stream;
   CaptureParams p;
   if ((rc = shard_params(ctx, tris, cfg, levels, shard, false, p, s))) return rc;
-  const unsigned long long n_local = hi - lo;
-  uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_local * 4);
-  if (!cursors) return FHV_NOMEM;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_local * 4, s)))) return rc;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->alloc, 0, 8, s)))) return rc;
-  EmitOut o = empty_out();
-  set_pool(o, pool);
-  o.levels = levels;
-  o.offsets = offsets_local;
-  o.counts = counts_local;
-  o.cursors = cursors;
-  o.base = base;
-  o.flags = flags;
-  if ((rc = emit<kPofa>(ctx, p, o, false, s))) return rc;
-  if (flags & FHV_EXACT_ORDER) {
-    {
-      LaunchScope L_(ctx, kStLeafOrder, s);
-      k_leaf_order<<<grid_for((long long)n_local, 128, 32), 128, 0, s>>>(offsets_local, counts_local, (long long)n_local,
-                                                                       base, pool->pos, pool->nrm, pool->mat, pool->obj,
-                                                                       pool->prev);
-    }
-    if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
-  }
+  if ((rc = pofa_scatter_async(ctx, p, levels, lo, hi, counts_local, offsets_local, base, pool, flags, s))) return rc;
   if ((rc = sync_control(ctx, s))) return rc;
   // cursors <= counts elementwise (checked per insert) and equal totals
   // imply cursors == counts (fhv/storage.py:614-619)
@@ -1585,10 +1643,36 @@ extern "C" int fhv_pofa_count(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_ca
 extern "C" int fhv_pofa_build(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
                               uint32_t* counts, uint32_t* offsets, uint8_t* pyramid, fhv_pool_t* pool, int32_t flags,
                               int64_t* total, void* stream) {
-  int rc = fhv_pofa_count(ctx, tris, cfg, levels, counts, offsets, pyramid, total, stream);
+  if (!ctx || !counts || !offsets || !pyramid || levels < 1 || levels > 10) return FHV_BAD_ARGS;
+  int rc = validate(tris, cfg);
   if (rc) return rc;
-  if (!pool || pool->capacity < ctx->pass1_total) return FHV_NEED_POOL;
-  return fhv_pofa_shard_scatter(ctx, tris, cfg, levels, nullptr, counts, offsets, 0, pool, flags, stream);
+  if (pool && (pool->capacity < 0 || (pool->capacity > 0 && (!pool->pos || !pool->nrm || !pool->mat || !pool->obj ||
+                                                              !pool->prev))))
+    return FHV_BAD_ARGS;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned long long n_leaves = 1ull << (3 * levels);
+  CaptureParams p;
+  // pass 1, directory and (into the caller's pool, sized by its guess) pass 2
+  // are enqueued back to back; the only wait is the final sync -- unless the
+  // speculative item plan turns out too small, then once more with an exact plan
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if ((rc = pofa_count_async(ctx, tris, cfg, levels, nullptr, counts, s, p, attempt == 0))) return rc;
+    if ((rc = fhv_pofa_shard_directory_nocheck(ctx, levels, counts, offsets, pyramid, s))) return rc;
+    if (pool && pool->capacity > 0 &&
+        (rc = pofa_scatter_async(ctx, p, levels, 0, n_leaves, counts, offsets, 0, pool, flags, s)))
+      return rc;
+    rc = sync_control(ctx, s);
+    if (rc != FHV_RETRY_ITEMS) break;
+  }
+  if (rc != FHV_OK && rc != FHV_NEED_POOL) return rc;
+  int rc2 = pofa_count_done(ctx, tris, levels, p);
+  if (rc2) return rc2;
+  if ((long long)ctx->ctl_host->scan_total != ctx->pass1_total) return FHV_PASS_MISMATCH;
+  if (total) *total = ctx->pass1_total;
+  if (!pool || pool->capacity < ctx->pass1_total) return FHV_NEED_POOL;  // finish with fhv_pofa_scatter
+  if (rc != FHV_OK) return rc;
+  if ((long long)ctx->ctl_host->alloc != ctx->pass1_total) return FHV_PASS_MISMATCH;
+  return FHV_OK;
 }
 
 extern "C" int fhv_pofa_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
@@ -1633,7 +1717,8 @@ extern "C" int fhv_deferred(fhv_ctx* ctx, const fhv_tris_t* tris, const double* 
   auto* win = (uint32_t*)scratch(ctx, kSplatWin, (size_t)P * 4);
   if (!p.persp || !key || !win) return FHV_NOMEM;
   int rc;
-  if ((rc = plan(ctx, p, s))) return rc;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+  if ((rc = plan(ctx, p, s, attempt == 0))) return rc;
   if ((rc = count(ctx, p, false, 0, nullptr, s))) return rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(key, 0xff, (size_t)P * 8, s)))) return rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(win, 0xff, (size_t)P * 4, s)))) return rc;
@@ -1655,6 +1740,8 @@ extern "C" int fhv_deferred(fhv_ctx* ctx, const fhv_tris_t* tris, const double* 
   }
   if ((rc = deferred_resolve(ctx, P, shading, eye, key, win, gb, background, out_rgba, out_depth, s))) return rc;
   rc = sync_control(ctx, s);
+  if (rc != FHV_RETRY_ITEMS) break;
+  }
   if (emitted) *emitted = (int64_t)ctx->ctl_host->scan_total;
   return rc;
 }
@@ -1686,7 +1773,8 @@ extern "C" int fhv_rebuild_pofa(fhv_ctx* ctx, int32_t levels, const fhv_pool_t* 
     }
     {
       LaunchScope L_(ctx, kStLeafOrder, s);
-      k_leaf_order<<<grid_for(n_leaves, 128, 32), 128, 0, s>>>(offsets, counts, n_leaves, 0ull, dst->pos, dst->nrm,
+      k_leaf_order<<<grid_for(n_leaves, 128, 32), 128, 0, s>>>(offsets, counts, n_leaves, 0ull,
+                                                               (unsigned long long)dst->capacity, dst->pos, dst->nrm,
                                                                dst->mat, dst->obj, dst->prev);
     }
     if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;

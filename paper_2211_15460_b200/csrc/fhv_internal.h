@@ -13,6 +13,10 @@
 
 namespace fhv {
 
+// internal status: a speculatively planned capture's item buffers were too
+// small (never returned to callers: the capture re-plans with a sync)
+constexpr int FHV_RETRY_ITEMS = 100;
+
 // small device-resident control block (one per ctx)
 struct Control {
   int status;                     // sticky FHV_* code raised by kernels
@@ -64,6 +68,10 @@ struct fhv_ctx {
   int64_t pass1_tris = -1;
   uint64_t pass1_lo = 0, pass1_hi = 0;
   int64_t n_binned = -1;  // triangles kept by the last shard binning (-1: no binning)
+  // speculative capture planning (fhv_capture.cu plan()): item buffers sized by
+  // the last exact plan with the same job count; spec = current plan is one
+  int64_t item_cap = 0, last_n_jobs = -1;
+  bool spec = false;
   int last_cuda_error = 0;
 };
 
@@ -93,7 +101,9 @@ int sync_control(fhv_ctx* ctx, cudaStream_t s);  // copies ctl -> ctl_host, sync
 int reset_control(fhv_ctx* ctx, cudaStream_t s);
 
 // exclusive scans (decoupled look-back, single pass); total lands in ctl->scan_total
-int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, int64_t n, cudaStream_t s);
+// n_dev: optional device-side element count (<= n) for a speculatively sized launch
+int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, int64_t n, cudaStream_t s,
+                    const unsigned long long* n_dev = nullptr);
 // POFA directory: offsets = excl-scan(counts), pyramid level L-1 from counts > 0, then upper levels
 int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
                             int levels, cudaStream_t s);

@@ -91,12 +91,21 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, unsigned til
 template <int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restrict__ in,
                                                        unsigned long long* __restrict__ out, int64_t n,
-                                                       uint64_t* status, Control* ctl, unsigned n_tiles) {
+                                                       uint64_t* status, Control* ctl, unsigned n_tiles,
+                                                       const unsigned long long* n_dev) {
   __shared__ unsigned tile_s;
   __shared__ uint64_t prefix_s, total_s;
   if (threadIdx.x == 0) tile_s = atomicAdd(&ctl->tile_counter, 1u);
   __syncthreads();
   const unsigned tile = tile_s;
+  if (n_dev) {  // speculatively sized launch: tiles past the device count retire at once
+    if ((int64_t)*n_dev < n) n = (int64_t)*n_dev;
+    n_tiles = (unsigned)((n + (int64_t)BLOCK * ITEMS - 1) / ((int64_t)BLOCK * ITEMS));
+    if (tile >= n_tiles) {
+      if (tile == 0 && threadIdx.x == 0) ctl->scan_total = 0;
+      return;
+    }
+  }
   const int64_t base = (int64_t)tile * BLOCK * ITEMS + (int64_t)threadIdx.x * ITEMS;
   uint32_t v[ITEMS];
   uint64_t sum = 0;
@@ -379,7 +388,8 @@ inline int grid_for(int64_t n, int block) {
 
 }  // namespace
 
-int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, int64_t n, cudaStream_t s) {
+int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, int64_t n, cudaStream_t s,
+                    const unsigned long long* n_dev) {
   constexpr int B = 256, I = 8;
   const int64_t per = (int64_t)B * I;
   const unsigned tiles = (unsigned)((n + per - 1) / per);
@@ -394,7 +404,7 @@ int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, i
   if (rc) return rc;
   {
     LaunchScope L_(ctx, kStScan, s);
-    k_scan_u32_u64<B, I><<<tiles, B, 0, s>>>(in, out, n, st, ctx->ctl, tiles);
+    k_scan_u32_u64<B, I><<<tiles, B, 0, s>>>(in, out, n, st, ctx->ctl, tiles, n_dev);
   }
   return check_cuda(ctx, cudaGetLastError());
 }
