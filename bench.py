@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
-    ap.add_argument("--config", default="C3", choices=("C3",))
+    ap.add_argument("--config", default="C3", choices=("C3", "C2", "C4", "C5"),
+                    help="C3 = the headline workload; C2 / C4 / C5 = the other BASELINE configs (1 GPU)")
     ap.add_argument("--exact-order", action="store_true", help="bit-identical in-leaf order (extra fix-up pass)")
     ap.add_argument("--packed", action="store_true", help="packed 64-bit splat z-test")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -192,10 +193,216 @@ def reference_arm(args):
 # GPU arm
 
 
+# ---------------------------------------------------------------------------
+# the other BASELINE configs, one GPU
+
+
+def _timed(fn, steps, stream):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    out = None
+    for _ in range(steps):
+        out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, out
+
+
+def _stage_profile(fn, steps, dev):
+    from paper_2211_15460_b200 import _lib
+    _lib.prof_enable(dev, True)
+    _lib.prof_collect(dev)
+    for _ in range(steps):
+        fn()
+    import torch
+    torch.cuda.synchronize()
+    prof = _lib.prof_collect(dev)
+    _lib.prof_enable(dev, False)
+    return {k: v[0] / steps for k, v in prof.items()}, prof
+
+
+def extra_config(args):
+    """C2: spheres100k POFL L8 capture + 1080p ray-cast view; C4: layers80
+    depth-complex 1080^2 PPFL vs POFA; C5: 64 4K ray-cast views of C3's POFA."""
+    import numpy as np
+    import torch
+    import paper_2211_15460_b200 as fhv
+    from paper_2211_15460_b200 import _lib, sample_scenes
+    from paper_2211_15460_b200.device import DeviceShading, device_scene
+    from paper_2211_15460_b200.lights import ImageBuffer, headlight
+    from paper_2211_15460_b200.raster import CaptureStrategy, RasterConfig
+    from paper_2211_15460_b200.scene import capture_camera, viewpoint_camera
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    peak, peak_kind = peaks()
+    ns = CaptureStrategy.normal_space()
+    nt = host_threads()
+    line = {"metric": METRIC, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, no dataset)", "scaling": "strong", "higher_is_better": True}
+
+    def ray_bytes(st, P):  # DESIGN.md section 4: 16 tested + 8 visited + 20 hits + 32 P
+        return 16 * st.tested_fragments + 8 * st.visited_leaves + 20 * st.hits + 32 * P
+
+    def img_buf(w, h):
+        return ImageBuffer(w, h, torch.empty((h, w, 4), dtype=torch.float64, device=dev),
+                           torch.empty((h, w), dtype=torch.float64, device=dev))
+
+    if args.config == "C2":
+        scene = sample_scenes.spheres100k()
+        cam = capture_camera(scene, "+z", 1080)
+        cfg = RasterConfig((1920, 1080), RasterConfig.from_camera(cam).projection, extent=1.0)
+        view = viewpoint_camera("+x", (1920, 1080), "perspective")
+        lights = [headlight(view)]
+        ds = device_scene(scene, dev)
+        sh = DeviceShading(scene.materials, lights, dev)
+        buf = img_buf(1920, 1080)
+        vol0 = fhv.build_pofl(scene, ns, cfg, 8, device=dev)
+        rcfg = fhv.default_raycast_config(vol0)
+
+        def step():
+            vol = fhv.build_pofl(scene, ns, cfg, 8, device=dev)
+            buf.pixels.zero_()
+            img, st = fhv.render_raycast(vol, view, lights, rcfg, out=buf, sync=False, shading=sh)
+            return vol, st
+        for _ in range(args.warmup):
+            step()
+        with ClockSampler(0) as clk:
+            ms, (vol, st) = _timed(step, args.steps, stream)
+        stats = fhv.RaycastStats(*st.counters.cpu().tolist())
+        n = vol.pool.next_free
+        stage, prof = _stage_profile(step, args.steps, dev)
+        t_ray = stage.get("raycast", 0.0)
+        P = 1920 * 1080
+        rb = ray_bytes(stats, P)
+        line.update({"value": n / (ms / 1e3), "unit": "frag/s", "ms_per_step": ms,
+                     "config": {"workload": "C2 spheres100k: 102,400 tris, NormalSpace pitch 1/1080 -> POFL L=8 "
+                                            "(linked lists), + 1920x1080 perspective ray-cast (transparency, "
+                                            "cutoff 1.0)", "fragments": n, "parallelism": "single"},
+                     "novel_view_fps": 1e3 / t_ray if t_ray else None, "raycast_stats": stats.as_dict(),
+                     "stage_ms": {k: round(v, 4) for k, v in sorted(stage.items(), key=lambda kv: -kv[1])},
+                     "roofline": {"bound": "hbm", "kernel": "raycast", "achieved": round(rb / (t_ray / 1e3) / 1e9, 1),
+                                  "peak": peak, "unit": "GB/s", "frac": round(rb / (t_ray / 1e3) / 1e9 / peak, 4),
+                                  "traffic": None, "algorithmic_bytes": rb, "peak_kind": peak_kind,
+                                  "note": "latency/divergence bound (f64 slab DFS), see profiles/"},
+                     "clocks": clk.summary()})
+        if not args.no_cpu_baseline:
+            from oracle import oracle as orc
+            with orc.threads(nt):
+                t0 = time.perf_counter()
+                rv = orc.build_pofl(scene, ns, cfg, 8)
+                t1 = time.perf_counter()
+            band = (480, 600)  # 120 of 1080 rows, scaled x9
+            orc.raycast(rv, view, lights, rcfg.splat_radius_world, materials=scene.materials, rows=band)
+            t2 = time.perf_counter()
+            tr = (t2 - t1) * 1080 / (band[1] - band[0])
+            line["cpu_baseline"] = {"value": rv["next_free"] / (t1 - t0 + tr), "unit": "frag/s", "cores": nt,
+                                    "kind": "port", "sample": f"POFL capture ({nt} threads) {t1 - t0:.2f} s + "
+                                    f"ray-cast rows {band} (1 thread) scaled to 1080 rows = {tr:.2f} s",
+                                    "novel_view_fps": 1.0 / tr}
+    elif args.config == "C4":
+        scene = sample_scenes.layers80()
+        cfg = RasterConfig.from_camera(capture_camera(scene, "+z", 1080))
+        one = CaptureStrategy.one_view()
+        device_scene(scene, dev)
+        n = fhv.pofa_build(scene, one, cfg, 8, device=dev).pool.next_free
+
+        def step_pofa():
+            return fhv.pofa_build(scene, one, cfg, 8, device=dev)
+
+        def step_ppfl():
+            return fhv.build_ppfl(scene, cfg, one, capacity=n, device=dev)
+        for _ in range(args.warmup):
+            step_pofa()
+            step_ppfl()
+        with ClockSampler(0) as clk:
+            ms_a, _ = _timed(step_pofa, args.steps, stream)
+            ms_p, _ = _timed(step_ppfl, args.steps, stream)
+        st_a, _ = _stage_profile(step_pofa, args.steps, dev)
+        st_p, _ = _stage_profile(step_ppfl, args.steps, dev)
+        mem_a = fhv.memory_report("POFA", levels=8, exact_count=n, record_size=36)["total_bytes"]
+        mem_p = fhv.memory_report("PPFL", resolution=(1080, 1080), capacity=n, record_size=36)["total_bytes"]
+        dom = max(st_a, key=st_a.get)
+        T = scene.n_triangles
+        algo = {"emit_pofa": 176 * T + 36 * n, "count_leaves": 72 * T + 4 * 8 ** 8,
+                "scan_leaves": 8 * 8 ** 8 + 8 ** 7}.get(dom)
+        line.update({"value": n / (ms_a / 1e3), "unit": "frag/s", "ms_per_step": ms_a,
+                     "config": {"workload": "C4 layers80: 80 translucent quads, 1080^2 OneView capture, POFA L=8 "
+                                            "(value) vs PPFL with explicit capacity", "fragments": n,
+                                "parallelism": "single"},
+                     "ppfl": {"value": n / (ms_p / 1e3), "unit": "frag/s", "ms_per_step": ms_p, "bytes": mem_p,
+                              "stage_ms": {k: round(v, 4) for k, v in st_p.items()}},
+                     "pofa": {"bytes": mem_a, "stage_ms": {k: round(v, 4) for k, v in st_a.items()}},
+                     "clocks": clk.summary()})
+        if algo:
+            t = st_a[dom] / 1e3
+            line["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": round(algo / t / 1e9, 1), "peak": peak,
+                                "unit": "GB/s", "frac": round(algo / t / 1e9 / peak, 4), "traffic": None,
+                                "algorithmic_bytes": algo, "peak_kind": peak_kind}
+    else:  # C5
+        scene = sample_scenes.scatter1m()
+        cam = capture_camera(scene, "+z", 1080)
+        cfg = RasterConfig((1920, 1080), RasterConfig.from_camera(cam).projection, extent=1.0)
+        vol = fhv.pofa_build(scene, ns, cfg, 8, device=dev)
+        rcfg = fhv.default_raycast_config(vol)
+        views = sample_scenes.c5_views(64)
+        W, H = views[0].resolution
+        shs = [DeviceShading(scene.materials, [headlight(v)], dev) for v in views]
+        buf = img_buf(W, H)
+
+        def step():
+            sts = []
+            for v, sh in zip(views, shs):
+                buf.pixels.zero_()
+                _, st = fhv.render_raycast(vol, v, [headlight(v)], rcfg, out=buf, sync=False, shading=sh)
+                sts.append(st.counters)
+            return sts
+        for _ in range(args.warmup):
+            step()
+        with ClockSampler(0) as clk:
+            ms, sts = _timed(step, args.steps, stream)
+        tot = torch.stack(sts).sum(0).cpu().tolist()
+        stats = fhv.RaycastStats(*tot)
+        stage, _ = _stage_profile(step, 1, dev)
+        P = W * H * len(views)
+        rb = ray_bytes(stats, P)  # per step (64 views)
+        t_ray = stage.get("raycast", ms)
+        line.update({"value": len(views) / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms,
+                     "rays_per_s": P / (ms / 1e3),
+                     "config": {"workload": "C5: 64 x 3840x2160 perspective ray-cast views (Fibonacci sphere, "
+                                            "distance 1.5, fov 45) of C3's POFA (scatter1M, L=8)",
+                                "fragments": vol.pool.next_free, "views": len(views), "parallelism": "single"},
+                     "raycast_stats": stats.as_dict(),
+                     "stage_ms": {k: round(v, 4) for k, v in stage.items()},
+                     "roofline": {"bound": "hbm", "kernel": "raycast", "achieved": round(rb / (t_ray / 1e3) / 1e9, 1),
+                                  "peak": peak, "unit": "GB/s", "frac": round(rb / (t_ray / 1e3) / 1e9 / peak, 4),
+                                  "traffic": None, "algorithmic_bytes": rb, "peak_kind": peak_kind,
+                                  "note": "latency/divergence bound (f64 slab DFS), see profiles/"},
+                     "clocks": clk.summary()})
+        if not args.no_cpu_baseline:
+            from oracle import oracle as orc
+            ref = orc.pofa_build(scene, ns, cfg, 8)
+            band = (1040, 1120)  # 80 of 2160 rows of view 0, scaled x27 x64
+            t0 = time.perf_counter()
+            orc.raycast(ref, views[0], [headlight(views[0])], rcfg.splat_radius_world, materials=scene.materials,
+                        rows=band)
+            dt = (time.perf_counter() - t0) * H / (band[1] - band[0])
+            line["cpu_baseline"] = {"value": 1.0 / dt, "unit": "frames/s", "cores": 1, "kind": "port",
+                                    "sample": f"rows {band} of one 4K view (1 thread), scaled to a full view: "
+                                              f"{dt:.2f} s per view"}
+    line["gpu_launches_total"] = _lib.launches(dev)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.config != "C3":
+        return extra_config(args)
     import numpy as np
     import torch
     import torch.distributed as dist

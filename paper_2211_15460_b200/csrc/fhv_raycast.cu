@@ -261,7 +261,11 @@ __device__ double transmit(const RayParams& x, const double p[3], int li, long l
   return tau;
 }
 
-// _shade_hit (fhv/_ckern.pyx:438-523): plain f64 Blinn-Phong
+// _shade_hit (fhv/_ckern.pyx:438-523): plain f64 Blinn-Phong.  kMode is the
+// ray-cast mode as a template parameter: only mode 2 (shadows) instantiates
+// the second (shadow) traversal and its stack, which keeps the stack frame of
+// the primary-ray kernels of modes 0 / 1 small.
+template <int kMode>
 __device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats& st, double out[3]) {
   const double p[3] = {(double)x.v.pos[3 * i], (double)x.v.pos[3 * i + 1], (double)x.v.pos[3 * i + 2]};
   const double n[3] = {(double)x.v.nrm[3 * i], (double)x.v.nrm[3 * i + 1], (double)x.v.nrm[3 * i + 2]};
@@ -295,7 +299,7 @@ __device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats
     double ndh = __dadd_rn(__dadd_rn(__dmul_rn(n[0], h[0]), __dmul_rn(n[1], h[1])), __dmul_rn(n[2], h[2]));
     if (ndh < 0.0) ndh = 0.0;
     double tau = 1.0;
-    if (x.mode == 2) tau = transmit(x, p, li, (long long)x.v.obj[i], leaf, st);
+    if (kMode == 2) tau = transmit(x, p, li, (long long)x.v.obj[i], leaf, st);
     const double sp = pow(ndh, shin);
     const double* amb = x.s.light_ambient + 3 * li;
     const double* col = x.s.light_color + 3 * li;
@@ -342,6 +346,7 @@ __device__ __forceinline__ void camera_ray(const RayParams& x, long long k, doub
   }
 }
 
+template <int kMode>
 __global__ void __launch_bounds__(128) k_raycast(RayParams x) {
   Stats st = {0, 0, 0, 0};
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -366,8 +371,8 @@ __global__ void __launch_bounds__(128) k_raycast(RayParams x) {
         st.hits++;
         if (first_obj < 0) first_obj = (long long)x.v.obj[i];
         double col[3];
-        if (x.mode == 0) {
-          shade_hit(x, i, code, st, col);
+        if (kMode == 0) {
+          shade_hit<kMode>(x, i, code, st, col);
           c0 = col[0];
           c1 = col[1];
           c2 = col[2];
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(128) k_raycast(RayParams x) {
           return false;
         }
         const double a = x.s.alpha[x.v.mat[i]];
-        shade_hit(x, i, code, st, col);
+        shade_hit<kMode>(x, i, code, st, col);
         const double tc = __dmul_rn(__dsub_rn(1.0, acc), a);
         c0 = __dadd_rn(c0, __dmul_rn(tc, col[0]));
         c1 = __dadd_rn(c1, __dmul_rn(tc, col[1]));
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(128) k_raycast(RayParams x) {
       return true;
     });
     double4 px;
-    if (x.mode == 0) {
+    if (kMode == 0) {
       px = any_hit ? make_double4(c0, c1, c2, 1.0) : make_double4(x.bg[0], x.bg[1], x.bg[2], x.bg[3]);
     } else {
       const double ra = __dsub_rn(1.0, acc);
@@ -431,7 +436,13 @@ int launch(fhv_ctx* ctx, RayParams& x, void* stream) {
   if (x.end <= x.start) return FHV_OK;
   {
     LaunchScope L_(ctx, kStRaycast, (cudaStream_t)stream);
-    k_raycast<<<grid_for(x.end - x.start, 128), 128, 0, (cudaStream_t)stream>>>(x);
+    const int g = grid_for(x.end - x.start, 128);
+    if (x.mode == 0)
+      k_raycast<0><<<g, 128, 0, (cudaStream_t)stream>>>(x);
+    else if (x.mode == 1)
+      k_raycast<1><<<g, 128, 0, (cudaStream_t)stream>>>(x);
+    else
+      k_raycast<2><<<g, 128, 0, (cudaStream_t)stream>>>(x);
   }
   return check_cuda(ctx, cudaGetLastError());
 }

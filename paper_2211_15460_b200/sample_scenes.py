@@ -229,3 +229,22 @@ def layers80(n: int = 80) -> Scene:
         mats.append(Material(diffuse=(0.2 + 0.6 * (k % 3) / 2, 0.5, 0.8 - 0.6 * (k % 4) / 3), alpha=0.05))
         tris += make_quad((a, a, z), (b, a, z), (b, b, z), (a, b, z), material_id=k, object_id=k)
     return Scene.from_triangles(tris, mats)
+
+
+def c5_views(n: int = 64, resolution=(3840, 2160), distance: float = 1.5, fov_deg: float = 45.0, seed: int = 2):
+    """BASELINE config C5's novel viewpoints: n cameras on
+    a Fibonacci sphere (random rotation from default_rng(seed)) at `distance`
+    from the cube centre, looking at it, fov 45, 4K."""
+    from .scene import look_at_camera
+    rng = np.random.default_rng(seed)
+    phi0 = rng.uniform(0.0, 2.0 * np.pi)
+    golden = np.pi * (3.0 - np.sqrt(5.0))
+    views = []
+    for i in range(n):
+        z = 1.0 - 2.0 * (i + 0.5) / n
+        r = np.sqrt(max(0.0, 1.0 - z * z))
+        a = phi0 + golden * i
+        d = np.array([r * np.cos(a), r * np.sin(a), z])
+        up = (0.0, 0.0, 1.0) if abs(z) < 0.9 else (0.0, 1.0, 0.0)
+        views.append(look_at_camera(0.5 + distance * d, up=up, resolution=resolution, fov_deg=fov_deg))
+    return views
