@@ -222,6 +222,11 @@ int fhv_rebuild_pofa(fhv_ctx *ctx, int32_t levels, const fhv_pool_t *src, int64_
 int fhv_pack_records(fhv_ctx *ctx, const fhv_pool_t *pool, int64_t n, void *out, void *stream);
 int fhv_unpack_records(fhv_ctx *ctx, const void *in, int64_t n, fhv_pool_t *pool, void *stream);
 
+/* Self-test of the library's shared-divisor IEEE division against
+   __ddiv_rn (device arrays of n doubles; fast / ref written).  Async. */
+int fhv_selftest_div(fhv_ctx *ctx, int64_t n, const double *x, const double *d, double *fast, double *ref,
+                     void *stream);
+
 /* deferred_baseline (fhv/render.py:327-382) -- the paper's DS comparison
    renderer: every triangle rasterised through the camera projection `proj`
    (4x4 row-major world->clip, RasterConfig.from_camera) at width x height,

@@ -2,6 +2,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "fhv_common.cuh"
 #include "fhv_internal.h"
 
 namespace fhv {
@@ -150,3 +151,24 @@ extern "C" void fhv_ctx_destroy(fhv_ctx* ctx) {
 }
 
 extern "C" int64_t fhv_ctx_launches(const fhv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// self-test of the shared-divisor division (fhv_common.cuh div_rn) against
+// __ddiv_rn: fast[i] = div_rn(x[i], recip_of(d[i])), ref[i] = __ddiv_rn(x[i], d[i])
+__global__ void k_selftest_div(long long n, const double* __restrict__ x, const double* __restrict__ d,
+                               double* __restrict__ fast, double* __restrict__ ref) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    fast[i] = fhv::div_rn(x[i], fhv::recip_of(d[i]));
+    ref[i] = __ddiv_rn(x[i], d[i]);
+  }
+}
+
+extern "C" int fhv_selftest_div(fhv_ctx* ctx, int64_t n, const double* x, const double* d, double* fast, double* ref,
+                                void* stream) {
+  if (!ctx || n < 0 || (n > 0 && (!x || !d || !fast || !ref))) return FHV_BAD_ARGS;
+  if (n == 0) return FHV_OK;
+  long long g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  k_selftest_div<<<(int)g, 256, 0, (cudaStream_t)stream>>>(n, x, d, fast, ref);
+  ++ctx->launches;
+  return fhv::check_cuda(ctx, cudaGetLastError());
+}

@@ -168,13 +168,14 @@ __device__ __forceinline__ void setup_screen(const CaptureParams& p, long long j
     const double c0 = __dadd_rn(fwd3(X, Y, Z, M[0], M[1], M[2]), M[3]);
     const double c1 = __dadd_rn(fwd3(X, Y, Z, M[4], M[5], M[6]), M[7]);
     const double c3 = __dadd_rn(fwd3(X, Y, Z, M[12], M[13], M[14]), M[15]);
+    const Recip r3 = recip_of(c3);
     if (p.strategy == kScreen) {
       const double c2 = __dadd_rn(fwd3(X, Y, Z, M[8], M[9], M[10]), M[11]);
-      nz[i] = __ddiv_rn(c2, c3);
+      nz[i] = div_rn(c2, r3);
       cw[i] = c3;
       behind = behind || (!p.ortho && c3 <= 1e-9);
     }
-    const double nx = __ddiv_rn(c0, c3), ny = __ddiv_rn(c1, c3);
+    const double nx = div_rn(c0, r3), ny = div_rn(c1, r3);
     xr[i] = __dmul_rn(__dmul_rn(__dadd_rn(nx, 1.0), 0.5), (double)p.width);
     yr[i] = __dmul_rn(__dmul_rn(__dsub_rn(1.0, ny), 0.5), (double)p.height);
   }
@@ -207,7 +208,8 @@ __device__ __forceinline__ void setup_tangent(const CaptureParams& p, long long 
     raise_status(status, FHV_BASIS);
     return;
   }
-  const double n0 = __ddiv_rn(F[0], norm), n1 = __ddiv_rn(F[1], norm), n2 = __ddiv_rn(F[2], norm);
+  const Recip rn = recip_of(norm);
+  const double n0 = div_rn(F[0], rn), n1 = div_rn(F[1], rn), n2 = div_rn(F[2], rn);
   const bool hx = fabs(n0) <= 0.6;
   const double h0 = hx ? 1.0 : 0.0, h1 = hx ? 0.0 : 1.0, h2 = 0.0;
   const double hn = fwd3(h0, h1, h2, n0, n1, n2);
@@ -215,9 +217,10 @@ __device__ __forceinline__ void setup_tangent(const CaptureParams& p, long long 
   double t1 = __dsub_rn(h1, __dmul_rn(hn, n1));
   double t2 = __dsub_rn(h2, __dmul_rn(hn, n2));
   const double tn = __dsqrt_rn(fwd3(t0, t1, t2, t0, t1, t2));
-  t0 = __ddiv_rn(t0, tn);
-  t1 = __ddiv_rn(t1, tn);
-  t2 = __ddiv_rn(t2, tn);
+  const Recip rt = recip_of(tn);
+  t0 = div_rn(t0, rt);
+  t1 = div_rn(t1, rt);
+  t2 = div_rn(t2, rt);
   const double b0 = __dsub_rn(__dmul_rn(n1, t2), __dmul_rn(n2, t1));
   const double b1 = __dsub_rn(__dmul_rn(n2, t0), __dmul_rn(n0, t2));
   const double b2 = __dsub_rn(__dmul_rn(n0, t1), __dmul_rn(n1, t0));
@@ -235,8 +238,9 @@ __device__ __forceinline__ void setup_tangent(const CaptureParams& p, long long 
     bmin = bc[i] < bmin ? bc[i] : bmin;
     bmax = bc[i] > bmax ? bc[i] : bmax;
   }
-  double nxd = ceil(__ddiv_rn(__dsub_rn(tmax, tmin), p.pitch));
-  double nyd = ceil(__ddiv_rn(__dsub_rn(bmax, bmin), p.pitch));
+  const Recip rp = recip_of(p.pitch);
+  double nxd = ceil(div_rn(__dsub_rn(tmax, tmin), rp));
+  double nyd = ceil(div_rn(__dsub_rn(bmax, bmin), rp));
   if (!(nxd >= 1.0)) nxd = 1.0;
   if (!(nyd >= 1.0)) nyd = 1.0;
   if (nxd > 2147483647.0 || nyd > 2147483647.0) {
@@ -246,8 +250,8 @@ __device__ __forceinline__ void setup_tangent(const CaptureParams& p, long long 
   double xr[3], yr[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    xr[i] = __ddiv_rn(__dsub_rn(tc[i], tmin), p.pitch);
-    yr[i] = __ddiv_rn(__dsub_rn(bmax, bc[i]), p.pitch);
+    xr[i] = div_rn(__dsub_rn(tc[i], tmin), rp);
+    yr[i] = div_rn(__dsub_rn(bmax, bc[i]), rp);
   }
   finish_setup(xr, yr, (long long)nxd, (long long)nyd, js);
 }
@@ -339,7 +343,8 @@ struct CoverS {  // per-item coverage state, staged in shared memory
   double area2;
   int32_t x0, y0, bw;
   uint32_t tri, swapped, tl;  // tl bit e: edge e is a top-left edge
-  uint32_t p0, pad;
+  uint32_t p0;
+  float inv_bw;  // 1.0f / bw: pixel index -> bbox row without an integer division
 };
 
 __device__ __forceinline__ void make_cover(const JobSetup& js, uint32_t p0, CoverS& c) {
@@ -357,6 +362,7 @@ __device__ __forceinline__ void make_cover(const JobSetup& js, uint32_t p0, Cove
   c.tri = js.tri;
   c.swapped = js.swapped;
   c.p0 = p0;
+  c.inv_bw = 1.0f / (float)(js.bw > 0 ? js.bw : 1);
 }
 
 // pixel-centre coverage test with the top-left rule; edge functions in f64
@@ -480,9 +486,10 @@ __device__ __forceinline__ void ds_fragment(const CaptureParams& p, const EmitOu
   if (!p.ortho) {
     const double lw0 = __ddiv_rn(l0, jp.w[0]), lw1 = __ddiv_rn(l1, jp.w[1]), lw2 = __ddiv_rn(l2, jp.w[2]);
     const double sum = __dadd_rn(__dadd_rn(lw0, lw1), lw2);
-    l0 = __ddiv_rn(lw0, sum);
-    l1 = __ddiv_rn(lw1, sum);
-    l2 = __ddiv_rn(lw2, sum);
+    const Recip rs = recip_of(sum);
+    l0 = div_rn(lw0, rs);
+    l1 = div_rn(lw1, rs);
+    l2 = div_rn(lw2, rs);
   }
   TriData td;
   load_tri(p, c.tri, c.swapped, td, true);
@@ -901,8 +908,16 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
         }
         const CoverS& c = cs[k];
         const uint32_t q = c.p0 + 32u * word + nth_set_bit(wv, rem);
-        const uint32_t r = q / (uint32_t)c.bw;
-        px = c.x0 + (int)(q - r * (uint32_t)c.bw);
+        const uint32_t bw = (uint32_t)c.bw;
+        uint32_t r;
+        if (q < (1u << 22)) {  // |float estimate - q / bw| <= 2^-23 q < 1/2 here; fix it up exactly
+          r = (uint32_t)__fmul_rn((float)q, c.inv_bw);
+          const int rem = (int)(q - r * bw);
+          r = rem < 0 ? r - 1 : (rem >= (int)bw ? r + 1 : r);
+        } else {
+          r = q / bw;
+        }
+        px = c.x0 + (int)(q - r * bw);
         py = c.y0 + (int)r;
       }
       raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, valid, k, px, py, local, own_cnt, rank0, ijob, st);
@@ -1038,9 +1053,10 @@ __global__ void k_face_normals(long long n, const double* __restrict__ pos, doub
     const double c1 = __dsub_rn(__dmul_rn(e1[2], e2[0]), __dmul_rn(e1[0], e2[2]));
     const double c2 = __dsub_rn(__dmul_rn(e1[0], e2[1]), __dmul_rn(e1[1], e2[0]));
     const double len = __dsqrt_rn(fwd3(c0, c1, c2, c0, c1, c2));
-    fn[3 * t] = len > 0.0 ? __ddiv_rn(c0, len) : 0.0;
-    fn[3 * t + 1] = len > 0.0 ? __ddiv_rn(c1, len) : 0.0;
-    fn[3 * t + 2] = len > 0.0 ? __ddiv_rn(c2, len) : 0.0;
+    const Recip rl = recip_of(len);
+    fn[3 * t] = len > 0.0 ? div_rn(c0, rl) : 0.0;
+    fn[3 * t + 1] = len > 0.0 ? div_rn(c1, rl) : 0.0;
+    fn[3 * t + 2] = len > 0.0 ? div_rn(c2, rl) : 0.0;
   }
 }
 

@@ -188,7 +188,7 @@ __device__ void traverse(const RayParams& x, const double o[3], const double d[3
     }
     const unsigned mask = __ldg(&x.v.pyramid[pyr_level_offset(level) + (long long)code]);
     if (mask == 0) continue;
-    const double half = __ddiv_rn(0.5, (double)(1 << level));
+    const double half = __longlong_as_double((1022LL - level) << 52);  // 0.5 / 2^level, exact
     const double size = __dmul_rn(2.0, half);
     const double lo[3] = {__dmul_rn((double)compact3(code), size), __dmul_rn((double)compact3(code >> 1), size),
                           __dmul_rn((double)compact3(code >> 2), size)};
@@ -243,8 +243,9 @@ __device__ double transmit(const RayParams& x, const double p[3], int li, long l
     for (int k = 0; k < 3; ++k) l[k] = __dsub_rn(x.s.light_vec[3 * li + k], p[k]);
     const double len = __dsqrt_rn(plain3(l[0], l[1], l[2]));
     if (len == 0.0) return 1.0;
+    const Recip rl = recip_of(len);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) l[k] = __ddiv_rn(l[k], len);
+    for (int k = 0; k < 3; ++k) l[k] = div_rn(l[k], rl);
     tmax = len;
   }
   double o[3];
@@ -338,9 +339,10 @@ __device__ __forceinline__ void camera_ray(const RayParams& x, long long k, doub
     for (int c = 0; c < 3; ++c)
       v[c] = __dadd_rn(__dadd_rn(x.ff[c], __dmul_rn(nx, __dmul_rn(ta, x.rr[c]))), __dmul_rn(ny, __dmul_rn(x.t, x.uu[c])));
     const double len = __dsqrt_rn(plain3(v[0], v[1], v[2]));
+    const Recip rl = recip_of(len);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      d[c] = __ddiv_rn(v[c], len);
+      d[c] = div_rn(v[c], rl);
       o[c] = x.eye[c];
     }
   }

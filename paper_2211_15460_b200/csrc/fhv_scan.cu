@@ -197,7 +197,7 @@ using DirSmall = DirTile<4, 4>;   // 8^4 leaves
 using DirBig = DirTile<16, 8>;    // 8^5 leaves
 
 template <bool kScan, int WARPS, int ITERS>
-__global__ void __launch_bounds__(32 * WARPS) k_dir_tiles(const uint4* __restrict__ counts,
+__global__ void __launch_bounds__(32 * WARPS, WARPS <= 16 ? 2 : 1) k_dir_tiles(const uint4* __restrict__ counts,
                                                           uint4* __restrict__ offsets,
                                                           const int4* __restrict__ heads, uint8_t* __restrict__ pyr,
                                                           int levels, uint64_t* status, Control* ctl,
@@ -219,31 +219,57 @@ __global__ void __launch_bounds__(32 * WARPS) k_dir_tiles(const uint4* __restric
   // local node index (counts / offsets / heads) and global node index (pyramid)
   const long long node0 = (long long)tile * (T::kLeaves / 8) + (long long)warp * (32 * ITERS);
   const long long gnode0 = (long long)gtile * (T::kLeaves / 8) + (long long)warp * (32 * ITERS);
-  uint32_t c[ITERS][8];
+  // phase 1, in chunks of kChunk iterations (loads of a chunk in flight
+  // together, registers bounded): leaf masks -> pyramid levels L-1..L-3, lane
+  // sums -> lane-exclusive prefixes within the warp's slice (u32: a directory
+  // holds < 2^32 fragments).  The counts are re-read after the tile look-back
+  // (L2 hits) instead of being held across it -> 2 CTAs per SM.
+  constexpr int kChunk = ITERS < 4 ? ITERS : 4;
+  static_assert(ITERS % kChunk == 0 && kChunk % 2 == 0, "chunking");
   unsigned ballots[ITERS];
+  uint32_t excl[ITERS];
+  uint64_t carry = 0;
 #pragma unroll
-  for (int i = 0; i < ITERS; ++i) {
-    const long long n = node0 + i * 32 + lane;
-    if (kScan) {
-      const uint4 a = __ldg(&counts[2 * n]), b = __ldg(&counts[2 * n + 1]);
-      c[i][0] = a.x; c[i][1] = a.y; c[i][2] = a.z; c[i][3] = a.w;
-      c[i][4] = b.x; c[i][5] = b.y; c[i][6] = b.z; c[i][7] = b.w;
-    } else {
-      const int4 a = __ldcs(&heads[2 * n]), b = __ldcs(&heads[2 * n + 1]);
-      const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  for (int h = 0; h < ITERS; h += kChunk) {
+    uint32_t c[kChunk][8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) c[i][k] = v[k] >= 0 ? 1u : 0u;
+    for (int q = 0; q < kChunk; ++q) {
+      const long long n = node0 + (h + q) * 32 + lane;
+      if (kScan) {
+        const uint4 a = __ldcg(&counts[2 * n]), b = __ldcg(&counts[2 * n + 1]);
+        c[q][0] = a.x; c[q][1] = a.y; c[q][2] = a.z; c[q][3] = a.w;
+        c[q][4] = b.x; c[q][5] = b.y; c[q][6] = b.z; c[q][7] = b.w;
+      } else {
+        const int4 a = __ldcs(&heads[2 * n]), b = __ldcs(&heads[2 * n + 1]);
+        const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c[q][k] = v[k] >= 0 ? 1u : 0u;
+      }
     }
-  }
 #pragma unroll
-  for (int i = 0; i < ITERS; ++i) {
-    unsigned m = 0;
+    for (int q = 0; q < kChunk; ++q) {
+      const int i = h + q;
+      unsigned m = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) m |= (c[i][k] != 0u ? 1u : 0u) << k;
-    lv1[gnode0 + i * 32 + lane] = (uint8_t)m;
-    ballots[i] = __ballot_sync(0xffffffffu, m != 0);
-    // level L-2: lane g < 4 writes node (gnode0 + 32 i) / 8 + g
-    if (lane < 4) lv2[(gnode0 + 32 * i) / 8 + lane] = (uint8_t)((ballots[i] >> (8 * lane)) & 0xffu);
+      for (int k = 0; k < 8; ++k) m |= (c[q][k] != 0u ? 1u : 0u) << k;
+      lv1[gnode0 + i * 32 + lane] = (uint8_t)m;
+      ballots[i] = __ballot_sync(0xffffffffu, m != 0);
+      // level L-2: lane g < 4 writes node (gnode0 + 32 i) / 8 + g
+      if (lane < 4) lv2[(gnode0 + 32 * i) / 8 + lane] = (uint8_t)((ballots[i] >> (8 * lane)) & 0xffu);
+      if (kScan) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sum += c[q][k];
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= (unsigned)o) inc += y;
+        }
+        excl[i] = (uint32_t)carry + inc - sum;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
   }
   // level L-3: iterations (2j, 2j+1) -> one node; bit g = L-2 node g non-empty
 #pragma unroll
@@ -261,22 +287,6 @@ __global__ void __launch_bounds__(32 * WARPS) k_dir_tiles(const uint4* __restric
     }
   }
   if (kScan) {
-    uint64_t excl[ITERS];
-    uint64_t carry = 0;
-#pragma unroll
-    for (int i = 0; i < ITERS; ++i) {
-      uint64_t sum = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) sum += c[i][k];
-      uint64_t inc = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= (unsigned)o) inc += y;
-      }
-      excl[i] = carry + inc - sum;
-      carry += __shfl_sync(0xffffffffu, inc, 31);
-    }
     if (lane == 0) warp_tot[warp] = carry;
     __syncthreads();
     if (warp == 0) {
@@ -295,12 +305,14 @@ __global__ void __launch_bounds__(32 * WARPS) k_dir_tiles(const uint4* __restric
 #pragma unroll
     for (int i = 0; i < ITERS; ++i) {
       const long long n = node0 + i * 32 + lane;
+      const uint4 a = __ldcg(&counts[2 * n]), b = __ldcg(&counts[2 * n + 1]);
+      const uint32_t cc[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
       uint64_t run = wbase + excl[i];
       uint32_t o[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         o[k] = (uint32_t)run;
-        run += c[i][k];
+        run += cc[k];
       }
       __stcs(&offsets[2 * n], make_uint4(o[0], o[1], o[2], o[3]));
       __stcs(&offsets[2 * n + 1], make_uint4(o[4], o[5], o[6], o[7]));

@@ -68,8 +68,15 @@ class DeviceScene:
         return self.fnrm
 
     def struct(self) -> _lib.Tris:
-        return _lib.Tris(self.n_tri, _lib.ptr(self.pos), _lib.ptr(self.vnrm), _lib.ptr(self.fnrm),
-                         _lib.ptr(self.mat), _lib.ptr(self.obj))
+        # the C struct is cached with the pointers it was built from
+        key = (self.n_tri, self.pos.data_ptr(), self.vnrm.data_ptr(), self.fnrm.data_ptr(), self.mat.data_ptr(),
+               self.obj.data_ptr())
+        hit = self.__dict__.get("_struct")
+        if hit is None or hit[0] != key:
+            hit = self.__dict__["_struct"] = (key, _lib.Tris(self.n_tri, _lib.ptr(self.pos), _lib.ptr(self.vnrm),
+                                                             _lib.ptr(self.fnrm), _lib.ptr(self.mat),
+                                                             _lib.ptr(self.obj)))
+        return hit[1]
 
     @property
     def nbytes(self) -> int:
@@ -112,9 +119,13 @@ class DeviceShading:
         self.n_mats = len(md)
 
     def struct(self) -> _lib.Shading:
-        t = self.tensors
-        return _lib.Shading(self.n_lights, _lib.ptr(t[0]), _lib.ptr(t[1]), _lib.ptr(t[2]), _lib.ptr(t[3]),
-                            self.n_mats, _lib.ptr(t[4]), _lib.ptr(t[5]), _lib.ptr(t[6]), _lib.ptr(t[7]))
+        st = self.__dict__.get("_struct")
+        if st is None:  # tables are immutable after construction
+            t = self.tensors
+            st = self.__dict__["_struct"] = _lib.Shading(
+                self.n_lights, _lib.ptr(t[0]), _lib.ptr(t[1]), _lib.ptr(t[2]), _lib.ptr(t[3]), self.n_mats,
+                _lib.ptr(t[4]), _lib.ptr(t[5]), _lib.ptr(t[6]), _lib.ptr(t[7]))
+        return st
 
 
 def host_f64(values) -> np.ndarray:

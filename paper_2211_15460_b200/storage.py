@@ -257,7 +257,16 @@ class OccupancyPyramid:
             raise FhvError("octree needs at least one level")
         self.leaf_levels = leaf_levels
         n = _pyr_offsets(leaf_levels)[-1]
-        self.data = data if data is not None else torch.zeros(n, dtype=torch.uint8, device=default_device(device))
+        if data is None:
+            data = torch.zeros(n, dtype=torch.uint8, device=default_device(device))
+        self.data = data
+
+    @staticmethod
+    def uninitialized(leaf_levels: int, device) -> "OccupancyPyramid":
+        """For a kernel that writes every level (the POFA directory pass)."""
+        _check_levels(leaf_levels)
+        return OccupancyPyramid(leaf_levels, torch.empty(_pyr_offsets(leaf_levels)[-1], dtype=torch.uint8,
+                                                         device=device))
 
     @property
     def levels(self) -> list:
@@ -427,7 +436,7 @@ def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     n_leaf = 8 ** levels
     counts = torch.empty(n_leaf, dtype=torch.uint32, device=dev)
     offsets = torch.empty(n_leaf, dtype=torch.uint32, device=dev)
-    pyr = OccupancyPyramid(levels, device=dev)
+    pyr = OccupancyPyramid.uninitialized(levels, dev)  # the directory pass writes every level
     lib = _lib.load()
     total = ctypes_i64()
     cx = _lib.ctx(dev)

@@ -145,3 +145,47 @@ def test_rebuild_equals_direct_pofa_build():
     a, b = rb.pool.numpy(), pa.pool.numpy()
     for f in a:
         assert np.array_equal(a[f], b[f]), f
+
+
+def _pool_from_positions(pos, dev):
+    n = len(pos)
+    pool = fhv.FragmentPool(n, dev)
+    pool.position.copy_(torch.from_numpy(np.ascontiguousarray(pos, dtype=np.float32)))
+    pool.normal.zero_()
+    pool.material_id.zero_()
+    pool.object_id.copy_(torch.arange(n, dtype=torch.int32, device=dev).view(torch.uint32))
+    pool.next_free = n
+    return pool
+
+
+def test_device_cell_codes_on_adversarial_floats():
+    """cell_code's f32 fast path (range bounds as floats, f32 floor) against the
+    oracle's f64 restatement on floats straddling every leaf boundary and the
+    [-1e-6, 1+1e-6] bounds, through the device repack's leaf histogram."""
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(7)
+    vals = []
+    for L in (8,):
+        b = np.arange(0, 2 ** L + 1, dtype=np.float64) / 2 ** L
+        f = b.astype(np.float32)
+        for k in range(-3, 4):
+            vals.append(f.view(np.int32) + k)
+    edge = np.array([-1e-6, 1.0 + 1e-6, 0.0, 1.0], np.float32).view(np.int32)
+    for k in range(-4, 5):
+        vals.append(edge + k)
+    v = np.concatenate(vals).view(np.float32)
+    v = v[(v.astype(np.float64) >= -1e-6) & (v.astype(np.float64) <= 1.0 + 1e-6)]
+    pos = np.stack([rng.permutation(v), rng.permutation(v), rng.permutation(v)], axis=1).astype(np.float32)
+    L = 8
+    codes = orc.cell_codes(pos, L)
+    vol = fhv.FhvPofl(fhv.storage.PoflDirectory(L, torch.full((8 ** L,), -1, dtype=torch.int32, device=dev)),
+                      fhv.OccupancyPyramid(L, device=dev), _pool_from_positions(pos, dev), 256)
+    rb = fhv.rebuild_pofl_as_pofa(vol)
+    assert np.array_equal(rb.directory.counts.cpu().numpy(), np.bincount(codes, minlength=8 ** L).astype(np.uint32))
+    for bad in (np.float32(np.nextafter(np.float32(-1e-6), np.float32(-1))), np.float32(1.0000011), np.float32("nan"),
+                np.float32("inf")):
+        p = pos[:4].copy()
+        p[2, 1] = bad
+        vol.pool = _pool_from_positions(p, dev)
+        with pytest.raises(fhv.FhvError):
+            fhv.rebuild_pofl_as_pofa(vol)

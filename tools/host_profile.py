@@ -45,6 +45,31 @@ def main(steps=20):
     torch.cuda.synchronize()
     pr.disable()
     pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+    # time inside each C-ABI call (includes the library's own syncs) vs the rest
+    from paper_2211_15460_b200 import _lib
+    lib = _lib.load()
+    acc = {}
+
+    class Timed:
+        def __init__(self, name, fn):
+            self.name, self.fn = name, fn
+
+        def __call__(self, *a):
+            t = time.perf_counter()
+            r = self.fn(*a)
+            acc[self.name] = acc.get(self.name, 0.0) + time.perf_counter() - t
+            return r
+    for name in ("fhv_pofa_build", "fhv_splat"):
+        setattr(lib, name, Timed(name, getattr(lib, name)))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / steps
+    print(f"wall per step {1e3 * wall:.3f} ms; inside C calls per step: " +
+          ", ".join(f"{k} {1e3 * v / steps:.3f} ms" for k, v in acc.items()) +
+          f"; python outside {1e3 * (wall - sum(acc.values()) / steps):.3f} ms")
 
 
 if __name__ == "__main__":
