@@ -63,6 +63,8 @@ enum {
 /* splat flags */
 enum {
   FHV_SPLAT_PACKED = 1,  /* one 64-bit atomicMin on (f32 depth | u32 index); default is the exact f64 two-pass z-test */
+  FHV_SPLAT_NOSYNC = 2,  /* caller proved the footprint bound (fhv/render.py:285-286) holds: return without
+                            waiting for the kernels (no FHV_SPLAT_BIG check) */
 };
 
 typedef struct fhv_ctx fhv_ctx; /* per-device scratch arena (grow-only); one per host thread / stream */

@@ -21,7 +21,7 @@ FHV_OK, FHV_OVERFLOW, FHV_PASS_MISMATCH, FHV_BAD_ARGS, FHV_CUDA_ERROR = 0, 1, 2,
 FHV_RANGE, FHV_BASIS, FHV_NOMEM, FHV_TOO_MANY, FHV_SPLAT_BIG = 5, 6, 7, 8, 9
 FHV_NEED_POOL = 10
 FHV_ALLOC_ATOMIC, FHV_EXACT_ORDER = 1, 2
-FHV_SPLAT_PACKED = 1
+FHV_SPLAT_PACKED, FHV_SPLAT_NOSYNC = 1, 2
 
 
 class Tris(ctypes.Structure):

@@ -50,13 +50,44 @@ def splat_render(pool, camera: Camera, lights, splat_radius_world: float, materi
                        _lib.ptr(id_buffer.object_id), _lib.ptr(id_buffer.valid))
     cam = host_f64(camera.scalars())
     bg = host_f64(background)
+    flags = _lib.FHV_SPLAT_PACKED if packed else 0
+    if getattr(pool, "in_unit_cube", False) and footprint_bounded(camera, float(splat_radius_world)):
+        flags |= _lib.FHV_SPLAT_NOSYNC  # SceneError impossible: no need to wait for the kernels
     lib = _lib.load()
     rc = lib.fhv_splat(_lib.ctx(dev), count, _lib.ptr(pool.position), _lib.ptr(pool.normal),
                        _lib.ptr(pool.material_id), _lib.ptr(pool.object_id), cam.ctypes.data, float(splat_radius_world),
                        bg.ctypes.data, shading.struct(), _lib.ptr(out.pixels), _lib.ptr(out.depth), None,
-                       gb, _lib.FHV_SPLAT_PACKED if packed else 0, _lib.stream_ptr(dev))
+                       gb, flags, _lib.stream_ptr(dev))
     _lib.check(rc, "splat_render")
     return out
+
+
+_UNIT_LO, _UNIT_HI = -1e-6, 1.0 + 1e-6  # cell_code's accepted range (fhv/storage.py:152-155)
+
+
+def footprint_bounded(camera: Camera, radius: float) -> bool:
+    """True when NO point of [-1e-6, 1+1e-6]^3 can get a splat footprint over
+    the reference's 4096-pixel limit (fhv/render.py:285-286) -- then the
+    device-side check (and its sync) is unnecessary.  Orthographic: the
+    half-size is a constant.  Perspective: half = r h / (2 tan zc) decreases
+    with the view depth zc, bounded below over the cube by its nearest corner
+    (points with zc <= 1e-9 are not drawn)."""
+    key = (camera.scalars().tobytes(), radius)
+    hit = camera.__dict__.get("_fp_bound")
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    c = camera.scalars()
+    h = c[14]
+    if c[0] == 0.0:
+        half = radius * h / c[21]
+    else:
+        f, eye = c[10:13], c[1:4]
+        zmin = sum(min(_UNIT_LO * fa, _UNIT_HI * fa) for fa in f) - float(eye @ f)
+        zmin -= 1e-9 * (1.0 + abs(zmin))  # slack for the device's rounding of zc
+        half = float("inf") if zmin <= 1e-9 else radius * h / ((2.0 * c[17]) * zmin) * (1.0 + 1e-9)
+    ok = bool((2.0 * max(half, 0.5) + 2.0) ** 2 <= 4096.0)
+    camera.__dict__["_fp_bound"] = (key, ok)
+    return ok
 
 
 def deferred_baseline(scene, camera: Camera, lights, background=(0.0, 0.0, 0.0, 0.0), *, device=None,

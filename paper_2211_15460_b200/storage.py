@@ -167,6 +167,9 @@ class FragmentPool:
             self.prev_index.fill_(-1)
         self.next_free = 0
         self.overflowed = False
+        # every stored position passed cell_code's [-1e-6, 1+1e-6]^3 check (POFL / POFA
+        # builds): lets splat_render bound the footprint on the host
+        self.in_unit_cube = False
 
     def narrow(self, n: int) -> "FragmentPool":
         """The first ``n`` records as a pool of capacity ``n`` (views, no copy)."""
@@ -178,6 +181,7 @@ class FragmentPool:
         out.material_id, out.object_id, out.prev_index = self.material_id[:n], self.object_id[:n], self.prev_index[:n]
         out.next_free = min(self.next_free, n)
         out.overflowed = False
+        out.in_unit_cube = self.in_unit_cube
         return out
 
     @property
@@ -416,6 +420,7 @@ def build_pofl(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     _lib.check(rc, "build_pofl", allow=(_lib.FHV_OK, _lib.FHV_OVERFLOW))
     pool.next_free = int(nf.value)
     pool.overflowed = pool.next_free > pool.capacity
+    pool.in_unit_cube = True
     return FhvPofl(PoflDirectory(levels, heads), pyr, pool, h, plan.stats(pool.next_free), scene.materials)
 
 
@@ -461,6 +466,7 @@ def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     if pool.capacity != n:
         pool = pool.narrow(n)
     pool.next_free = n
+    pool.in_unit_cube = True
     return FhvPofa(PofaDirectory(levels, offsets, counts), pyr, pool, int(cfg.resolution[1]),
                    plan.stats(pool.next_free), scene.materials)
 
@@ -499,6 +505,7 @@ def rebuild_pofl_as_pofa(fhv: FhvPofl) -> FhvPofa:
                               _lib.ptr(pyr.data), new.struct(), _lib.stream_ptr(dev))
     _lib.check(rc, "rebuild_pofl_as_pofa")
     new.next_free = n
+    new.in_unit_cube = True
     return FhvPofa(PofaDirectory(L, offsets, counts), pyr, new, fhv.capture_resolution, fhv.stats, fhv.materials)
 
 
