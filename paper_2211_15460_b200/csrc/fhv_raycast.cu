@@ -348,8 +348,11 @@ __device__ __forceinline__ void camera_ray(const RayParams& x, long long k, doub
   }
 }
 
+#ifndef FHV_RAY_MINB
+#define FHV_RAY_MINB 1  // resident 128-thread CTAs per SM the ray kernel is register-budgeted for
+#endif
 template <int kMode>
-__global__ void __launch_bounds__(128) k_raycast(RayParams x) {
+__global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
   Stats st = {0, 0, 0, 0};
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   for (long long k = x.start + blockIdx.x * (long long)blockDim.x + threadIdx.x; k < x.end;
