@@ -229,6 +229,12 @@ int fhv_unpack_records(fhv_ctx *ctx, const void *in, int64_t n, fhv_pool_t *pool
 int fhv_selftest_div(fhv_ctx *ctx, int64_t n, const double *x, const double *d, double *fast, double *ref,
                      void *stream);
 
+/* Scene ingest (load_scene, fhv/scene.py:291-378): rows of `in` [n][3]
+   divided by sqrt(row . row) in NumPy's ddot order -- np.linalg.norm and
+   _unit of the reference.  *zero_first = index of the first zero-length row,
+   or -1.  Synchronises. */
+int fhv_unit_rows(fhv_ctx *ctx, int64_t n, const double *in, double *out, int64_t *zero_first, void *stream);
+
 /* deferred_baseline (fhv/render.py:327-382) -- the paper's DS comparison
    renderer: every triangle rasterised through the camera projection `proj`
    (4x4 row-major world->clip, RasterConfig.from_camera) at width x height,

@@ -7,6 +7,7 @@ in hand-written sm_100a kernels behind a C ABI (include/fhv_b200.h).
 """
 from . import sample_scenes
 from .api import capture, reconstruct
+from .ingest import load_material_table, load_scene, save_material_table, save_scene
 from .capture import capture_fragments, capture_pass
 from .lights import (GBuffer, ImageBuffer, Light, composite_over, front_to_back_accumulate, headlight,
                      write_float_dump, write_ppm)
@@ -14,7 +15,8 @@ from .raster import (CaptureStats, CaptureStrategy, FragmentBatch, RasterConfig,
                      perspective_projection, tangent_basis, world_pixel_footprint)
 from .raycast import RaycastConfig, RaycastStats, default_raycast_config, primary_rays, render_raycast
 from .render import deferred_baseline, splat_render
-from .scene import (Aabb, Camera, Material, Scene, SceneError, SceneLoadError, Triangle, Vertex, capture_camera,
+from .scene import (Aabb, Camera, Material, Scene, SceneError, SceneLoadError, SceneTransform, Triangle, Vertex,
+                    capture_camera,
                     make_quad, make_triangle, normalize_scene, viewpoint_camera)
 from .storage import (FhvError, FhvPofa, FhvPofl, FhvPpfl, FragmentPool, FragmentRecord, OccupancyPyramid,
                       PofaBuildError, build_pofl, build_ppfl, cell_of, load_snapshot, memory_report, morton_decode,

@@ -95,6 +95,7 @@ _SIGS = {
     "fhv_pack_records": (ctypes.c_int, [c_vp, _P(Pool), c_i64, c_vp, c_vp]),
     "fhv_unpack_records": (ctypes.c_int, [c_vp, c_vp, c_i64, _P(Pool), c_vp]),
     "fhv_selftest_div": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "fhv_unit_rows": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, _P(c_i64), c_vp]),
     "fhv_deferred": (ctypes.c_int, [c_vp, _P(Tris), c_vp, c_i32, c_i32, c_vp, _P(Shading), c_vp, c_vp, c_vp,
                                     _P(GBuf), _P(c_i64), c_vp]),
     "fhv_face_normals": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp]),

@@ -1060,6 +1060,25 @@ __global__ void k_face_normals(long long n, const double* __restrict__ pos, doub
   }
 }
 
+// unit rows (scene ingest): out = v / sqrt(v . v) with NumPy's ddot order
+// (FWD) -- np.linalg.norm of a 3-vector and _unit (fhv/scene.py:73-77, 327-332);
+// the first zero-length row index lands in *zero_first
+__global__ void k_unit_rows(long long n, const double* __restrict__ in, double* __restrict__ out,
+                            unsigned long long* zero_first) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double a = in[3 * i], b = in[3 * i + 1], c = in[3 * i + 2];
+    const double len = __dsqrt_rn(fwd3(a, b, c, a, b, c));
+    if (len == 0.0) {
+      atomicMin(zero_first, (unsigned long long)i);
+      out[3 * i] = out[3 * i + 1] = out[3 * i + 2] = 0.0;
+      continue;
+    }
+    out[3 * i] = __ddiv_rn(a, len);
+    out[3 * i + 1] = __ddiv_rn(b, len);
+    out[3 * i + 2] = __ddiv_rn(c, len);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // shard binning: keep a triangle iff its f64 AABB,
 // grown by the margin, meets one of the shard's boxes.  Fragments are convex
@@ -1820,6 +1839,24 @@ extern "C" int fhv_unpack_records(fhv_ctx* ctx, const void* in, int64_t n, fhv_p
                                                           pool->obj, pool->prev);
   }
   return check_cuda(ctx, cudaGetLastError());
+}
+
+extern "C" int fhv_unit_rows(fhv_ctx* ctx, int64_t n, const double* in, double* out, int64_t* zero_first,
+                             void* stream) {
+  if (!ctx || n < 0 || (n > 0 && (!in || !out))) return FHV_BAD_ARGS;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = reset_control(ctx, s);
+  if (rc) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->spare[2], 0xff, 8, s)))) return rc;
+  if (n > 0) {
+    LaunchScope L_(ctx, kStFaceNormals, s);
+    k_unit_rows<<<grid_for(n, 256), 256, 0, s>>>(n, in, out, &ctx->ctl->spare[2]);
+  }
+  if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  if ((rc = sync_control(ctx, s))) return rc;
+  const unsigned long long z = ctx->ctl_host->spare[2];
+  if (zero_first) *zero_first = z == ~0ull ? -1 : (int64_t)z;
+  return FHV_OK;
 }
 
 extern "C" int fhv_face_normals(fhv_ctx* ctx, int64_t n_tri, const double* pos, double* fnrm, void* stream) {

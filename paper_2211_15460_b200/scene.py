@@ -20,7 +20,7 @@ import numpy as np
 
 __all__ = [
     "AXIS_VIEWS", "Aabb", "Camera", "Material", "Scene", "SceneError", "SceneLoadError",
-    "Triangle", "Vertex", "capture_camera", "make_quad", "make_triangle", "normalize_scene",
+    "SceneTransform", "Triangle", "Vertex", "capture_camera", "make_quad", "make_triangle", "normalize_scene",
     "viewpoint_camera",
 ]
 
@@ -69,8 +69,9 @@ class Material:
     alpha: float = 1.0
 
     def __post_init__(self):
-        if any(not 0.0 <= c <= 1.0 for c in (*self.diffuse, *self.specular)):
-            raise SceneError("material channel outside [0,1]")
+        for channel in (*self.diffuse, *self.specular):
+            if not 0.0 <= channel <= 1.0:
+                raise SceneError(f"material channel {channel} outside [0,1]")
         if not self.shininess > 0.0:
             raise SceneError("shininess must be > 0")
         if not 0.0 <= self.alpha <= 1.0:
@@ -292,8 +293,28 @@ class Camera:
         return out
 
 
+@dataclass(frozen=True)
+class SceneTransform:
+    """Uniform scale followed by translation: p' = scale * p + offset (fhv/scene.py:441-457)."""
+
+    scale: float
+    offset: np.ndarray
+
+    def apply(self, points) -> np.ndarray:
+        return np.asarray(points, dtype=np.float64) * self.scale + self.offset
+
+    def invert(self, points) -> np.ndarray:
+        return (np.asarray(points, dtype=np.float64) - self.offset) / self.scale
+
+    @property
+    def is_identity(self) -> bool:
+        return self.scale == 1.0 and not self.offset.any()
+
+
 def normalize_scene(scene: Scene, margin: float = 0.0):
-    """Uniformly map the scene bounds into [margin, 1-margin]^3 (fhv/scene.py:460-487)."""
+    """Uniformly map the scene bounds into [margin, 1-margin]^3 (fhv/scene.py:460-487),
+    vectorised over all vertices (same elementwise p * scale + offset).
+    Returns the normalised scene and its SceneTransform."""
     if not 0.0 <= margin < 0.25:
         raise SceneError(f"margin {margin} outside [0, 0.25)")
     longest = float(scene.bounds.extent.max())
@@ -305,7 +326,7 @@ def normalize_scene(scene: Scene, margin: float = 0.0):
     out = Scene(materials=scene.materials, arrays={
         "positions": pos, "normals": scene.normals, "face_normals": scene.face_normals,
         "material_id": scene.material_id, "object_id": scene.object_id})
-    return out, (scale, offset)
+    return out, SceneTransform(scale, offset)
 
 
 def capture_camera(scene: Scene, axis: str = "+z", resolution: int = 256) -> Camera:
