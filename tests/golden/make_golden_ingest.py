@@ -158,8 +158,12 @@ def main():
                 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
                 from paper_2211_15460_b200 import sample_scenes as ours
                 mine = ours.scatter1m()
-                tris = [fscene.make_triangle(*p, *n, material_id=int(mi), object_id=int(oi))
-                        for p, n, mi, oi in zip(mine.positions, mine.normals, mine.material_id, mine.object_id)]
+                # the package's own scatter1M arrays as reference Triangles, verbatim
+                tris = [fscene.Triangle(fscene.Vertex(p[0], n[0]), fscene.Vertex(p[1], n[1]),
+                                        fscene.Vertex(p[2], n[2]), material_id=int(mi), object_id=int(oi),
+                                        face_normal=f)
+                        for p, n, f, mi, oi in zip(mine.positions, mine.normals, mine.face_normals,
+                                                   mine.material_id, mine.object_id)]
                 s = fscene.Scene.from_triangles(tris, [fscene.Material(m.diffuse, m.specular, m.shininess, m.alpha)
                                                        for m in mine.materials])
             else:
