@@ -355,8 +355,19 @@ template <int kMode>
 __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
   Stats st = {0, 0, 0, 0};
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  for (long long k = x.start + blockIdx.x * (long long)blockDim.x + threadIdx.x; k < x.end;
-       k += (long long)gridDim.x * blockDim.x) {
+  // camera rays: a warp takes an 8x4 pixel tile instead of 32 pixels of one
+  // row (coherent rays walk similar octree nodes -> less divergence); the
+  // band [start, end) must be whole 4-row strips of a width divisible by 8
+  const bool tiled = x.from_camera && x.W % 8 == 0 && x.start % (4 * x.W) == 0 && x.end % (4 * x.W) == 0;
+  const long long tiles_per_row = x.W / 8;
+  for (long long kk = x.start + blockIdx.x * (long long)blockDim.x + threadIdx.x; kk < x.end;
+       kk += (long long)gridDim.x * blockDim.x) {
+    long long k = kk;
+    if (tiled) {
+      const long long i = kk - x.start, tile = i >> 5, l = i & 31;
+      const long long ty = tile / tiles_per_row, tx = tile - ty * tiles_per_row;
+      k = x.start + (ty * 4 + (l >> 3)) * x.W + tx * 8 + (l & 7);
+    }
     double o[3], d[3];
     if (x.from_camera) {
       camera_ray(x, k, o, d);
