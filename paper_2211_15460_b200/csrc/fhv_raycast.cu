@@ -167,20 +167,30 @@ __device__ bool leaf_hits(const RayParams& x, long long code, const double o[3],
 
 // DFS over the occupancy pyramid, nearest child first (fhv/_ckern.pyx:548-633).
 // visit_leaf(code) -> false stops.
-template <class V>
+// Stack entries pack (level, code): E = uint32_t when the octree has <= 9
+// levels (27-bit codes, half the local-memory traffic of the DFS stack), else
+// uint64_t.
+template <class E>
+struct StackCodec {
+  static constexpr int kShift = sizeof(E) == 4 ? 27 : 58;
+  static constexpr E kMask = (E)(((E)1 << kShift) - 1);
+};
+
+template <class E, class V>
 __device__ void traverse(const RayParams& x, const double o[3], const double d[3], double tmax, Stats& st,
                          V&& visit_leaf) {
+  using SC = StackCodec<E>;
   const double zero3[3] = {0.0, 0.0, 0.0}, one3[3] = {1.0, 1.0, 1.0};
   double te;
   if (!slab_box(o, d, zero3, one3, 0.0, tmax, &te)) return;
   const int L = x.v.levels;
-  unsigned long long stack[kStack];
+  E stack[kStack];
   int sp = 0;
-  stack[sp++] = 0ull;  // level 0, code 0
+  stack[sp++] = (E)0;  // level 0, code 0
   while (sp > 0) {
-    const unsigned long long e = stack[--sp];
-    const int level = (int)(e >> 58);
-    const unsigned long long code = e & ((1ull << 58) - 1);
+    const E e = stack[--sp];
+    const int level = (int)(e >> SC::kShift);
+    const unsigned long long code = (unsigned long long)(e & SC::kMask);
     if (level == L) {
       st.visited++;
       if (!visit_leaf((long long)code)) return;
@@ -225,12 +235,13 @@ __device__ void traverse(const RayParams& x, const double o[3], const double d[3
       cc[m + 1] = c;
       ++nc;
     }
-    const unsigned long long lvl = (unsigned long long)(level + 1) << 58;
-    for (int j = nc - 1; j >= 0; --j) stack[sp++] = lvl | (code * 8ull + (unsigned long long)cc[j]);
+    const E lvl = (E)((E)(level + 1) << SC::kShift);
+    for (int j = nc - 1; j >= 0; --j) stack[sp++] = lvl | (E)(code * 8ull + (unsigned long long)cc[j]);
   }
 }
 
 // _transmit (fhv/_ckern.pyx:326-435)
+template <class E>
 __device__ double transmit(const RayParams& x, const double p[3], int li, long long ex_obj, long long ex_cell,
                            Stats& st) {
   double l[3], tmax;
@@ -252,7 +263,7 @@ __device__ double transmit(const RayParams& x, const double p[3], int li, long l
 #pragma unroll
   for (int k = 0; k < 3; ++k) o[k] = __dadd_rn(p[k], __dmul_rn(x.eps, l[k]));
   double tau = 1.0;
-  traverse(x, o, l, tmax, st, [&](long long code) {
+  traverse<E>(x, o, l, tmax, st, [&](long long code) {
     return leaf_hits(x, code, o, l, 0.0, tmax, st, [&](double, long long k) {
       if ((long long)__ldg(&x.v.obj[k]) == ex_obj && code == ex_cell) return true;
       tau = __dmul_rn(tau, __dsub_rn(1.0, x.s.alpha[__ldg(&x.v.mat[k])]));
@@ -266,7 +277,7 @@ __device__ double transmit(const RayParams& x, const double p[3], int li, long l
 // ray-cast mode as a template parameter: only mode 2 (shadows) instantiates
 // the second (shadow) traversal and its stack, which keeps the stack frame of
 // the primary-ray kernels of modes 0 / 1 small.
-template <int kMode>
+template <int kMode, class E>
 __device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats& st, double out[3]) {
   const double p[3] = {(double)x.v.pos[3 * i], (double)x.v.pos[3 * i + 1], (double)x.v.pos[3 * i + 2]};
   const double n[3] = {(double)x.v.nrm[3 * i], (double)x.v.nrm[3 * i + 1], (double)x.v.nrm[3 * i + 2]};
@@ -300,7 +311,7 @@ __device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats
     double ndh = __dadd_rn(__dadd_rn(__dmul_rn(n[0], h[0]), __dmul_rn(n[1], h[1])), __dmul_rn(n[2], h[2]));
     if (ndh < 0.0) ndh = 0.0;
     double tau = 1.0;
-    if (kMode == 2) tau = transmit(x, p, li, (long long)x.v.obj[i], leaf, st);
+    if (kMode == 2) tau = transmit<E>(x, p, li, (long long)x.v.obj[i], leaf, st);
     const double sp = pow(ndh, shin);
     const double* amb = x.s.light_ambient + 3 * li;
     const double* col = x.s.light_color + 3 * li;
@@ -349,9 +360,9 @@ __device__ __forceinline__ void camera_ray(const RayParams& x, long long k, doub
 }
 
 #ifndef FHV_RAY_MINB
-#define FHV_RAY_MINB 1  // resident 128-thread CTAs per SM the ray kernel is register-budgeted for
+#define FHV_RAY_MINB 4  // resident 128-thread CTAs per SM the ray kernel is register-budgeted for
 #endif
-template <int kMode>
+template <int kMode, class E>
 __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
   Stats st = {0, 0, 0, 0};
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -381,14 +392,14 @@ __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
     double c0 = 0.0, c1 = 0.0, c2 = 0.0, acc = 0.0;
     bool any_hit = false;
     long long first_obj = -1;
-    traverse(x, o, d, inf, st, [&](long long code) {
+    traverse<E>(x, o, d, inf, st, [&](long long code) {
       bool stop = false;
       leaf_hits(x, code, o, d, 0.0, inf, st, [&](double, long long i) {
         st.hits++;
         if (first_obj < 0) first_obj = (long long)x.v.obj[i];
         double col[3];
         if (kMode == 0) {
-          shade_hit<kMode>(x, i, code, st, col);
+          shade_hit<kMode, E>(x, i, code, st, col);
           c0 = col[0];
           c1 = col[1];
           c2 = col[2];
@@ -398,7 +409,7 @@ __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
           return false;
         }
         const double a = x.s.alpha[x.v.mat[i]];
-        shade_hit<kMode>(x, i, code, st, col);
+        shade_hit<kMode, E>(x, i, code, st, col);
         const double tc = __dmul_rn(__dsub_rn(1.0, acc), a);
         c0 = __dadd_rn(c0, __dmul_rn(tc, col[0]));
         c1 = __dadd_rn(c1, __dmul_rn(tc, col[1]));
@@ -453,12 +464,22 @@ int launch(fhv_ctx* ctx, RayParams& x, void* stream) {
   {
     LaunchScope L_(ctx, kStRaycast, (cudaStream_t)stream);
     const int g = grid_for(x.end - x.start, 128);
-    if (x.mode == 0)
-      k_raycast<0><<<g, 128, 0, (cudaStream_t)stream>>>(x);
-    else if (x.mode == 1)
-      k_raycast<1><<<g, 128, 0, (cudaStream_t)stream>>>(x);
-    else
-      k_raycast<2><<<g, 128, 0, (cudaStream_t)stream>>>(x);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (x.v.levels <= 9) {
+      if (x.mode == 0)
+        k_raycast<0, uint32_t><<<g, 128, 0, st>>>(x);
+      else if (x.mode == 1)
+        k_raycast<1, uint32_t><<<g, 128, 0, st>>>(x);
+      else
+        k_raycast<2, uint32_t><<<g, 128, 0, st>>>(x);
+    } else {
+      if (x.mode == 0)
+        k_raycast<0, unsigned long long><<<g, 128, 0, st>>>(x);
+      else if (x.mode == 1)
+        k_raycast<1, unsigned long long><<<g, 128, 0, st>>>(x);
+      else
+        k_raycast<2, unsigned long long><<<g, 128, 0, st>>>(x);
+    }
   }
   return check_cuda(ctx, cudaGetLastError());
 }

@@ -109,11 +109,19 @@ __global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restri
   const int64_t base = (int64_t)tile * BLOCK * ITEMS + (int64_t)threadIdx.x * ITEMS;
   uint32_t v[ITEMS];
   uint64_t sum = 0;
+  const bool vec = ITEMS % 4 == 0 && base + ITEMS <= n && ((uintptr_t)(in + base) & 15) == 0;
+  if (vec) {  // 16-B loads: a thread's ITEMS consecutive counts
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    v[i] = base + i < n ? in[base + i] : 0u;
-    sum += v[i];
+    for (int i = 0; i < ITEMS; i += 4) {
+      const uint4 q = *reinterpret_cast<const uint4*>(in + base + i);
+      v[i] = q.x; v[i + 1] = q.y; v[i + 2] = q.z; v[i + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) v[i] = base + i < n ? in[base + i] : 0u;
   }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) sum += v[i];
   const uint64_t excl = block_excl_scan<BLOCK>(sum, &total_s);
   if (threadIdx.x < 32) {
     const uint64_t pf = lookback_warp(status, tile, total_s);
@@ -121,10 +129,20 @@ __global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restri
   }
   __syncthreads();
   uint64_t run = prefix_s + excl;
+  if (vec && ((uintptr_t)(out + base) & 15) == 0) {  // 16-B stores
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    if (base + i < n) out[base + i] = run;
-    run += v[i];
+    for (int i = 0; i < ITEMS; i += 2) {
+      const unsigned long long a = run;
+      run += v[i];
+      *reinterpret_cast<ulonglong2*>(out + base + i) = make_ulonglong2(a, run);
+      run += v[i + 1];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (base + i < n) out[base + i] = run;
+      run += v[i];
+    }
   }
   if (threadIdx.x == 0 && tile == n_tiles - 1) ctl->scan_total = prefix_s + total_s;
 }
@@ -402,7 +420,7 @@ inline int grid_for(int64_t n, int block) {
 
 int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, int64_t n, cudaStream_t s,
                     const unsigned long long* n_dev) {
-  constexpr int B = 256, I = 8;
+  constexpr int B = 512, I = 16;  // 8192 elements per tile: a short look-back chain
   const int64_t per = (int64_t)B * I;
   const unsigned tiles = (unsigned)((n + per - 1) / per);
   if (n <= 0) {
