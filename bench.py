@@ -50,6 +50,9 @@ def parse():
                     help="C3 = the headline workload; C2 / C4 / C5 = the other BASELINE configs (1 GPU)")
     ap.add_argument("--exact-order", action="store_true", help="bit-identical in-leaf order (extra fix-up pass)")
     ap.add_argument("--packed", action="store_true", help="packed 64-bit splat z-test")
+    ap.add_argument("--composite", default="auto", choices=("auto", "peer", "allreduce"),
+                    help="multi-GPU splat composite: peer memory (fhv_splat_peer over NVLink P2P) or NCCL "
+                         "all-reduces; auto = peer when the peer mappings can be set up")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="few steps, no clocks/e2e/cpu (for ncu)")
     return ap.parse_args()
@@ -450,14 +453,26 @@ def main():
         comm = shard.TorchComm(device=dev)
         ranges = shard.shard_ranges(L, world, shard.fragment_weights(scene, strat, cfg, L))
         bufs = shard.SplatBuffers(W, H, dev)
+        peer, composite = None, args.composite
+        if composite != "allreduce":
+            try:  # NVLink peer mappings of every rank's splat buffers (symmetric memory)
+                peer = shard.PeerFrame(W, H, comm, dev)
+                composite = "peer"
+            except Exception as e:  # noqa: BLE001
+                if composite == "peer":
+                    raise
+                composite = f"allreduce (peer mapping unavailable: {type(e).__name__})"
+        mode = "peer" if peer is not None else "allreduce"
 
         def step(tris=ds, out=img):
             vol = shard.pofa_build_shard(scene, strat, cfg, L, comm, ranges=ranges, exact_order=args.exact_order,
                                          device=dev, tris=tris)
             shard.splat_render_shard(vol, view, w["lights"], w["radius"], scene.materials, comm, out=out,
-                                     shading=shading, buffers=bufs)
+                                     shading=shading, buffers=bufs, composite=mode, peer=peer)
             return vol
     else:
+        composite = None
+
         def step(tris=ds, out=img):
             vol = fhv.pofa_build(scene, strat, cfg, L, exact_order=args.exact_order, device=dev, tris=tris)
             fhv.splat_render(vol.pool, view, w["lights"], w["radius"], scene.materials, out=out, packed=args.packed,
@@ -652,6 +667,7 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded icosphere field, no dataset)",
                 "config": dict(CONFIG, fragments=n_frags,
                                parallelism=f"morton-range shards x{world} (NCCL)" if world > 1 else "single",
+                               composite=composite if world > 1 else None,
                                exact_order=bool(args.exact_order), splat="packed" if args.packed else "exact"),
                 "novel_view_fps": 1e3 / recon_ms if recon_ms else None,
                 "capture_frag_per_s": n_frags / (capture_ms / 1e3) if capture_ms else None,

@@ -224,6 +224,33 @@ int fhv_rebuild_pofa(fhv_ctx *ctx, int32_t levels, const fhv_pool_t *src, int64_
 int fhv_pack_records(fhv_ctx *ctx, const fhv_pool_t *pool, int64_t n, void *out, void *stream);
 int fhv_unpack_records(fhv_ctx *ctx, const void *in, int64_t n, fhv_pool_t *pool, void *stream);
 
+/* Multi-GPU splat composited over peer memory (NVLink / NVSwitch P2P; on one
+   device: plain pointers).  The frame's rows are cut into one slab per rank
+   (rank q owns rows [q H / N, (q+1) H / N)); keys[q] / winners[q] are rank
+   q's slab buffers (8 B per pixel each), rgba[q] / depth[q] rank q's full
+   frame ([H][W][4] / [H][W] f64) -- all as seen from the calling process.
+   SURVEY.md section 8(e) "composite per-GPU reconstructions by depth". */
+#define FHV_MAX_PEERS 8
+typedef struct {
+  int32_t nranks;
+  int64_t width, height;
+  void *keys[FHV_MAX_PEERS];
+  void *winners[FHV_MAX_PEERS];
+  double *rgba[FHV_MAX_PEERS];
+  double *depth[FHV_MAX_PEERS];
+} fhv_peer_t;
+
+/* One phase of the peer splat for rank `rank` holding records [index_base,
+   index_base + n) of the union pool: 0 = empty its own slab, 1 = RED.MIN
+   depth keys into the owners' slabs (synchronises; extent[2] = max
+   footprint, the caller all-reduces it for the 4096-pixel check), 2 = winner
+   candidates, 3 = shade the winners it owns and store them (and, for its own
+   slab, the background) into every rank's frame.  Between phases every rank
+   must have finished the previous one (caller's barrier). */
+int fhv_splat_peer(fhv_ctx *ctx, int32_t phase, int64_t n, const float *pos, const float *nrm, const uint32_t *mat,
+                   const double *cam, double radius, const fhv_shading_t *shading, const double *background,
+                   const fhv_peer_t *peers, int32_t rank, int64_t index_base, int64_t *extent, void *stream);
+
 /* Self-test of the library's shared-divisor IEEE division against
    __ddiv_rn (device arrays of n doubles; fast / ref written).  Async. */
 int fhv_selftest_div(fhv_ctx *ctx, int64_t n, const double *x, const double *d, double *fast, double *ref,

@@ -47,6 +47,14 @@ class Shading(ctypes.Structure):
                 ("shininess", c_vp), ("alpha", c_vp)]
 
 
+FHV_MAX_PEERS = 8
+
+
+class Peer(ctypes.Structure):
+    _fields_ = [("nranks", c_i32), ("width", c_i64), ("height", c_i64), ("keys", c_vp * FHV_MAX_PEERS),
+                ("winners", c_vp * FHV_MAX_PEERS), ("rgba", c_vp * FHV_MAX_PEERS), ("depth", c_vp * FHV_MAX_PEERS)]
+
+
 class Volume(ctypes.Structure):
     _fields_ = [("layout", c_i32), ("levels", c_i32), ("offsets", c_vp), ("counts", c_vp), ("heads", c_vp),
                 ("prev", c_vp), ("pyramid", c_vp), ("pos", c_vp), ("nrm", c_vp), ("mat", c_vp), ("obj", c_vp)]
@@ -87,6 +95,8 @@ _SIGS = {
     "fhv_splat_shard_winners": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_f64, c_vp, c_i64, c_vp, c_vp]),
     "fhv_splat_shard_resolve": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_f64, _P(Shading), c_vp, c_vp,
                                                c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "fhv_splat_peer": (ctypes.c_int, [c_vp, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_f64, _P(Shading), c_vp, _P(Peer),
+                                      c_i32, c_i64, c_vp, c_vp]),
     "fhv_raycast": (ctypes.c_int, [c_vp, _P(Volume), _P(Shading), c_vp, c_vp, c_f64, c_f64, c_i32, c_f64, c_i64,
                                    c_i64, c_vp, c_vp, c_vp, c_vp]),
     "fhv_raycast_image": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, _P(Volume), _P(Shading), c_vp, c_vp,

@@ -44,7 +44,7 @@ from .scene import Camera, SceneError
 from .storage import FhvError, FragmentPool, OccupancyPyramid, PofaDirectory, _check_levels, morton_decode
 
 __all__ = ["Comm", "FhvPofaShard", "ThreadComm", "TorchComm", "fragment_weights", "pofa_build_shard",
-           "range_boxes", "shard_ranges", "splat_render_shard", "tile_leaves"]
+           "range_boxes", "shard_ranges", "splat_render_shard", "tile_leaves", "PeerFrame"]
 
 MAX_BOXES = 64
 BIN_MARGIN = 1e-5  # world units; fragments lie within 1 f32 ulp of the triangle's AABB
@@ -149,6 +149,15 @@ class Comm:
     def all_reduce_(self, t: torch.Tensor, op: str) -> torch.Tensor:
         raise NotImplementedError
 
+    def barrier(self) -> None:
+        """Every rank's device work issued so far is complete on return."""
+        raise NotImplementedError
+
+    def peer_alloc(self, shapes_dtypes: list, device) -> tuple:
+        """Peer-visible device buffers: (local tensors, per-rank lists of the
+        buffers' device pointers as mapped in THIS process)."""
+        raise NotImplementedError
+
 
 class TorchComm(Comm):
     """torch.distributed over the default (or given) process group.  NCCL
@@ -184,6 +193,26 @@ class TorchComm(Comm):
             self.dist.all_reduce(t, op=rop, group=self.group)
         return t
 
+    def barrier(self) -> None:
+        if self.device is not None:
+            torch.cuda.synchronize(self.device)
+        self.dist.barrier(group=self.group)
+
+    def peer_alloc(self, shapes_dtypes: list, device) -> tuple:
+        # NVLink peer mappings through torch's symmetric memory (one buffer per
+        # tensor, rendezvous over this group): buffer_ptrs[r] = rank r's buffer
+        # in this process's address space
+        import torch.distributed._symmetric_memory as symm_mem
+        group = self.group if self.group is not None else self.dist.group.WORLD
+        tensors, ptrs = [], [[] for _ in range(self.world)]
+        for shape, dtype in shapes_dtypes:
+            t = symm_mem.empty(shape, dtype=dtype, device=device)
+            hdl = symm_mem.rendezvous(t, group.group_name)
+            tensors.append(t)
+            for r in range(self.world):
+                ptrs[r].append(int(hdl.buffer_ptrs[r]))
+        return tensors, ptrs
+
 
 class _ThreadHub:
     def __init__(self, world: int):
@@ -215,6 +244,16 @@ class ThreadComm(Comm):
 
     def all_gather_int(self, v: int) -> list:
         return [int(x) for x in self._exchange(int(v))]
+
+    def barrier(self) -> None:
+        torch.cuda.synchronize(self.device)
+        self.hub.barrier.wait()
+
+    def peer_alloc(self, shapes_dtypes: list, device) -> tuple:
+        # one process, one device: every rank's pointers are directly usable
+        tensors = [torch.empty(shape, dtype=dtype, device=device) for shape, dtype in shapes_dtypes]
+        mine = [t.data_ptr() for t in tensors]
+        return tensors, [list(p) for p in self._exchange(mine)]
 
     def all_reduce_(self, t: torch.Tensor, op: str) -> torch.Tensor:
         if t.is_cuda:
@@ -340,13 +379,77 @@ class SplatBuffers:
         self.winners = torch.empty(width * height, dtype=torch.int64, device=device)
 
 
+class PeerFrame:
+    """Peer-visible splat buffers of one rank for a W x H view (reusable
+    across frames): its row slab of depth keys and winners (rank q owns rows
+    [q H / N, (q+1) H / N)) and its full-frame rgba / depth, plus the table
+    of every rank's buffers as mapped in this process (fhv_peer_t)."""
+
+    def __init__(self, width: int, height: int, comm: Comm, device):
+        N, q = comm.world, comm.rank
+        if N > _lib.FHV_MAX_PEERS or height < N:
+            raise FhvError(f"peer splat supports up to {_lib.FHV_MAX_PEERS} ranks and height >= ranks")
+        rows = (q + 1) * height // N - q * height // N
+        t, ptrs = comm.peer_alloc([((rows * width,), torch.int64), ((rows * width,), torch.int64),
+                                   ((height, width, 4), torch.float64), ((height, width), torch.float64)], device)
+        self.keys, self.winners, self.rgba, self.depth = t
+        self.width, self.height, self.comm = width, height, comm
+        st = _lib.Peer()
+        st.nranks, st.width, st.height = N, width, height
+        for r in range(N):
+            st.keys[r], st.winners[r], st.rgba[r], st.depth[r] = ptrs[r]
+        self.struct = st
+
+
+def _splat_peer(vol, camera, splat_radius_world, comm, background, out, shading, peer):
+    """Peer-memory composite (fhv_splat_peer): RED.MIN into the owners' row
+    slabs, winner candidates likewise, then each rank shades the winners it
+    owns straight into every rank's frame; four phases separated by barriers."""
+    pool = vol.pool
+    dev = pool.device
+    w, h = camera.resolution
+    if peer is None or (peer.width, peer.height) != (w, h):
+        peer = PeerFrame(w, h, comm, dev)
+    n = pool.stored_count
+    cam = host_f64(camera.scalars())
+    bg = host_f64(background)
+    lib = _lib.load()
+    cx, st = _lib.ctx(dev), _lib.stream_ptr(dev)
+    r = float(splat_radius_world)
+    args = (n, _lib.ptr(pool.position), _lib.ptr(pool.normal), _lib.ptr(pool.material_id), cam.ctypes.data, r,
+            shading.struct(), bg.ctypes.data, peer.struct, comm.rank, vol.base)
+    _lib.check(lib.fhv_splat_peer(cx, 0, *args, None, st), "splat peer fill")
+    comm.barrier()
+    fp = (ctypes.c_int64 * 2)()
+    _lib.check(lib.fhv_splat_peer(cx, 1, *args, fp, st), "splat peer keys")
+    ext = torch.tensor([fp[0], fp[1]], dtype=torch.int64, device=dev)
+    comm.all_reduce_(ext, "max")
+    kx, ky = (int(v) for v in ext.cpu().tolist())
+    if kx * ky > 4096:
+        _lib.check(_lib.FHV_SPLAT_BIG, "splat_render_shard")
+    comm.barrier()
+    _lib.check(lib.fhv_splat_peer(cx, 2, *args, None, st), "splat peer winners")
+    comm.barrier()
+    _lib.check(lib.fhv_splat_peer(cx, 3, *args, None, st), "splat peer resolve")
+    comm.barrier()
+    out.pixels.copy_(peer.rgba)
+    out.depth.copy_(peer.depth)
+    return out
+
+
 def splat_render_shard(vol: FhvPofaShard, camera: Camera, lights, splat_radius_world: float, materials, comm: Comm,
                        background=(0.0, 0.0, 0.0, 0.0), *, out: ImageBuffer | None = None,
-                       shading: DeviceShading | None = None, buffers: SplatBuffers | None = None) -> ImageBuffer:
+                       shading: DeviceShading | None = None, buffers: SplatBuffers | None = None,
+                       composite: str = "allreduce", peer: PeerFrame | None = None) -> ImageBuffer:
     """``splat_render`` of the union of all ranks' pools; every rank returns
-    the full frame."""
+    the full frame.  ``composite="allreduce"``: key / winner / pixel planes
+    combined with collective all-reduces (NCCL); ``"peer"``: written straight
+    into the owner's / every rank's buffers over peer memory (fhv_splat_peer,
+    ``peer`` = a reusable PeerFrame)."""
     if splat_radius_world <= 0.0:
         raise SceneError("splat radius must be > 0")
+    if composite not in ("allreduce", "peer"):
+        raise FhvError(f"unknown composite {composite!r}")
     pool = vol.pool
     dev = pool.device
     w, h = camera.resolution
@@ -355,6 +458,8 @@ def splat_render_shard(vol: FhvPofaShard, camera: Camera, lights, splat_radius_w
                           torch.empty((h, w), dtype=torch.float64, device=dev))
     if shading is None:
         shading = DeviceShading(materials, lights, dev)
+    if composite == "peer":
+        return _splat_peer(vol, camera, splat_radius_world, comm, background, out, shading, peer)
     if buffers is None:
         buffers = SplatBuffers(w, h, dev)
     n = pool.stored_count

@@ -98,3 +98,39 @@ def test_sharded_fast_order_is_a_per_leaf_permutation():
         a = pos[off[c]:off[c] + cnt[c]]
         b = rpos[off[c]:off[c] + cnt[c]]
         assert np.array_equal(a[np.lexsort(a.T)], b[np.lexsort(b.T)])
+
+
+@pytest.mark.parametrize("name", ("cornell", "spheres"))
+@pytest.mark.parametrize("world", (2, 3, 4, 8))
+def test_peer_composited_splat_equals_single_gpu(name, world):
+    """composite="peer": depth keys / winners RED.MIN'd straight into the
+    owning rank's row slab and shaded pixels stored into every rank's frame
+    (fhv_splat_peer) -- every rank's frame bit-identical to splat_render of
+    the whole pool, twice in a row (buffers reused)."""
+    scene = _scene(name)
+    res, L = 256, 6
+    cfg = fhv.RasterConfig.from_camera(fhv.capture_camera(scene, "+z", res))
+    ns = fhv.CaptureStrategy.normal_space()
+    ref = fhv.pofa_build(scene, ns, cfg, L, exact_order=True)
+    cams = [fhv.viewpoint_camera("+x", (96, 80), "perspective"),
+            fhv.viewpoint_camera("+y", (64, 70), "perspective", fov_deg=50.0, distance=1.2)]
+    r = 1.0 / res
+    bg = (0.1, 0.2, 0.3, 0.5)
+    refs = [image_numpy(fhv.splat_render(ref.pool, cam, [fhv.headlight(cam)], r, scene.materials, bg))
+            for cam in cams]
+
+    def rank_fn(c):
+        v = shard.pofa_build_shard(scene, ns, cfg, L, c, exact_order=True)
+        imgs = []
+        for cam in cams:
+            peer = shard.PeerFrame(*cam.resolution, c, torch.device("cuda", 0))
+            for _ in range(2):
+                imgs.append(image_numpy(shard.splat_render_shard(v, cam, [fhv.headlight(cam)], r, scene.materials, c,
+                                                                 bg, composite="peer", peer=peer)))
+        return imgs
+
+    for imgs in _run_ranks(world, rank_fn):
+        for i, img in enumerate(imgs):
+            want = refs[i // 2]
+            assert np.array_equal(img.depth, want.depth)
+            assert np.array_equal(img.pixels, want.pixels)
