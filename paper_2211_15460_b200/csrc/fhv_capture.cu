@@ -647,17 +647,21 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
     if (slot >= 0) o.prev[slot] = lower ? prev_slot : old;
   }
   if (slot >= 0) {
-    o.pos[3 * slot] = __double2float_rn(w[0]);
-    o.pos[3 * slot + 1] = __double2float_rn(w[1]);
-    o.pos[3 * slot + 2] = __double2float_rn(w[2]);
-    o.nrm[3 * slot] = __double2float_rn(nn[0]);
-    o.nrm[3 * slot + 1] = __double2float_rn(nn[1]);
-    o.nrm[3 * slot + 2] = __double2float_rn(nn[2]);
-    o.mat[slot] = d.mat;
-    o.obj[slot] = d.obj;
+    // pool capacities are < 2^32 records: 32-bit slot, one wide multiply-add per address
+    const uint32_t s32 = (uint32_t)slot;
+    float* pp = o.pos + 3ull * s32;
+    float* np = o.nrm + 3ull * s32;
+    pp[0] = __double2float_rn(w[0]);
+    pp[1] = __double2float_rn(w[1]);
+    pp[2] = __double2float_rn(w[2]);
+    np[0] = __double2float_rn(nn[0]);
+    np[1] = __double2float_rn(nn[1]);
+    np[2] = __double2float_rn(nn[2]);
+    o.mat[s32] = d.mat;
+    o.obj[s32] = d.obj;
     // POFA: prev_index = -1; under EXACT_ORDER the emission rank is parked
     // here until k_leaf_order restores the reference's in-leaf order
-    if (kMode == kPofa) o.prev[slot] = (o.flags & FHV_EXACT_ORDER) ? (int32_t)(uint32_t)rank : -1;
+    if (kMode == kPofa) o.prev[s32] = (o.flags & FHV_EXACT_ORDER) ? (int32_t)(uint32_t)rank : -1;
   }
 }
 

@@ -42,6 +42,7 @@ struct RayParams {
   double* out_rgba;
   int32_t* out_ids;
   long long* counters;
+  unsigned long long* tile_ticket;  // dynamic 32-ray work fetching (zeroed before the launch)
 };
 
 struct Stats {
@@ -202,16 +203,22 @@ __device__ void traverse(const RayParams& x, const double o[3], const double d[3
     const double size = __dmul_rn(2.0, half);
     const double lo[3] = {__dmul_rn((double)compact3(code), size), __dmul_rn((double)compact3(code >> 1), size),
                           __dmul_rn((double)compact3(code >> 2), size)};
-    // plane parameters for lo, lo+half, lo+2*half on each axis
+    // plane parameters for lo, lo+half, lo+2*half on each axis; the outer
+    // plane of a side is only divided out when an occupied child lies on
+    // that side (children with bit a = 0 use planes 0,1; = 1 use planes 1,2)
     double tp[3][3];
     double pl[3][3];
+    const unsigned side_lo[3] = {mask & 0x55u, mask & 0x33u, mask & 0x0Fu};
+    const unsigned side_hi[3] = {mask & 0xAAu, mask & 0xCCu, mask & 0xF0u};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       pl[a][0] = lo[a];
       pl[a][1] = __dadd_rn(lo[a], half);
       pl[a][2] = __dadd_rn(pl[a][1], half);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) tp[a][k] = d[a] != 0.0 ? __ddiv_rn(__dsub_rn(pl[a][k], o[a]), d[a]) : 0.0;
+      const bool dz = d[a] == 0.0;
+      tp[a][0] = (!dz && side_lo[a]) ? __ddiv_rn(__dsub_rn(pl[a][0], o[a]), d[a]) : 0.0;
+      tp[a][1] = !dz ? __ddiv_rn(__dsub_rn(pl[a][1], o[a]), d[a]) : 0.0;
+      tp[a][2] = (!dz && side_hi[a]) ? __ddiv_rn(__dsub_rn(pl[a][2], o[a]), d[a]) : 0.0;
     }
     double cte[8];
     int cc[8];
@@ -371,8 +378,16 @@ __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
   // band [start, end) must be whole 4-row strips of a width divisible by 8
   const bool tiled = x.from_camera && x.W % 8 == 0 && x.start % (4 * x.W) == 0 && x.end % (4 * x.W) == 0;
   const long long tiles_per_row = x.W / 8;
-  for (long long kk = x.start + blockIdx.x * (long long)blockDim.x + threadIdx.x; kk < x.end;
-       kk += (long long)gridDim.x * blockDim.x) {
+  // warps fetch 32-ray tiles from a global ticket (ray costs vary by orders
+  // of magnitude: dynamic fetching instead of a static stride evens the tail)
+  const long long n_rays = x.end - x.start;
+  while (true) {
+    unsigned long long t = 0;
+    if (lane_id() == 0) t = atomicAdd(x.tile_ticket, 1ull);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if ((long long)t * 32 >= n_rays) break;
+    const long long kk = x.start + (long long)t * 32 + lane_id();
+    if (kk >= x.end) continue;
     long long k = kk;
     if (tiled) {
       const long long i = kk - x.start, tile = i >> 5, l = i & 31;
@@ -461,6 +476,9 @@ inline int grid_for(long long n, int block, int per_sm = 16) {
 
 int launch(fhv_ctx* ctx, RayParams& x, void* stream) {
   if (x.end <= x.start) return FHV_OK;
+  x.tile_ticket = &ctx->ctl->spare[3];
+  int rc = check_cuda(ctx, cudaMemsetAsync(x.tile_ticket, 0, sizeof(unsigned long long), (cudaStream_t)stream));
+  if (rc) return rc;
   {
     LaunchScope L_(ctx, kStRaycast, (cudaStream_t)stream);
     const int g = grid_for(x.end - x.start, 128);
