@@ -177,6 +177,61 @@ struct StackCodec {
   static constexpr E kMask = (E)(((E)1 << kShift) - 1);
 };
 
+// one inner node of the DFS: children whose slabs the ray meets pushed far
+// first, so the nearest (t_enter, child) pops next (fhv/_ckern.pyx:580-632)
+template <class E>
+__device__ __forceinline__ void expand_node(const RayParams& x, const double o[3], const double d[3], double tmax,
+                                            int level, unsigned long long code, E* stack, int& sp) {
+  using SC = StackCodec<E>;
+  const unsigned mask = __ldg(&x.v.pyramid[pyr_level_offset(level) + (long long)code]);
+  if (mask == 0) return;
+  const double half = __longlong_as_double((1022LL - level) << 52);  // 0.5 / 2^level, exact
+  const double size = __dmul_rn(2.0, half);
+  const double lo[3] = {__dmul_rn((double)compact3(code), size), __dmul_rn((double)compact3(code >> 1), size),
+                        __dmul_rn((double)compact3(code >> 2), size)};
+  // plane parameters for lo, lo+half, lo+2*half on each axis; the outer
+  // plane of a side is only divided out when an occupied child lies on
+  // that side (children with bit a = 0 use planes 0,1; = 1 use planes 1,2)
+  double tp[3][3];
+  double pl[3][3];
+  const unsigned side_lo[3] = {mask & 0x55u, mask & 0x33u, mask & 0x0Fu};
+  const unsigned side_hi[3] = {mask & 0xAAu, mask & 0xCCu, mask & 0xF0u};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    pl[a][0] = lo[a];
+    pl[a][1] = __dadd_rn(lo[a], half);
+    pl[a][2] = __dadd_rn(pl[a][1], half);
+    const bool dz = d[a] == 0.0;
+    tp[a][0] = (!dz && side_lo[a]) ? __ddiv_rn(__dsub_rn(pl[a][0], o[a]), d[a]) : 0.0;
+    tp[a][1] = !dz ? __ddiv_rn(__dsub_rn(pl[a][1], o[a]), d[a]) : 0.0;
+    tp[a][2] = (!dz && side_hi[a]) ? __ddiv_rn(__dsub_rn(pl[a][2], o[a]), d[a]) : 0.0;
+  }
+  double cte[8];
+  int cc[8];
+  int nc = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (!((mask >> c) & 1u)) continue;
+    const int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
+    double t0 = 0.0, t1 = tmax;
+    if (!slab_axis(o[0], d[0], pl[0][bx], pl[0][bx + 1], tp[0][bx], tp[0][bx + 1], t0, t1)) continue;
+    if (!slab_axis(o[1], d[1], pl[1][by], pl[1][by + 1], tp[1][by], tp[1][by + 1], t0, t1)) continue;
+    if (!slab_axis(o[2], d[2], pl[2][bz], pl[2][bz + 1], tp[2][bz], tp[2][bz + 1], t0, t1)) continue;
+    if (t0 > t1) continue;
+    int m = nc - 1;
+    while (m >= 0 && (cte[m] > t0 || (cte[m] == t0 && cc[m] > c))) {
+      cte[m + 1] = cte[m];
+      cc[m + 1] = cc[m];
+      --m;
+    }
+    cte[m + 1] = t0;
+    cc[m + 1] = c;
+    ++nc;
+  }
+  const E lvl = (E)((E)(level + 1) << SC::kShift);
+  for (int j = nc - 1; j >= 0; --j) stack[sp++] = lvl | (E)(code * 8ull + (unsigned long long)cc[j]);
+}
+
 template <class E, class V>
 __device__ void traverse(const RayParams& x, const double o[3], const double d[3], double tmax, Stats& st,
                          V&& visit_leaf) {
@@ -197,53 +252,7 @@ __device__ void traverse(const RayParams& x, const double o[3], const double d[3
       if (!visit_leaf((long long)code)) return;
       continue;
     }
-    const unsigned mask = __ldg(&x.v.pyramid[pyr_level_offset(level) + (long long)code]);
-    if (mask == 0) continue;
-    const double half = __longlong_as_double((1022LL - level) << 52);  // 0.5 / 2^level, exact
-    const double size = __dmul_rn(2.0, half);
-    const double lo[3] = {__dmul_rn((double)compact3(code), size), __dmul_rn((double)compact3(code >> 1), size),
-                          __dmul_rn((double)compact3(code >> 2), size)};
-    // plane parameters for lo, lo+half, lo+2*half on each axis; the outer
-    // plane of a side is only divided out when an occupied child lies on
-    // that side (children with bit a = 0 use planes 0,1; = 1 use planes 1,2)
-    double tp[3][3];
-    double pl[3][3];
-    const unsigned side_lo[3] = {mask & 0x55u, mask & 0x33u, mask & 0x0Fu};
-    const unsigned side_hi[3] = {mask & 0xAAu, mask & 0xCCu, mask & 0xF0u};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      pl[a][0] = lo[a];
-      pl[a][1] = __dadd_rn(lo[a], half);
-      pl[a][2] = __dadd_rn(pl[a][1], half);
-      const bool dz = d[a] == 0.0;
-      tp[a][0] = (!dz && side_lo[a]) ? __ddiv_rn(__dsub_rn(pl[a][0], o[a]), d[a]) : 0.0;
-      tp[a][1] = !dz ? __ddiv_rn(__dsub_rn(pl[a][1], o[a]), d[a]) : 0.0;
-      tp[a][2] = (!dz && side_hi[a]) ? __ddiv_rn(__dsub_rn(pl[a][2], o[a]), d[a]) : 0.0;
-    }
-    double cte[8];
-    int cc[8];
-    int nc = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      if (!((mask >> c) & 1u)) continue;
-      const int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
-      double t0 = 0.0, t1 = tmax;
-      if (!slab_axis(o[0], d[0], pl[0][bx], pl[0][bx + 1], tp[0][bx], tp[0][bx + 1], t0, t1)) continue;
-      if (!slab_axis(o[1], d[1], pl[1][by], pl[1][by + 1], tp[1][by], tp[1][by + 1], t0, t1)) continue;
-      if (!slab_axis(o[2], d[2], pl[2][bz], pl[2][bz + 1], tp[2][bz], tp[2][bz + 1], t0, t1)) continue;
-      if (t0 > t1) continue;
-      int m = nc - 1;
-      while (m >= 0 && (cte[m] > t0 || (cte[m] == t0 && cc[m] > c))) {
-        cte[m + 1] = cte[m];
-        cc[m + 1] = cc[m];
-        --m;
-      }
-      cte[m + 1] = t0;
-      cc[m + 1] = c;
-      ++nc;
-    }
-    const E lvl = (E)((E)(level + 1) << SC::kShift);
-    for (int j = nc - 1; j >= 0; --j) stack[sp++] = lvl | (E)(code * 8ull + (unsigned long long)cc[j]);
+    expand_node<E>(x, o, d, tmax, level, code, stack, sp);
   }
 }
 
