@@ -237,13 +237,27 @@ def extra_config(args):
     from paper_2211_15460_b200.lights import ImageBuffer, headlight
     from paper_2211_15460_b200.raster import CaptureStrategy, RasterConfig
     from paper_2211_15460_b200.scene import capture_camera, viewpoint_camera
-    dev = torch.device("cuda", 0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("FHV_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
+    if world > 1 and args.config != "C5":
+        raise SystemExit("--config C2 / C4 run on one GPU (C4's PPFL is view-bound: replicas only)")
+    dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    import torch.distributed as dist
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     stream = torch.cuda.current_stream(dev)
     peak, peak_kind = peaks()
     ns = CaptureStrategy.normal_space()
     nt = host_threads()
-    line = {"metric": METRIC, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "vs_baseline": None,
+    line = {"metric": METRIC, "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded, no dataset)", "scaling": "strong", "higher_is_better": True}
 
     def ray_bytes(st, P):  # 16 tested + 8 visited + 20 hits + 32 P
@@ -348,9 +362,11 @@ def extra_config(args):
         scene = sample_scenes.scatter1m()
         cam = capture_camera(scene, "+z", 1080)
         cfg = RasterConfig((1920, 1080), RasterConfig.from_camera(cam).projection, extent=1.0)
+        # views shard across ranks, the FHV replicated
         vol = fhv.pofa_build(scene, ns, cfg, 8, device=dev)
         rcfg = fhv.default_raycast_config(vol)
-        views = sample_scenes.c5_views(64)
+        all_views = sample_scenes.c5_views(64)
+        views = all_views[rank::world]
         W, H = views[0].resolution
         shs = [DeviceShading(scene.materials, [headlight(v)], dev) for v in views]
         buf = img_buf(W, H)
@@ -364,19 +380,26 @@ def extra_config(args):
             return sts
         for _ in range(args.warmup):
             step()
-        with ClockSampler(0) as clk:
+        if world > 1:
+            dist.barrier()
+        with ClockSampler(local) as clk:
             ms, sts = _timed(step, args.steps, stream)
+        if world > 1:  # max over ranks, on the device clock
+            t = torch.tensor([ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
         tot = torch.stack(sts).sum(0).cpu().tolist()
         stats = fhv.RaycastStats(*tot)
         stage, _ = _stage_profile(step, 1, dev)
         P = W * H * len(views)
-        rb = ray_bytes(stats, P)  # per step (64 views)
+        rb = ray_bytes(stats, P)  # per step (this rank's views)
         t_ray = stage.get("raycast", ms)
-        line.update({"value": len(views) / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms,
-                     "rays_per_s": P / (ms / 1e3),
+        line.update({"value": len(all_views) / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms,
+                     "rays_per_s": W * H * len(all_views) / (ms / 1e3),
                      "config": {"workload": "C5: 64 x 3840x2160 perspective ray-cast views (Fibonacci sphere, "
                                             "distance 1.5, fov 45) of C3's POFA (scatter1M, L=8)",
-                                "fragments": vol.pool.next_free, "views": len(views), "parallelism": "single"},
+                                "fragments": vol.pool.next_free, "views": len(all_views),
+                                "parallelism": f"views sharded x{world}, FHV replicated" if world > 1 else "single"},
                      "raycast_stats": stats.as_dict(),
                      "stage_ms": {k: round(v, 4) for k, v in stage.items()},
                      "roofline": {"bound": "hbm", "kernel": "raycast", "achieved": round(rb / (t_ray / 1e3) / 1e9, 1),
@@ -384,7 +407,7 @@ def extra_config(args):
                                   "traffic": None, "algorithmic_bytes": rb, "peak_kind": peak_kind,
                                   "note": "latency/divergence bound (f64 slab DFS), see profiles/"},
                      "clocks": clk.summary()})
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and rank == 0 and world == 1:
             from oracle import oracle as orc
             ref = orc.pofa_build(scene, ns, cfg, 8)
             band = (1040, 1120)  # 80 of 2160 rows of view 0, scaled x27 x64
@@ -396,7 +419,10 @@ def extra_config(args):
                                     "sample": f"rows {band} of one 4K view (1 thread), scaled to a full view: "
                                               f"{dt:.2f} s per view"}
     line["gpu_launches_total"] = _lib.launches(dev)
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
