@@ -385,6 +385,22 @@ struct TriData {
   uint32_t mat, obj;
 };
 
+__device__ __forceinline__ void prefetch_l1(const void* a) { asm volatile("prefetch.global.L1 [%0];" ::"l"(a)); }
+
+// pull a triangle's records (positions, vertex + face normals, ids) toward L1
+// ahead of the fragments that read them
+__device__ __forceinline__ void prefetch_tri(const CaptureParams& p, uint32_t tri) {
+  const char* P = reinterpret_cast<const char*>(p.pos + 9 * (long long)tri);
+  const char* N = reinterpret_cast<const char*>(p.vnrm + 9 * (long long)tri);
+  prefetch_l1(P);
+  prefetch_l1(P + 64);
+  prefetch_l1(N);
+  prefetch_l1(N + 64);
+  prefetch_l1(p.fnrm + 3 * (long long)tri);
+  prefetch_l1(p.mat + tri);
+  prefetch_l1(p.obj + tri);
+}
+
 __device__ __forceinline__ void load_tri_pos(const CaptureParams& p, uint32_t tri, uint32_t swapped, TriData& d) {
   const double* P = p.pos + 9 * (long long)tri;
   const int o[3] = {0, swapped ? 2 : 1, swapped ? 1 : 2};
@@ -705,6 +721,11 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
       const uint32_t p0 = item_p0[item];
       const unsigned long long pe = (unsigned long long)js.bw * (unsigned long long)js.bh;
       npix = (unsigned long long)p0 + kItemPix < pe ? kItemPix : (uint32_t)(pe - p0);
+      if (kMode == kCntLeaves) {  // the positions the keying batches read
+        const char* P = reinterpret_cast<const char*>(p.pos + 9 * (long long)js.tri);
+        prefetch_l1(P);
+        prefetch_l1(P + 64);
+      }
       make_cover(js, p0, cs[lane]);
       ijob[lane] = jid;
       if (!kOwned && kMode != kCnt && !kAtomicAlloc) rank0 = item_off[item];
@@ -718,6 +739,13 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
       k0 = __dmul_rn(c.e0x, __dsub_rn(sy, c.by));
       k1 = __dmul_rn(c.e1x, __dsub_rn(sy, c.cy));
       k2 = __dmul_rn(c.e2x, __dsub_rn(sy, c.ay));
+    }
+    {  // the next group's item records
+      const long long nx = item + nw * 32;
+      if (nx < n_items) {
+        prefetch_l1(item_job + nx);
+        prefetch_l1(item_p0 + nx);
+      }
     }
     own_cnt[lane] = 0;
     __syncwarp();
@@ -861,10 +889,21 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
     unsigned long long rank0 = 0;
     if (item < n_items) {
       const uint32_t jid = item_job[item];
-      make_cover(jobs[jid], item_p0[item], cs[lane]);
-      ijob[lane] = jid;
       mk = item_mask[item];
       if (!kAtomicAlloc) rank0 = item_off[item];
+      const JobSetup js = jobs[jid];
+      if (mk.x | mk.y | mk.z | mk.w) prefetch_tri(p, js.tri);
+      make_cover(js, item_p0[item], cs[lane]);
+      ijob[lane] = jid;
+    }
+    {  // the next group's item records
+      const long long nx = item + nw * 32;
+      if (nx < n_items) {
+        prefetch_l1(item_job + nx);
+        prefetch_l1(item_mask + nx);
+        prefetch_l1(item_p0 + nx);
+        if (!kAtomicAlloc) prefetch_l1(item_off + nx);
+      }
     }
     own_cnt[lane] = 0;
     const uint32_t cnt = (uint32_t)(__popc(mk.x) + __popc(mk.y) + __popc(mk.z) + __popc(mk.w));
