@@ -157,7 +157,8 @@ extern "C" int64_t fhv_ctx_launches(const fhv_ctx* ctx) { return ctx ? ctx->laun
 __global__ void k_selftest_div(long long n, const double* __restrict__ x, const double* __restrict__ d,
                                double* __restrict__ fast, double* __restrict__ ref) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    fast[i] = fhv::div_rn(x[i], fhv::recip_of(d[i]));
+    // odd elements: the zero-dividend shortcut alone; even: the shared-divisor form
+    fast[i] = (i & 1) ? fhv::ddiv_z(x[i], d[i]) : fhv::div_rn(x[i], fhv::recip_of(d[i]));
     ref[i] = __ddiv_rn(x[i], d[i]);
   }
 }

@@ -445,7 +445,7 @@ __device__ __forceinline__ void interp_nrm(const TriData& d, double l0, double l
   const double len = __dsqrt_rn(e021(v[0], v[1], v[2], v[0], v[1], v[2]));
   if (len > 1e-12) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) out[k] = __ddiv_rn(v[k], len);
+    for (int k = 0; k < 3; ++k) out[k] = ddiv_zd(v[k], len);
   } else {
 #pragma unroll
     for (int k = 0; k < 3; ++k) out[k] = d.f[k];
@@ -484,7 +484,7 @@ __device__ __forceinline__ void ds_fragment(const CaptureParams& p, const EmitOu
                                             int px, int py) {
   double f0, f1, f2;
   cover_test(c, px, py, f0, f1, f2);
-  double l0 = __ddiv_rn(f0, c.area2), l1 = __ddiv_rn(f1, c.area2), l2 = __ddiv_rn(f2, c.area2);
+  double l0 = ddiv_zd(f0, c.area2), l1 = ddiv_zd(f1, c.area2), l2 = ddiv_zd(f2, c.area2);
   const JobPersp& jp = p.persp[job];
   const double d = jp.n1 ? fwd3(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]) : g102(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]);
   if (isnan(d)) return;  // np.minimum.at would poison the pixel; no winner either way
@@ -500,7 +500,7 @@ __device__ __forceinline__ void ds_fragment(const CaptureParams& p, const EmitOu
   }
   if (o.ds_win[pix] != job) return;
   if (!p.ortho) {
-    const double lw0 = __ddiv_rn(l0, jp.w[0]), lw1 = __ddiv_rn(l1, jp.w[1]), lw2 = __ddiv_rn(l2, jp.w[2]);
+    const double lw0 = ddiv_z(l0, jp.w[0]), lw1 = ddiv_z(l1, jp.w[1]), lw2 = ddiv_z(l2, jp.w[2]);
     const double sum = __dadd_rn(__dadd_rn(lw0, lw1), lw2);
     const Recip rs = recip_of(sum);
     l0 = div_rn(lw0, rs);
@@ -543,9 +543,9 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   if (valid) {
     double f0, f1, f2;
     cover_test(c, px, py, f0, f1, f2);  // the same f64 values the sweep tested
-    l0 = __ddiv_rn(f0, c.area2);
-    l1 = __ddiv_rn(f1, c.area2);
-    l2 = __ddiv_rn(f2, c.area2);
+    l0 = ddiv_zd(f0, c.area2);
+    l1 = ddiv_zd(f1, c.area2);
+    l2 = ddiv_zd(f2, c.area2);
     load_tri_pos(p, c.tri, c.swapped, d);
     interp_pos(d, l0, l1, l2, w);
     live = true;
@@ -1116,9 +1116,9 @@ __global__ void k_unit_rows(long long n, const double* __restrict__ in, double* 
       out[3 * i] = out[3 * i + 1] = out[3 * i + 2] = 0.0;
       continue;
     }
-    out[3 * i] = __ddiv_rn(a, len);
-    out[3 * i + 1] = __ddiv_rn(b, len);
-    out[3 * i + 2] = __ddiv_rn(c, len);
+    out[3 * i] = ddiv_z(a, len);
+    out[3 * i + 1] = ddiv_z(b, len);
+    out[3 * i + 2] = ddiv_z(c, len);
   }
 }
 

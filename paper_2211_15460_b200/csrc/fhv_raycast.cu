@@ -69,8 +69,8 @@ __device__ __forceinline__ bool slab_box(const double o[3], const double d[3], c
   for (int a = 0; a < 3; ++a) {
     double ta = 0.0, tb = 0.0;
     if (d[a] != 0.0) {
-      ta = __ddiv_rn(__dsub_rn(lo[a], o[a]), d[a]);
-      tb = __ddiv_rn(__dsub_rn(hi[a], o[a]), d[a]);
+      ta = ddiv_z(__dsub_rn(lo[a], o[a]), d[a]);
+      tb = ddiv_z(__dsub_rn(hi[a], o[a]), d[a]);
     }
     if (!slab_axis(o[a], d[a], lo[a], hi[a], ta, tb, t0, t1)) return false;
   }
@@ -202,9 +202,9 @@ __device__ __forceinline__ void expand_node(const RayParams& x, const double o[3
     pl[a][1] = __dadd_rn(lo[a], half);
     pl[a][2] = __dadd_rn(pl[a][1], half);
     const bool dz = d[a] == 0.0;
-    tp[a][0] = (!dz && side_lo[a]) ? __ddiv_rn(__dsub_rn(pl[a][0], o[a]), d[a]) : 0.0;
-    tp[a][1] = !dz ? __ddiv_rn(__dsub_rn(pl[a][1], o[a]), d[a]) : 0.0;
-    tp[a][2] = (!dz && side_hi[a]) ? __ddiv_rn(__dsub_rn(pl[a][2], o[a]), d[a]) : 0.0;
+    tp[a][0] = (!dz && side_lo[a]) ? ddiv_z(__dsub_rn(pl[a][0], o[a]), d[a]) : 0.0;
+    tp[a][1] = !dz ? ddiv_z(__dsub_rn(pl[a][1], o[a]), d[a]) : 0.0;
+    tp[a][2] = (!dz && side_hi[a]) ? ddiv_z(__dsub_rn(pl[a][2], o[a]), d[a]) : 0.0;
   }
   double cte[8];
   int cc[8];
@@ -304,7 +304,7 @@ __device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats
   double v[3] = {__dsub_rn(x.eye[0], p[0]), __dsub_rn(x.eye[1], p[1]), __dsub_rn(x.eye[2], p[2])};
   const double vl = __dsqrt_rn(plain3(v[0], v[1], v[2]));
 #pragma unroll
-  for (int k = 0; k < 3; ++k) v[k] = vl > 0.0 ? __ddiv_rn(v[k], vl) : 0.0;
+  for (int k = 0; k < 3; ++k) v[k] = vl > 0.0 ? ddiv_z(v[k], vl) : 0.0;
   double r = 0.0, g = 0.0, b = 0.0;
   for (int li = 0; li < x.s.n_lights; ++li) {
     double l[3];
@@ -316,12 +316,12 @@ __device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats
       for (int k = 0; k < 3; ++k) l[k] = __dsub_rn(x.s.light_vec[3 * li + k], p[k]);
       const double ll = __dsqrt_rn(plain3(l[0], l[1], l[2]));
 #pragma unroll
-      for (int k = 0; k < 3; ++k) l[k] = ll > 0.0 ? __ddiv_rn(l[k], ll) : 0.0;
+      for (int k = 0; k < 3; ++k) l[k] = ll > 0.0 ? ddiv_z(l[k], ll) : 0.0;
     }
     double h[3] = {__dadd_rn(l[0], v[0]), __dadd_rn(l[1], v[1]), __dadd_rn(l[2], v[2])};
     const double hl = __dsqrt_rn(plain3(h[0], h[1], h[2]));
 #pragma unroll
-    for (int k = 0; k < 3; ++k) h[k] = hl > 0.0 ? __ddiv_rn(h[k], hl) : 0.0;
+    for (int k = 0; k < 3; ++k) h[k] = hl > 0.0 ? ddiv_z(h[k], hl) : 0.0;
     double ndl = __dadd_rn(__dadd_rn(__dmul_rn(n[0], l[0]), __dmul_rn(n[1], l[1])), __dmul_rn(n[2], l[2]));
     if (ndl < 0.0) ndl = 0.0;
     double ndh = __dadd_rn(__dadd_rn(__dmul_rn(n[0], h[0]), __dmul_rn(n[1], h[1])), __dmul_rn(n[2], h[2]));
@@ -350,8 +350,8 @@ __device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats
 // primary_rays (fhv/raycast.py:148-172), elementwise numpy semantics
 __device__ __forceinline__ void camera_ray(const RayParams& x, long long k, double o[3], double d[3]) {
   const long long iy = k / x.W, ix = k - iy * x.W;
-  const double nx = __dsub_rn(__dmul_rn(__ddiv_rn(__dadd_rn((double)ix, 0.5), (double)x.W), 2.0), 1.0);
-  const double ny = __dsub_rn(1.0, __dmul_rn(__ddiv_rn(__dadd_rn((double)iy, 0.5), (double)x.H), 2.0));
+  const double nx = __dsub_rn(__dmul_rn(ddiv_z(__dadd_rn((double)ix, 0.5), (double)x.W), 2.0), 1.0);
+  const double ny = __dsub_rn(1.0, __dmul_rn(ddiv_z(__dadd_rn((double)iy, 0.5), (double)x.H), 2.0));
   if (!x.persp) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
