@@ -561,7 +561,10 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
     }
   }
   uint32_t local = push_local;
-  if (kOwned) {
+  // owned-fragment numbering only matters for a shard (a sub-range of the
+  // leaves): over the whole directory every covered fragment is owned
+  const bool whole = p.cell_lo == 0 && p.cell_hi >= (1ull << (3 * o.levels));
+  if (kOwned && !whole) {
     const unsigned m = __ballot_sync(0xffffffffu, live);
     const unsigned grp = __match_any_sync(0xffffffffu, valid ? k : -1);
     local = own_cnt[k] + (uint32_t)__popc(grp & m & below);
@@ -825,7 +828,8 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
     __syncwarp();
     if (item < n_items) {
       if (kMode == kCnt) item_cnt[item] = covered;
-      if (kMode == kCntLeaves) item_cnt[item] = own_cnt[lane];
+      if (kMode == kCntLeaves)
+        item_cnt[item] = (p.cell_lo == 0 && p.cell_hi >= (1ull << (3 * o.levels))) ? covered : own_cnt[lane];
       item_mask[item] = make_uint4(mw0, mw1, mw2, mw3);
     }
     __syncwarp();
