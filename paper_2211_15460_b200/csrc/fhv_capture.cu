@@ -894,7 +894,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
     if (item < n_items) {
       const uint32_t jid = item_job[item];
       mk = item_mask[item];
-      if (!kAtomicAlloc) rank0 = item_off[item];
+      if (!kAtomicAlloc && (kMode != kPofa || (o.flags & FHV_EXACT_ORDER))) rank0 = item_off[item];
       const JobSetup js = jobs[jid];
       if (mk.x | mk.y | mk.z | mk.w) prefetch_tri(p, js.tri);
       make_cover(js, item_p0[item], cs[lane]);
@@ -906,7 +906,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
         prefetch_l1(item_job + nx);
         prefetch_l1(item_mask + nx);
         prefetch_l1(item_p0 + nx);
-        if (!kAtomicAlloc) prefetch_l1(item_off + nx);
+        if (!kAtomicAlloc && (kMode != kPofa || (o.flags & FHV_EXACT_ORDER))) prefetch_l1(item_off + nx);
       }
     }
     own_cnt[lane] = 0;
@@ -1355,7 +1355,8 @@ int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s, bool allow_spec =
 inline const unsigned long long* items_dev(fhv_ctx* ctx) { return ctx->spec ? &ctx->ctl->items_total : nullptr; }
 
 // counts per item (+ leaf histogram) and their scan (fragment ranks); async
-int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_t* leaf_counts, cudaStream_t s) {
+int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_t* leaf_counts, cudaStream_t s,
+          bool ranks = true) {
   const long long n = ctx->n_items;
   uint32_t* item_cnt = (uint32_t*)scratch(ctx, kItemCnt, (size_t)(n > 0 ? n : 1) * 4);
   auto* item_off = (unsigned long long*)scratch(ctx, kItemOff, (size_t)(n > 0 ? n : 1) * 8);
@@ -1383,6 +1384,9 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
     int rc = check_cuda(ctx, cudaGetLastError());
     if (rc) return rc;
   }
+  // item fragment offsets = emission ranks; a POFA build that keeps no
+  // emission order (atomic in-leaf order) needs neither them nor their total
+  if (!ranks) return FHV_OK;
   return scan_u32_to_u64(ctx, item_cnt, item_off, n, s, nd);
 }
 
@@ -1587,15 +1591,17 @@ namespace {
 // item scan's total is parked in ctl->frags_total for the caller's next sync
 int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
                      const fhv_shard_t* shard, uint32_t* counts_local, cudaStream_t s, CaptureParams& p,
-                     bool spec = false) {
+                     bool spec = false, bool ranks = true) {
   ctx->pass1_levels = -1;
+  ctx->pass1_ranks = ranks;
   int rc;
   if ((rc = reset_control(ctx, s))) return rc;
   if ((rc = shard_params(ctx, tris, cfg, levels, shard, true, p, s))) return rc;
   const unsigned long long n_local = p.cell_hi - p.cell_lo;
   if ((rc = plan(ctx, p, s, spec))) return rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(counts_local, 0, (size_t)n_local * 4, s)))) return rc;
-  if ((rc = count(ctx, p, true, levels, counts_local, s))) return rc;
+  if ((rc = count(ctx, p, true, levels, counts_local, s, ranks))) return rc;
+  if (!ranks) return FHV_OK;  // the total comes from the directory scan (caller)
   return check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total, sizeof(unsigned long long),
                                          cudaMemcpyDeviceToDevice, s));
 }
@@ -1694,6 +1700,7 @@ extern "C" int fhv_pofa_shard_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, cons
   if (ctx->pass1_levels != levels || ctx->pass1_tris != tris->n_tri || ctx->pass1_lo != lo || ctx->pass1_hi != hi)
     return FHV_BAD_ARGS;
   if (pool->capacity < ctx->pass1_total) return FHV_BAD_ARGS;
+  if ((flags & FHV_EXACT_ORDER) && !ctx->pass1_ranks) return FHV_BAD_ARGS;  // pass 1 skipped the ranks
   cudaStream_t s = (cudaStream_t)stream;
   CaptureParams p;
   if ((rc = shard_params(ctx, tris, cfg, levels, shard, false, p, s))) return rc;
@@ -1737,9 +1744,14 @@ extern "C" int fhv_pofa_build(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_ca
   // pass 1, directory and (into the caller's pool, sized by its guess) pass 2
   // are enqueued back to back; the only wait is the final sync -- unless the
   // speculative item plan turns out too small, then once more with an exact plan
+  const bool ranks = (flags & FHV_EXACT_ORDER) != 0;  // emission ranks only for the exact in-leaf order
   for (int attempt = 0; attempt < 2; ++attempt) {
-    if ((rc = pofa_count_async(ctx, tris, cfg, levels, nullptr, counts, s, p, attempt == 0))) return rc;
+    if ((rc = pofa_count_async(ctx, tris, cfg, levels, nullptr, counts, s, p, attempt == 0, ranks))) return rc;
     if ((rc = fhv_pofa_shard_directory_nocheck(ctx, levels, counts, offsets, pyramid, s))) return rc;
+    if (!ranks &&
+        (rc = check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total,
+                                              sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s))))
+      return rc;
     if (pool && pool->capacity > 0 &&
         (rc = pofa_scatter_async(ctx, p, levels, 0, n_leaves, counts, offsets, 0, pool, flags, s)))
       return rc;

@@ -65,6 +65,7 @@ struct fhv_ctx {
   // state carried from fhv_pofa_count to fhv_pofa_scatter
   int64_t n_jobs = 0, n_items = 0, pass1_total = 0;
   int32_t pass1_levels = -1;
+  bool pass1_ranks = true;  // pass 1 scanned emission ranks (needed by an EXACT_ORDER scatter)
   int64_t pass1_tris = -1;
   uint64_t pass1_lo = 0, pass1_hi = 0;
   int64_t n_binned = -1;  // triangles kept by the last shard binning (-1: no binning)
