@@ -140,28 +140,40 @@ __device__ bool leaf_hits(const RayParams& x, long long code, const double o[3],
     if (nb < kHitBuf) ++nb;
   });
   st.tested += tested;
-  for (int q = 0; q < nb; ++q)
-    if (!visit(bt[q], bi[q])) return false;
-  if (nh <= kHitBuf) return true;
-  // exact fallback: repeatedly select the next (t, idx) after the last one
-  double lt = bt[kHitBuf - 1];
-  long long li = bi[kHitBuf - 1];
-  for (long long done = kHitBuf; done < nh; ++done) {
-    double mt = 0.0;
-    long long mi = -1;
-    for_leaf(x, code, [&](long long k) {
-      double t;
-      if (!hit_test(x, k, o, d, tmin, tmax, &t)) return;
-      if (!hit_less(lt, li, t, k)) return;
-      if (mi < 0 || hit_less(t, k, mt, mi)) {
-        mt = t;
-        mi = k;
-      }
-    });
-    if (mi < 0) break;
-    if (!visit(mt, mi)) return false;
-    lt = mt;
-    li = mi;
+  // deliver the hits in (t, index) order through ONE call site of visit (the
+  // shading is inlined once): the buffered ones, then -- only for leaves with
+  // more than kHitBuf hits -- an exact rescan selecting the next one each time
+  double lt = 0.0;
+  long long li = -1, delivered = 0;
+  for (int q = 0;; ) {
+    double ct;
+    long long ci;
+    if (q < nb) {
+      ct = bt[q];
+      ci = bi[q];
+      ++q;
+    } else if (delivered < nh) {
+      double mt = 0.0;
+      long long mi = -1;
+      for_leaf(x, code, [&](long long k) {
+        double t;
+        if (!hit_test(x, k, o, d, tmin, tmax, &t)) return;
+        if (!hit_less(lt, li, t, k)) return;
+        if (mi < 0 || hit_less(t, k, mt, mi)) {
+          mt = t;
+          mi = k;
+        }
+      });
+      if (mi < 0) break;
+      ct = mt;
+      ci = mi;
+    } else {
+      break;
+    }
+    if (!visit(ct, ci)) return false;
+    lt = ct;
+    li = ci;
+    ++delivered;
   }
   return true;
 }
