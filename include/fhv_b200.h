@@ -245,8 +245,10 @@ typedef struct {
    depth keys into the owners' slabs (synchronises; extent[2] = max
    footprint, the caller all-reduces it for the 4096-pixel check), 2 = winner
    candidates, 3 = shade the winners it owns and store them (and, for its own
-   slab, the background) into every rank's frame.  Between phases every rank
-   must have finished the previous one (caller's barrier). */
+   slab, the background) into every rank's frame; 4 = probe: extent (a
+   DEVICE array of nranks int64) <- the first winner word of every rank's
+   slab, read through the peer mappings.  Between phases every rank must
+   have finished the previous one (caller's barrier). */
 int fhv_splat_peer(fhv_ctx *ctx, int32_t phase, int64_t n, const float *pos, const float *nrm, const uint32_t *mat,
                    const double *cam, double radius, const fhv_shading_t *shading, const double *background,
                    const fhv_peer_t *peers, int32_t rank, int64_t index_base, int64_t *extent, void *stream);

@@ -399,6 +399,25 @@ class PeerFrame:
         for r in range(N):
             st.keys[r], st.winners[r], st.rgba[r], st.depth[r] = ptrs[r]
         self.struct = st
+        self._probe(comm, device)
+
+    def _probe(self, comm: Comm, device) -> None:
+        """Each rank stamps its slab, every rank reads all stamps back through
+        its peer mappings: raises if a mapping does not reach its buffer."""
+        N = comm.world
+        self.winners[0] = 1000 + comm.rank
+        comm.barrier()
+        out = torch.zeros(N, dtype=torch.int64, device=device)
+        lib = _lib.load()
+        cam = np.zeros(22)
+        cam[13], cam[14] = self.width, self.height
+        rc = lib.fhv_splat_peer(_lib.ctx(device), 4, 0, None, None, None, cam.ctypes.data, 1.0, None, None,
+                                self.struct, comm.rank, 0, ctypes.c_void_p(out.data_ptr()), _lib.stream_ptr(device))
+        _lib.check(rc, "peer probe")
+        got = out.cpu().tolist()
+        comm.barrier()
+        if got != [1000 + r for r in range(N)]:
+            raise FhvError(f"peer mappings do not reach the peers' buffers: {got}")
 
 
 def _splat_peer(vol, camera, splat_radius_world, comm, background, out, shading, peer):
