@@ -172,6 +172,21 @@ int fhv_capture_list(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg
                      int64_t max_out, int64_t *job, int32_t *px, int32_t *py, double *wpos,
                      double *wnrm, int64_t *n_out, void *stream);
 
+/* fhv_capture_list plus FragmentBatch.depth per fragment (capture_pass,
+   fhv/raster.py:204,240: screen strategies lam @ ndc_z, normal_space 0.5). */
+int fhv_capture_list_depth(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg,
+                           int64_t max_out, int64_t *job, int32_t *px, int32_t *py, double *wpos,
+                           double *wnrm, double *depth, int64_t *n_out, void *stream);
+
+/* rasterize_triangle / _raster_screen (fhv/raster.py:184-209, 245-252) for
+   every triangle through one 4x4 row-major projection (orthographic or
+   perspective, RasterConfig.projection) into width x height: fragments in
+   (triangle, y, x) order, job[] = triangle index, perspective-correct
+   interpolation, depth = lam @ ndc_z.  Synchronises. */
+int fhv_raster_screen(fhv_ctx *ctx, const fhv_tris_t *tris, const double *proj, int32_t width,
+                      int32_t height, int64_t max_out, int64_t *job, int32_t *px, int32_t *py,
+                      double *wpos, double *wnrm, double *depth, int64_t *n_out, void *stream);
+
 /* build_ppfl: heads[W*H] and pool->prev must be pre-filled with -1 by the
    caller; width = PixelDirectory.width.  *next_free = fragments emitted
    (FragmentPool.next_free).  Synchronises.  Returns FHV_OVERFLOW if
@@ -351,6 +366,85 @@ int fhv_raycast_image(fhv_ctx *ctx, int64_t start, int64_t end, const double *or
 
 /* make_triangle face normals for a bulk scene (fhv/scene.py:137-139). Async. */
 int fhv_face_normals(fhv_ctx *ctx, int64_t n_tri, const double *pos, double *fnrm, void *stream);
+
+/* ---- the reference's operator API, kernels() (fhv/_backend.py:25-29), batched ----
+   coverage (fhv/_ckern.pyx:25-105) of n raster-space triangles v6[n][6] =
+   (ax, ay, bx, by, cx, cy) on rasters wh[n][2] = (w, h): covered pixel
+   centres per triangle in row-major order at tri_off[t] .. tri_off[t+1]
+   (tri_off: n+1 int64, device), barycentrics l0/l1/l2 = f_i / area2.
+   Triangles with area2 <= 0 (or non-finite) emit nothing and *first_bad =
+   the first such index (the reference raises ValueError), else -1.
+   max_out bounds the outputs, *n_out = total.  Synchronises. */
+int fhv_op_coverage(fhv_ctx *ctx, int64_t n, const double *v6, const int32_t *wh, int64_t max_out,
+                    int64_t *tri_off, int32_t *px, int32_t *py, double *l0, double *l1, double *l2,
+                    int64_t *n_out, int64_t *first_bad, void *stream);
+/* linked_insert (fhv/_ckern.pyx:112-123): for i in order, prev[start+i] =
+   heads[keys[i]]; heads[keys[i]] = start+i.  Keys outside [0, n_keys) ->
+   FHV_BAD_ARGS before any write.  Synchronises. */
+int fhv_op_linked_insert(fhv_ctx *ctx, int64_t n, const int64_t *keys, int64_t n_keys, int32_t *heads,
+                         int32_t *prev, int64_t prev_len, int64_t start, void *stream);
+/* pofa_scatter (fhv/_ckern.pyx:126-143): dest[i] = offsets[c] + cursors[c]++
+   in order; stops at the first i whose cursor reaches counts[c] (*bad = i,
+   else -1).  Synchronises. */
+int fhv_op_pofa_scatter(fhv_ctx *ctx, int64_t n, const int64_t *codes, int64_t n_leaves,
+                        const uint32_t *offsets, const uint32_t *counts, uint32_t *cursors, int64_t *dest,
+                        int64_t *bad, void *stream);
+
+/* OccupancyPyramid.set_paths (fhv/storage.py:294-301): OR the root paths of
+   n leaf codes (< 8^levels, else FHV_BAD_ARGS) into the concatenated
+   pyramid.  Synchronises. */
+int fhv_set_paths(fhv_ctx *ctx, int32_t levels, int64_t n, const int64_t *codes, uint8_t *pyramid,
+                  void *stream);
+/* OccupancyPyramid.from_leaf_occupancy (fhv/storage.py:316-328): occupied
+   u8[8^levels] (nonzero = occupied) -> every pyramid level.  Async. */
+int fhv_pyramid_from_occupancy(fhv_ctx *ctx, int32_t levels, const uint8_t *occupied, uint8_t *pyramid,
+                               void *stream);
+
+/* chain_indices (fhv/storage.py:480-488): the pool indices of one linked
+   list (heads[key], then prev[]), most recent first; up to cap into out,
+   *n_out = length.  Synchronises. */
+int fhv_chain_indices(fhv_ctx *ctx, const int32_t *heads, int64_t n_keys, const int32_t *prev,
+                      int64_t prev_len, int64_t key, int64_t cap, int64_t *out, int64_t *n_out, void *stream);
+
+/* ---- scalar queries (fhv/raycast.py:205-453, fhv/render.py:120-166) ----
+   shade_many: n f64 points / normals, int64 material ids (< n_materials,
+   checked by the caller), out_rgb [n][3].  Async. */
+int fhv_shade(fhv_ctx *ctx, int64_t n, const double *points, const double *normals,
+              const int64_t *material_id, int64_t n_materials, const fhv_shading_t *shading,
+              const double *eye, double *out_rgb, void *stream);
+/* project_points (fhv/render.py:211-233): n device f64 points through the
+   camera scalars (as fhv_splat's cam): raster x, y, depth, view distance zc
+   [n] each.  Async. */
+int fhv_project_points(fhv_ctx *ctx, int64_t n, const double *points, const double *cam, double *xr,
+                       double *yr, double *depth, double *zc, void *stream);
+/* raycast_pixel (mode 0..2) / gather_ray_hits (mode 3) for n rays (device
+   origins/dirs [n][3], optional tmin/tmax [n]; eye NULL = each ray's
+   origin).  Per ray: out_rgba [n][4] (NULL allowed for mode 3), up to
+   hit_cap hits (t, pool index, leaf) in traversal order, hit_n = hits found
+   (> hit_cap: call again with more room), stats [n][4] RaycastStats.  Async. */
+int fhv_ray_probe(fhv_ctx *ctx, int64_t n, const double *origins, const double *dirs, const double *tmin,
+                  const double *tmax, const fhv_volume_t *vol, const fhv_shading_t *shading,
+                  const double *eye, const double *background, double radius, double cutoff, int32_t mode,
+                  double shadow_eps, int64_t hit_cap, double *out_rgba, double *hit_t, int64_t *hit_idx,
+                  int64_t *hit_leaf, int64_t *hit_n, int64_t *stats, void *stream);
+/* shadow_transmittance toward light `light` of the shading table for n
+   device points; exclude_obj / exclude_cell [n] (-1 = none, NULL = none).
+   tau [n], stats [n][4].  Async. */
+int fhv_transmittance(fhv_ctx *ctx, int64_t n, const double *points, int32_t light,
+                      const int64_t *exclude_obj, const int64_t *exclude_cell, const fhv_volume_t *vol,
+                      const fhv_shading_t *shading, double radius, double shadow_eps, double *tau,
+                      int64_t *stats, void *stream);
+/* traverse_octree: occupied leaves along one ray (device origin/dir [3]),
+   nearest entry first, with t_enter / t_exit; up to cap, *n_out (device) =
+   total.  Async. */
+int fhv_leaf_order(fhv_ctx *ctx, int32_t levels, const uint8_t *pyramid, const double *origin,
+                   const double *dir, double tmin, double tmax, int64_t cap, int64_t *code_out,
+                   double *te_out, double *tx_out, int64_t *n_out, void *stream);
+/* intersect_fragment for n device points against one ray (host origin/dir):
+   t_out [n], hit [n] (1 = within [tmin, tmax] and radius).  Async. */
+int fhv_intersect_points(fhv_ctx *ctx, int64_t n, const double *points, const double *origin,
+                         const double *dir, double tmin, double tmax, double radius, double *t_out,
+                         int8_t *hit, void *stream);
 
 #ifdef __cplusplus
 }

@@ -382,3 +382,65 @@ def rebuild_pofl_as_pofa(vol):
     return {"layout": "POFA", "pool": pool, "offsets": offsets, "counts": counts,
             "pyramid": pyramid_from_occupancy(counts > 0, L), "levels": L, "next_free": n, "capacity": n,
             "overflowed": False, "capture_resolution": vol["capture_resolution"]}
+
+
+# ---------------------------------------------------------------------------
+# the reference's operator module, restated as plain Python loops (small
+# cases only; checked against tests/golden/scalar.npz)
+
+
+def coverage(ax, ay, bx, by, cx, cy, w, h):
+    """coverage (fhv/_ckern.pyx:25-105 == fhv/_kernels_py.py:17-66): covered
+    pixel centres in row-major order with barycentrics f_i / area2."""
+    import math
+    area2 = (bx - ax) * (cy - ay) - (by - ay) * (cx - ax)
+    if area2 <= 0.0:
+        raise ValueError("coverage() requires positively wound vertices")
+    x0 = max(0, math.ceil(min(ax, bx, cx) - 0.5))
+    x1 = min(w - 1, math.floor(max(ax, bx, cx) - 0.5))
+    y0 = max(0, math.ceil(min(ay, by, cy) - 0.5))
+    y1 = min(h - 1, math.floor(max(ay, by, cy) - 0.5))
+    d0x, d0y, d1x, d1y, d2x, d2y = cx - bx, cy - by, ax - cx, ay - cy, bx - ax, by - ay
+    tl = [d0y < 0.0 or (d0y == 0.0 and d0x > 0.0), d1y < 0.0 or (d1y == 0.0 and d1x > 0.0),
+          d2y < 0.0 or (d2y == 0.0 and d2x > 0.0)]
+    px, py, lam = [], [], []
+    for y in range(y0, y1 + 1):
+        sy = y + 0.5
+        for x in range(x0, x1 + 1):
+            sx = x + 0.5
+            f = (d0x * (sy - by) - d0y * (sx - bx), d1x * (sy - cy) - d1y * (sx - cx),
+                 d2x * (sy - ay) - d2y * (sx - ax))
+            if all(fi > 0.0 or (fi == 0.0 and t) for fi, t in zip(f, tl)):
+                px.append(x)
+                py.append(y)
+                lam.append([fi / area2 for fi in f])
+    return (np.array(px, np.int32), np.array(py, np.int32), np.array(lam, np.float64).reshape(-1, 3))
+
+
+def linked_insert(keys, heads, prev, start) -> None:
+    """linked_insert (fhv/_ckern.pyx:112-123), in place."""
+    idx = int(start)
+    for k in np.asarray(keys).tolist():
+        prev[idx] = heads[k]
+        heads[k] = idx
+        idx += 1
+
+
+def pofa_scatter(codes, offsets, counts, cursors, dest) -> int:
+    """pofa_scatter (fhv/_ckern.pyx:126-143), in place; -1 or the first bad index."""
+    for i, c in enumerate(np.asarray(codes).tolist()):
+        cur = int(cursors[c])
+        if cur >= int(counts[c]):
+            return i
+        dest[i] = int(offsets[c]) + cur
+        cursors[c] = cur + 1
+    return -1
+
+
+def set_paths(pyramid_levels, codes, L) -> None:
+    """OccupancyPyramid.set_paths (fhv/storage.py:294-301) on a list of level arrays."""
+    for code in np.asarray(codes).tolist():
+        for k in range(L):
+            node = code >> (3 * (L - k))
+            child = (code >> (3 * (L - k - 1))) & 7
+            pyramid_levels[k][node] |= np.uint8(1 << child)

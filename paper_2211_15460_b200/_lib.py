@@ -109,6 +109,26 @@ _SIGS = {
     "fhv_deferred": (ctypes.c_int, [c_vp, _P(Tris), c_vp, c_i32, c_i32, c_vp, _P(Shading), c_vp, c_vp, c_vp,
                                     _P(GBuf), _P(c_i64), c_vp]),
     "fhv_face_normals": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "fhv_capture_list_depth": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                              c_vp, _P(c_i64), c_vp]),
+    "fhv_raster_screen": (ctypes.c_int, [c_vp, _P(Tris), c_vp, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                         c_vp, _P(c_i64), c_vp]),
+    "fhv_op_coverage": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                       _P(c_i64), _P(c_i64), c_vp]),
+    "fhv_op_linked_insert": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp]),
+    "fhv_op_pofa_scatter": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, _P(c_i64), c_vp]),
+    "fhv_chain_indices": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, _P(c_i64), c_vp]),
+    "fhv_set_paths": (ctypes.c_int, [c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
+    "fhv_pyramid_from_occupancy": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "fhv_project_points": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "fhv_shade": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, _P(Shading), c_vp, c_vp, c_vp]),
+    "fhv_ray_probe": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, _P(Volume), _P(Shading), c_vp, c_vp,
+                                     c_f64, c_f64, c_i32, c_f64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "fhv_transmittance": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, _P(Volume), _P(Shading), c_f64,
+                                         c_f64, c_vp, c_vp, c_vp]),
+    "fhv_leaf_order": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_f64, c_f64, c_i64, c_vp, c_vp, c_vp, c_vp,
+                                      c_vp]),
+    "fhv_intersect_points": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_f64, c_f64, c_f64, c_vp, c_vp, c_vp]),
 }
 EXPORTED = tuple(_SIGS)
 

@@ -20,7 +20,9 @@ __all__ = ["capture_fragments", "capture_pass"]
 
 
 def capture_fragments(scene, strategy: CaptureStrategy, cfg: RasterConfig, max_out: int | None = None,
-                      device=None) -> dict:
+                      device=None, depth: bool = False) -> dict:
+    """``depth=True`` adds FragmentBatch.depth per fragment (screen
+    strategies: lam @ ndc_z, fhv/raster.py:204; normal_space: 0.5)."""
     plan = capture_plan(scene, strategy, cfg)
     ds = device_scene(scene, device)
     dev = ds.device
@@ -37,19 +39,23 @@ def capture_fragments(scene, strategy: CaptureStrategy, cfg: RasterConfig, max_o
     py = torch.empty(max_out, dtype=torch.int32, device=dev)
     wpos = torch.empty((max_out, 3), dtype=torch.float64, device=dev)
     wnrm = torch.empty((max_out, 3), dtype=torch.float64, device=dev)
-    rc = lib.fhv_capture_list(cx, tris, c, max_out, _lib.ptr(job), _lib.ptr(px), _lib.ptr(py), _lib.ptr(wpos),
-                              _lib.ptr(wnrm), n, st)
+    dep = torch.empty(max_out, dtype=torch.float64, device=dev) if depth else None
+    rc = lib.fhv_capture_list_depth(cx, tris, c, max_out, _lib.ptr(job), _lib.ptr(px), _lib.ptr(py), _lib.ptr(wpos),
+                                    _lib.ptr(wnrm), _lib.ptr(dep), n, st)
     _lib.check(rc, "capture_fragments")
     total = int(n.value)
     k = min(total, max_out)
-    return {"job": job[:k], "raster_x": px[:k], "raster_y": py[:k], "world_position": wpos[:k],
-            "world_normal": wnrm[:k], "stats": plan.stats(total), "plan": plan}
+    out = {"job": job[:k], "raster_x": px[:k], "raster_y": py[:k], "world_position": wpos[:k],
+           "world_normal": wnrm[:k], "stats": plan.stats(total), "plan": plan}
+    if depth:
+        out["depth"] = dep[:k]
+    return out
 
 
 def capture_pass(scene, strategy: CaptureStrategy, cfg: RasterConfig, sink, threads: int = 1,
                  device=None) -> CaptureStats:
     """Reference-compatible capture_pass: device rasterisation, host sink calls."""
-    out = capture_fragments(scene, strategy, cfg, device=device)
+    out = capture_fragments(scene, strategy, cfg, device=device, depth=True)
     plan = out["plan"]
     job = out["job"].cpu().numpy()
     if len(job):
@@ -57,6 +63,7 @@ def capture_pass(scene, strategy: CaptureStrategy, cfg: RasterConfig, sink, thre
         py = out["raster_y"].cpu().numpy()
         wp = out["world_position"].cpu().numpy()
         wn = out["world_normal"].cpu().numpy()
+        dp = out["depth"].cpu().numpy()
         cuts = np.flatnonzero(np.diff(job)) + 1
         starts = np.concatenate(([0], cuts))
         ends = np.concatenate((cuts, [len(job)]))
@@ -64,7 +71,6 @@ def capture_pass(scene, strategy: CaptureStrategy, cfg: RasterConfig, sink, thre
         for s, e in zip(starts, ends):
             j = int(job[s])
             t = j % T if plan.strategy == 1 else (j // 3 if plan.strategy == 2 else j)
-            depth = np.full(e - s, 0.5) if plan.strategy == 3 else np.full(e - s, np.nan)
-            sink(FragmentBatch(px[s:e], py[s:e], wp[s:e], wn[s:e], depth, int(scene.material_id[t]),
+            sink(FragmentBatch(px[s:e], py[s:e], wp[s:e], wn[s:e], dp[s:e], int(scene.material_id[t]),
                                int(scene.object_id[t])))
     return out["stats"]

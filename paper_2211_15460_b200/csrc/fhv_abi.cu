@@ -81,7 +81,7 @@ LaunchScope::~LaunchScope() {
 static const char* kStageNames[kNumStages] = {
     "job_setup", "scan", "item_expand", "count", "count_leaves", "emit_list", "emit_ppfl", "emit_pofl",
     "emit_pofa", "chain_order", "leaf_order", "scan_leaves", "pyramid", "splat_depth", "splat_index",
-    "splat_resolve", "raycast", "face_normals", "deferred"};
+    "splat_resolve", "raycast", "face_normals", "deferred", "ops", "scalar"};
 
 }  // namespace fhv
 

@@ -92,6 +92,7 @@ struct EmitOut {
   int32_t* py;
   double* wpos;
   double* wnrm;
+  double* depth;  // list mode: FragmentBatch.depth (screen: lam @ ndc_z; tangent: 0.5), or null
   int flags;
   // deferred_baseline (kScreen): per-pixel depth keys, winning job, G-buffer
   unsigned long long* ds_key;
@@ -169,7 +170,7 @@ __device__ __forceinline__ void setup_screen(const CaptureParams& p, long long j
     const double c1 = __dadd_rn(fwd3(X, Y, Z, M[4], M[5], M[6]), M[7]);
     const double c3 = __dadd_rn(fwd3(X, Y, Z, M[12], M[13], M[14]), M[15]);
     const Recip r3 = recip_of(c3);
-    if (p.strategy == kScreen) {
+    if (p.persp) {  // the deferred pass, or a list capture that reports depth
       const double c2 = __dadd_rn(fwd3(X, Y, Z, M[8], M[9], M[10]), M[11]);
       nz[i] = div_rn(c2, r3);
       cw[i] = c3;
@@ -185,7 +186,7 @@ __device__ __forceinline__ void setup_screen(const CaptureParams& p, long long j
     return;
   }
   finish_setup(xr, yr, p.width, p.height, js);
-  if (p.strategy == kScreen) {
+  if (p.persp) {
     JobPersp jp;
     const int o1 = js.swapped ? 2 : 1, o2 = js.swapped ? 1 : 2;
     jp.w[0] = cw[0]; jp.w[1] = cw[o1]; jp.w[2] = cw[o2];
@@ -521,6 +522,28 @@ __device__ __forceinline__ void ds_fragment(const CaptureParams& p, const EmitOu
   o.gb.object_id[pix] = (int32_t)td.obj;
 }
 
+// list mode with depth (FragmentBatch.depth): _raster_screen's depth =
+// lam @ ndc_z over the winding-ordered vertices (gemv: G102, FWD for a
+// one-fragment batch), then -- perspective only -- lam / w renormalised
+// before interpolation (fhv/raster.py:204-208); _raster_tangent's is 0.5
+__device__ __forceinline__ void list_depth(const CaptureParams& p, uint32_t job, double& l0, double& l1, double& l2,
+                                           double& dep) {
+  if (p.strategy == 3) {
+    dep = 0.5;
+    return;
+  }
+  const JobPersp& jp = p.persp[job];
+  dep = jp.n1 ? fwd3(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]) : g102(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]);
+  if (!p.ortho) {
+    const double lw0 = ddiv_z(l0, jp.w[0]), lw1 = ddiv_z(l1, jp.w[1]), lw2 = ddiv_z(l2, jp.w[2]);
+    const double sum = __dadd_rn(__dadd_rn(lw0, lw1), lw2);
+    const Recip rs = recip_of(sum);
+    l0 = div_rn(lw0, rs);
+    l1 = div_rn(lw1, rs);
+    l2 = div_rn(lw2, rs);
+  }
+}
+
 template <int kMode, bool kAtomicAlloc>
 __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitOut& o, Control* ctl,
                                              const CoverS* cs, bool valid, int k, int px, int py,
@@ -538,7 +561,7 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   bool live = false;
   TriData d;
   double w[3] = {0.0, 0.0, 0.0};
-  double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+  double l0 = 0.0, l1 = 0.0, l2 = 0.0, dep = 0.0;
   uint64_t code = ~0ull;
   if (valid) {
     double f0, f1, f2;
@@ -546,6 +569,7 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
     l0 = ddiv_zd(f0, c.area2);
     l1 = ddiv_zd(f1, c.area2);
     l2 = ddiv_zd(f2, c.area2);
+    if (kMode == kList && (p.persp || o.depth)) list_depth(p, item_job_g[k], l0, l1, l2, dep);
     load_tri_pos(p, c.tri, c.swapped, d);
     interp_pos(d, l0, l1, l2, w);
     live = true;
@@ -609,6 +633,7 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
         o.wpos[3 * rank + e] = w[e];
         o.wnrm[3 * rank + e] = nn[e];
       }
+      if (o.depth) o.depth[rank] = dep;
     }
     return;
   }
@@ -1444,16 +1469,28 @@ int chain_order(fhv_ctx* ctx, int32_t* heads, int32_t* prev, long long n_keys, l
 
 using namespace fhv;
 
-extern "C" int fhv_capture_list(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int64_t max_out,
-                                int64_t* job, int32_t* px, int32_t* py, double* wpos, double* wnrm, int64_t* n_out,
-                                void* stream) {
-  if (!ctx) return FHV_BAD_ARGS;
-  int rc = validate(tris, cfg);
-  if (rc) return rc;
-  cudaStream_t s = (cudaStream_t)stream;
-  const CaptureParams p = make_params(tris, cfg);
+namespace fhv {
+namespace {
+// capture_pass + ListSink (fhv/raster.py:309-388) in emission order; with
+// `depth`, FragmentBatch.depth too (needs the per-job ndc z, kept in p.persp)
+int list_capture(fhv_ctx* ctx, CaptureParams& p, int64_t max_out, int64_t* job, int32_t* px, int32_t* py,
+                 double* wpos, double* wnrm, double* depth, int64_t* n_out, cudaStream_t s) {
+  int rc;
+  if ((depth && p.strategy != 3) || p.strategy == kScreen) {
+    p.persp = (JobPersp*)scratch(ctx, kJobPersp, (size_t)(p.n_jobs > 0 ? p.n_jobs : 1) * sizeof(JobPersp));
+    if (!p.persp) return FHV_NOMEM;
+  }
   if ((rc = plan(ctx, p, s))) return rc;
   if ((rc = count(ctx, p, false, 0, nullptr, s))) return rc;
+  if (p.persp && ctx->n_items > 0) {
+    {
+      LaunchScope L_(ctx, kStEmitList, s);
+      k_job_n1<<<grid_for(p.n_jobs, 256), 256, 0, s>>>(p.n_jobs, (const uint32_t*)ctx->bufs[kJobItems].ptr,
+                                                       (const unsigned long long*)ctx->bufs[kJobItemOff].ptr,
+                                                       (const uint32_t*)ctx->bufs[kItemCnt].ptr, p.persp);
+    }
+    if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  }
   EmitOut o = empty_out();
   o.max_out = max_out;
   o.job = (long long*)job;
@@ -1461,10 +1498,59 @@ extern "C" int fhv_capture_list(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_
   o.py = py;
   o.wpos = wpos;
   o.wnrm = wnrm;
+  o.depth = depth;
   if (max_out > 0 && (rc = emit<kList>(ctx, p, o, false, s))) return rc;
   rc = sync_control(ctx, s);
   if (n_out) *n_out = (int64_t)ctx->ctl_host->scan_total;
   return rc;
+}
+}  // namespace
+}  // namespace fhv
+
+extern "C" int fhv_capture_list(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int64_t max_out,
+                                int64_t* job, int32_t* px, int32_t* py, double* wpos, double* wnrm, int64_t* n_out,
+                                void* stream) {
+  return fhv_capture_list_depth(ctx, tris, cfg, max_out, job, px, py, wpos, wnrm, nullptr, n_out, stream);
+}
+
+extern "C" int fhv_capture_list_depth(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
+                                      int64_t max_out, int64_t* job, int32_t* px, int32_t* py, double* wpos,
+                                      double* wnrm, double* depth, int64_t* n_out, void* stream) {
+  if (!ctx) return FHV_BAD_ARGS;
+  int rc = validate(tris, cfg);
+  if (rc) return rc;
+  CaptureParams p = make_params(tris, cfg);
+  return list_capture(ctx, p, max_out, job, px, py, wpos, wnrm, depth, n_out, (cudaStream_t)stream);
+}
+
+// _raster_screen (fhv/raster.py:184-209) of every triangle through one
+// arbitrary 4x4 projection into a width x height raster: the fragments of
+// rasterize_triangle, in (triangle, y, x) order, with depth; a perspective
+// triangle with any clip w <= 1e-9 emits nothing
+extern "C" int fhv_raster_screen(fhv_ctx* ctx, const fhv_tris_t* tris, const double* proj, int32_t width,
+                                 int32_t height, int64_t max_out, int64_t* job, int32_t* px, int32_t* py, double* wpos,
+                                 double* wnrm, double* depth, int64_t* n_out, void* stream) {
+  if (!ctx || !tris || !proj || width < 1 || height < 1) return FHV_BAD_ARGS;
+  if (tris->n_tri < 0 || (tris->n_tri > 0 && (!tris->pos || !tris->vnrm || !tris->fnrm || !tris->mat || !tris->obj)))
+    return FHV_BAD_ARGS;
+  if (tris->n_tri >= (1LL << 32) - 1) return FHV_BAD_ARGS;
+  CaptureParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.strategy = kScreen;
+  p.res = height;
+  p.width = width;
+  p.height = height;
+  p.ortho = proj[12] == 0.0 && proj[13] == 0.0 && proj[14] == 0.0 && proj[15] == 1.0;
+  std::memcpy(p.proj[0], proj, 16 * sizeof(double));
+  p.n_tri = tris->n_tri;
+  p.n_jobs = tris->n_tri;
+  p.pos = tris->pos;
+  p.vnrm = tris->vnrm;
+  p.fnrm = tris->fnrm;
+  p.mat = tris->mat;
+  p.obj = tris->obj;
+  p.cell_hi = ~0ull;
+  return list_capture(ctx, p, max_out, job, px, py, wpos, wnrm, depth, n_out, (cudaStream_t)stream);
 }
 
 static int build_linked(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, bool pofl, int64_t width,

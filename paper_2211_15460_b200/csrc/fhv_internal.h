@@ -43,7 +43,7 @@ namespace fhv {
 enum Stage {
   kStJobSetup = 0, kStScan, kStItemExpand, kStCount, kStCountLeaves, kStEmitList, kStEmitPpfl, kStEmitPofl,
   kStEmitPofa, kStChainOrder, kStLeafOrder, kStScanLeaves, kStPyramid, kStSplatDepth, kStSplatIndex,
-  kStSplatResolve, kStRaycast, kStFaceNormals, kStDeferred, kNumStages
+  kStSplatResolve, kStRaycast, kStFaceNormals, kStDeferred, kStOps, kStScalar, kNumStages
 };
 struct PendingEvent {
   int stage;

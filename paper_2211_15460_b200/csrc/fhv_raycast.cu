@@ -192,8 +192,8 @@ struct StackCodec {
 // one inner node of the DFS: children whose slabs the ray meets pushed far
 // first, so the nearest (t_enter, child) pops next (fhv/_ckern.pyx:580-632)
 template <class E>
-__device__ __forceinline__ void expand_node(const RayParams& x, const double o[3], const double d[3], double tmax,
-                                            int level, unsigned long long code, E* stack, int& sp) {
+__device__ __forceinline__ void expand_node(const RayParams& x, const double o[3], const double d[3], double tmin,
+                                            double tmax, int level, unsigned long long code, E* stack, int& sp) {
   using SC = StackCodec<E>;
   const unsigned mask = __ldg(&x.v.pyramid[pyr_level_offset(level) + (long long)code]);
   if (mask == 0) return;
@@ -225,7 +225,7 @@ __device__ __forceinline__ void expand_node(const RayParams& x, const double o[3
   for (int c = 0; c < 8; ++c) {
     if (!((mask >> c) & 1u)) continue;
     const int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
-    double t0 = 0.0, t1 = tmax;
+    double t0 = tmin, t1 = tmax;
     if (!slab_axis(o[0], d[0], pl[0][bx], pl[0][bx + 1], tp[0][bx], tp[0][bx + 1], t0, t1)) continue;
     if (!slab_axis(o[1], d[1], pl[1][by], pl[1][by + 1], tp[1][by], tp[1][by + 1], t0, t1)) continue;
     if (!slab_axis(o[2], d[2], pl[2][bz], pl[2][bz + 1], tp[2][bz], tp[2][bz + 1], t0, t1)) continue;
@@ -244,13 +244,15 @@ __device__ __forceinline__ void expand_node(const RayParams& x, const double o[3
   for (int j = nc - 1; j >= 0; --j) stack[sp++] = lvl | (E)(code * 8ull + (unsigned long long)cc[j]);
 }
 
+// ray interval [tmin, tmax] (traverse_octree's ray.t_min / t_max; the image
+// kernels use [0, tmax])
 template <class E, class V>
-__device__ void traverse(const RayParams& x, const double o[3], const double d[3], double tmax, Stats& st,
-                         V&& visit_leaf) {
+__device__ void traverse_range(const RayParams& x, const double o[3], const double d[3], double tmin, double tmax,
+                               Stats& st, V&& visit_leaf) {
   using SC = StackCodec<E>;
   const double zero3[3] = {0.0, 0.0, 0.0}, one3[3] = {1.0, 1.0, 1.0};
   double te;
-  if (!slab_box(o, d, zero3, one3, 0.0, tmax, &te)) return;
+  if (!slab_box(o, d, zero3, one3, tmin, tmax, &te)) return;
   const int L = x.v.levels;
   E stack[kStack];
   int sp = 0;
@@ -264,8 +266,14 @@ __device__ void traverse(const RayParams& x, const double o[3], const double d[3
       if (!visit_leaf((long long)code)) return;
       continue;
     }
-    expand_node<E>(x, o, d, tmax, level, code, stack, sp);
+    expand_node<E>(x, o, d, tmin, tmax, level, code, stack, sp);
   }
+}
+
+template <class E, class V>
+__device__ __forceinline__ void traverse(const RayParams& x, const double o[3], const double d[3], double tmax,
+                                         Stats& st, V&& visit_leaf) {
+  traverse_range<E>(x, o, d, 0.0, tmax, st, visit_leaf);
 }
 
 // _transmit (fhv/_ckern.pyx:326-435)
@@ -487,6 +495,181 @@ __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// scalar query API (fhv/raycast.py:205-453): raycast_pixel with its hit list,
+// gather_ray_hits, shadow_transmittance, traverse_octree's leaf sequence and
+// intersect_fragment -- one thread per query ray, same device functions as
+// the image kernel (not a hot path: a handful of rays per call)
+
+struct ProbeOut {
+  const double* tmin;  // per-ray interval, or null -> [0, inf)
+  const double* tmax;
+  int eye_is_origin;   // raycast_pixel(eye=None): shade toward each ray's origin
+  long long cap;       // hit slots per ray
+  double* hit_t;
+  long long* hit_idx;
+  long long* hit_leaf;
+  long long* hit_n;    // hits found per ray (may exceed cap: the caller retries)
+  long long* stats;    // n x 4 RaycastStats counters
+};
+
+// kMode 0..2 = raycast_pixel modes; 3 = gather_ray_hits (no shading, no
+// cutoff, hits not counted -- fhv/raycast.py:294-308)
+template <int kMode, class E>
+__global__ void __launch_bounds__(64) k_ray_probe(RayParams x, long long n, ProbeOut po) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    RayParams xr = x;
+    double o[3], d[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      o[c] = x.origins[3 * r + c];
+      d[c] = x.dirs[3 * r + c];
+      if (po.eye_is_origin) xr.eye[c] = o[c];
+    }
+    const double tmin = po.tmin ? po.tmin[r] : 0.0;
+    const double tmax = po.tmax ? po.tmax[r] : __longlong_as_double(0x7ff0000000000000ll);
+    Stats st = {0, 0, 0, 0};
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, acc = 0.0;
+    bool any_hit = false;
+    long long cnt = 0;
+    traverse_range<E>(xr, o, d, tmin, tmax, st, [&](long long code) {
+      bool stop = false;
+      leaf_hits(xr, code, o, d, tmin, tmax, st, [&](double t, long long i) {
+        if (cnt < po.cap) {
+          po.hit_t[r * po.cap + cnt] = t;
+          po.hit_idx[r * po.cap + cnt] = i;
+          po.hit_leaf[r * po.cap + cnt] = code;
+        }
+        ++cnt;
+        if (kMode == 3) return true;
+        st.hits++;
+        double col[3];
+        if (kMode == 0) {
+          shade_hit<0, E>(xr, i, code, st, col);
+          c0 = col[0];
+          c1 = col[1];
+          c2 = col[2];
+          acc = 1.0;
+          any_hit = true;
+          stop = true;
+          return false;
+        }
+        const double a = xr.s.alpha[xr.v.mat[i]];
+        shade_hit<kMode == 3 ? 1 : kMode, E>(xr, i, code, st, col);
+        const double tc = __dmul_rn(__dsub_rn(1.0, acc), a);
+        c0 = __dadd_rn(c0, __dmul_rn(tc, col[0]));
+        c1 = __dadd_rn(c1, __dmul_rn(tc, col[1]));
+        c2 = __dadd_rn(c2, __dmul_rn(tc, col[2]));
+        acc = __dadd_rn(acc, tc);
+        any_hit = true;
+        return true;
+      });
+      if (stop) return false;
+      if (kMode != 3 && xr.cutoff >= 0.0 && acc >= xr.cutoff) {
+        st.early++;
+        return false;
+      }
+      return true;
+    });
+    if (x.out_rgba) {
+      double* px = x.out_rgba + 4 * r;
+      if (kMode == 0) {
+        px[0] = any_hit ? c0 : x.bg[0];
+        px[1] = any_hit ? c1 : x.bg[1];
+        px[2] = any_hit ? c2 : x.bg[2];
+        px[3] = any_hit ? 1.0 : x.bg[3];
+      } else {
+        const double ra = __dsub_rn(1.0, acc);
+        px[0] = __dadd_rn(c0, __dmul_rn(__dmul_rn(ra, x.bg[3]), x.bg[0]));
+        px[1] = __dadd_rn(c1, __dmul_rn(__dmul_rn(ra, x.bg[3]), x.bg[1]));
+        px[2] = __dadd_rn(c2, __dmul_rn(__dmul_rn(ra, x.bg[3]), x.bg[2]));
+        px[3] = __dadd_rn(acc, __dmul_rn(ra, x.bg[3]));
+      }
+    }
+    po.hit_n[r] = cnt;
+    po.stats[4 * r] = (long long)st.visited;
+    po.stats[4 * r + 1] = (long long)st.tested;
+    po.stats[4 * r + 2] = (long long)st.hits;
+    po.stats[4 * r + 3] = (long long)st.early;
+  }
+}
+
+// shadow_transmittance (fhv/raycast.py:408-453 = _transmit): light li of the
+// shading table; exclusion (object id, leaf) = -1 for none
+template <class E>
+__global__ void __launch_bounds__(64) k_transmit_probe(RayParams x, long long n, const double* __restrict__ pts,
+                                                       int li, const long long* ex_obj, const long long* ex_cell,
+                                                       double* __restrict__ tau, long long* __restrict__ stats) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const double p[3] = {pts[3 * r], pts[3 * r + 1], pts[3 * r + 2]};
+    Stats st = {0, 0, 0, 0};
+    tau[r] = transmit<E>(x, p, li, ex_obj ? ex_obj[r] : -1, ex_cell ? ex_cell[r] : -1, st);
+    stats[4 * r] = (long long)st.visited;
+    stats[4 * r + 1] = (long long)st.tested;
+    stats[4 * r + 2] = (long long)st.hits;
+    stats[4 * r + 3] = (long long)st.early;
+  }
+}
+
+// traverse_octree (fhv/raycast.py:205-243): the occupied leaves one ray
+// crosses, nearest entry first, with their clipped [t_enter, t_exit].  The
+// order does not depend on the visitor, so the whole sequence is listed and
+// the host replays visit() over it (stopping where visit returns False).
+template <class E>
+__global__ void k_leaf_order(RayParams x, double tmin, double tmax, long long cap, long long* __restrict__ code_out,
+                             double* __restrict__ te_out, double* __restrict__ tx_out, long long* n_out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const double o[3] = {x.origins[0], x.origins[1], x.origins[2]};
+  const double d[3] = {x.dirs[0], x.dirs[1], x.dirs[2]};
+  const double size = __longlong_as_double((1023LL - x.v.levels) << 52);  // 2^-L
+  Stats st = {0, 0, 0, 0};
+  long long cnt = 0;
+  traverse_range<E>(x, o, d, tmin, tmax, st, [&](long long code) {
+    if (cnt < cap) {
+      const double lo[3] = {__dmul_rn((double)compact3((unsigned long long)code), size),
+                            __dmul_rn((double)compact3((unsigned long long)code >> 1), size),
+                            __dmul_rn((double)compact3((unsigned long long)code >> 2), size)};
+      double t0 = tmin, t1 = tmax;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double hi = __dadd_rn(lo[a], size);
+        double ta = 0.0, tb = 0.0;
+        if (d[a] != 0.0) {
+          ta = ddiv_z(__dsub_rn(lo[a], o[a]), d[a]);
+          tb = ddiv_z(__dsub_rn(hi, o[a]), d[a]);
+        }
+        slab_axis(o[a], d[a], lo[a], hi, ta, tb, t0, t1);  // the DFS only reaches leaves whose slab test passed
+      }
+      code_out[cnt] = code;
+      te_out[cnt] = t0;
+      tx_out[cnt] = t1;
+    }
+    ++cnt;
+    return true;
+  });
+  *n_out = cnt;
+}
+
+// intersect_fragment (fhv/raycast.py:246-262): t = (p - o) @ d and
+// |p - (o + t d)|^2 as ddot (FWD order), inclusive interval and radius tests
+__global__ void k_intersect_points(long long n, const double* __restrict__ pts, double o0, double o1, double o2,
+                                   double d0, double d1, double d2, double tmin, double tmax, double r2,
+                                   double* __restrict__ t_out, int8_t* __restrict__ hit) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double p0 = pts[3 * i], p1 = pts[3 * i + 1], p2 = pts[3 * i + 2];
+    const double t = fwd3(__dsub_rn(p0, o0), __dsub_rn(p1, o1), __dsub_rn(p2, o2), d0, d1, d2);
+    bool h = !(t < tmin || t > tmax);
+    if (h) {
+      const double e0 = __dsub_rn(p0, __dadd_rn(o0, __dmul_rn(t, d0)));
+      const double e1 = __dsub_rn(p1, __dadd_rn(o1, __dmul_rn(t, d1)));
+      const double e2 = __dsub_rn(p2, __dadd_rn(o2, __dmul_rn(t, d2)));
+      h = fwd3(e0, e1, e2, e0, e1, e2) <= r2;
+    }
+    t_out[i] = t;
+    hit[i] = h ? 1 : 0;
+  }
+}
+
 namespace {
 inline int grid_for(long long n, int block, int per_sm = 16) {
   long long g = (n + block - 1) / block;
@@ -596,4 +779,117 @@ extern "C" int fhv_raycast_image(fhv_ctx* ctx, int64_t start, int64_t end, const
   x.start = start;
   x.end = end;
   return launch(ctx, x, stream);
+}
+
+// raycast_pixel / gather_ray_hits over n caller rays (mode 3 = gather)
+extern "C" int fhv_ray_probe(fhv_ctx* ctx, int64_t n, const double* origins, const double* dirs, const double* tmin,
+                             const double* tmax, const fhv_volume_t* vol, const fhv_shading_t* shading,
+                             const double* eye, const double* background, double radius, double cutoff, int32_t mode,
+                             double shadow_eps, int64_t hit_cap, double* out_rgba, double* hit_t, int64_t* hit_idx,
+                             int64_t* hit_leaf, int64_t* hit_n, int64_t* stats, void* stream) {
+  if (!ctx || n < 0 || !origins || !dirs || !hit_n || !stats || hit_cap < 0) return FHV_BAD_ARGS;
+  if (hit_cap > 0 && (!hit_t || !hit_idx || !hit_leaf)) return FHV_BAD_ARGS;
+  if (mode < 0 || mode > 3) return FHV_BAD_ARGS;
+  if (n == 0) return FHV_OK;
+  RayParams x;
+  std::memset(&x, 0, sizeof(x));
+  // common() validates the volume / shading / radius; mode 3 shades nothing
+  int64_t dummy_counters[4];
+  int rc = common(x, vol, shading, background, radius, cutoff, mode == 3 ? 1 : mode, shadow_eps,
+                  out_rgba ? out_rgba : (double*)dummy_counters, nullptr, dummy_counters);
+  if (rc) return rc;
+  x.out_rgba = out_rgba;
+  x.counters = nullptr;
+  x.origins = origins;
+  x.dirs = dirs;
+  for (int c = 0; c < 3; ++c) x.eye[c] = eye ? eye[c] : 0.0;
+  ProbeOut po{tmin, tmax, eye ? 0 : 1, hit_cap, hit_t, (long long*)hit_idx, (long long*)hit_leaf, (long long*)hit_n,
+              (long long*)stats};
+  cudaStream_t s = (cudaStream_t)stream;
+  const int g = grid_for(n, 64, 8);
+  {
+    LaunchScope L_(ctx, kStScalar, s);
+    if (x.v.levels <= 9) {
+      if (mode == 0) k_ray_probe<0, uint32_t><<<g, 64, 0, s>>>(x, n, po);
+      else if (mode == 1) k_ray_probe<1, uint32_t><<<g, 64, 0, s>>>(x, n, po);
+      else if (mode == 2) k_ray_probe<2, uint32_t><<<g, 64, 0, s>>>(x, n, po);
+      else k_ray_probe<3, uint32_t><<<g, 64, 0, s>>>(x, n, po);
+    } else {
+      if (mode == 0) k_ray_probe<0, unsigned long long><<<g, 64, 0, s>>>(x, n, po);
+      else if (mode == 1) k_ray_probe<1, unsigned long long><<<g, 64, 0, s>>>(x, n, po);
+      else if (mode == 2) k_ray_probe<2, unsigned long long><<<g, 64, 0, s>>>(x, n, po);
+      else k_ray_probe<3, unsigned long long><<<g, 64, 0, s>>>(x, n, po);
+    }
+  }
+  return check_cuda(ctx, cudaGetLastError());
+}
+
+// shadow_transmittance toward light `light` of the shading table, n points
+extern "C" int fhv_transmittance(fhv_ctx* ctx, int64_t n, const double* points, int32_t light,
+                                 const int64_t* exclude_obj, const int64_t* exclude_cell, const fhv_volume_t* vol,
+                                 const fhv_shading_t* shading, double radius, double shadow_eps, double* tau,
+                                 int64_t* stats, void* stream) {
+  if (!ctx || n < 0 || !shading || light < 0 || light >= shading->n_lights) return FHV_BAD_ARGS;
+  if (n == 0) return FHV_OK;
+  if (!points || !tau || !stats) return FHV_BAD_ARGS;
+  RayParams x;
+  std::memset(&x, 0, sizeof(x));
+  const double bg[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t dummy[4];
+  int rc = common(x, vol, shading, bg, radius, -1.0, 2, shadow_eps, (double*)dummy, nullptr, dummy);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int g = grid_for(n, 64, 8);
+  {
+    LaunchScope L_(ctx, kStScalar, s);
+    if (x.v.levels <= 9)
+      k_transmit_probe<uint32_t><<<g, 64, 0, s>>>(x, n, points, light, (const long long*)exclude_obj,
+                                                  (const long long*)exclude_cell, tau, (long long*)stats);
+    else
+      k_transmit_probe<unsigned long long><<<g, 64, 0, s>>>(x, n, points, light, (const long long*)exclude_obj,
+                                                            (const long long*)exclude_cell, tau, (long long*)stats);
+  }
+  return check_cuda(ctx, cudaGetLastError());
+}
+
+// traverse_octree's leaf sequence for one ray (origin/dir: 3 device doubles)
+extern "C" int fhv_leaf_order(fhv_ctx* ctx, int32_t levels, const uint8_t* pyramid, const double* origin,
+                              const double* dir, double tmin, double tmax, int64_t cap, int64_t* code_out,
+                              double* te_out, double* tx_out, int64_t* n_out, void* stream) {
+  if (!ctx || levels < 1 || levels > kRayMaxLevels || !pyramid || !origin || !dir || !n_out || cap < 0)
+    return FHV_BAD_ARGS;
+  if (cap > 0 && (!code_out || !te_out || !tx_out)) return FHV_BAD_ARGS;
+  RayParams x;
+  std::memset(&x, 0, sizeof(x));
+  x.v.levels = levels;
+  x.v.pyramid = pyramid;
+  x.origins = origin;
+  x.dirs = dir;
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    LaunchScope L_(ctx, kStScalar, s);
+    if (levels <= 9)
+      k_leaf_order<uint32_t><<<1, 32, 0, s>>>(x, tmin, tmax, cap, (long long*)code_out, te_out, tx_out,
+                                              (long long*)n_out);
+    else
+      k_leaf_order<unsigned long long><<<1, 32, 0, s>>>(x, tmin, tmax, cap, (long long*)code_out, te_out, tx_out,
+                                                        (long long*)n_out);
+  }
+  return check_cuda(ctx, cudaGetLastError());
+}
+
+// intersect_fragment for n points against one ray
+extern "C" int fhv_intersect_points(fhv_ctx* ctx, int64_t n, const double* points, const double* origin,
+                                    const double* dir, double tmin, double tmax, double radius, double* t_out,
+                                    int8_t* hit, void* stream) {
+  if (!ctx || n < 0 || !origin || !dir) return FHV_BAD_ARGS;
+  if (n == 0) return FHV_OK;
+  if (!points || !t_out || !hit) return FHV_BAD_ARGS;
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    LaunchScope L_(ctx, kStScalar, s);
+    k_intersect_points<<<grid_for(n, 128, 8), 128, 0, s>>>(n, points, origin[0], origin[1], origin[2], dir[0], dir[1],
+                                                           dir[2], tmin, tmax, radius * radius, t_out, hit);
+  }
+  return check_cuda(ctx, cudaGetLastError());
 }

@@ -118,6 +118,19 @@ class DeviceShading:
         self.n_lights = len(lights)
         self.n_mats = len(md)
 
+    @staticmethod
+    def from_arrays(mats: dict, lights, device: torch.device) -> "DeviceShading":
+        """From material_arrays()-style tables (the reference's ``mats`` dicts)."""
+        self = DeviceShading.__new__(DeviceShading)
+        lk, lv, lc, la = pack_lights(lights)
+        arrs = [np.ascontiguousarray(np.asarray(mats[k], dtype=np.float64))
+                for k in ("diffuse", "specular", "shininess", "alpha")]
+        self.tensors = [torch.from_numpy(np.ascontiguousarray(a)).to(device) for a in (lk.astype(np.uint8), lv, lc, la)]
+        self.tensors += [torch.from_numpy(a).to(device) for a in arrs]
+        self.n_lights = len(lights)
+        self.n_mats = len(arrs[3])
+        return self
+
     def struct(self) -> _lib.Shading:
         st = self.__dict__.get("_struct")
         if st is None:  # tables are immutable after construction

@@ -16,9 +16,9 @@ import numpy as np
 
 from .scene import Camera, Scene, SceneError, capture_camera
 
-__all__ = ["CAPTURE_STRATEGIES", "CapturePlan", "CaptureStats", "CaptureStrategy", "FragmentBatch",
-           "RasterConfig", "capture_plan", "ortho_projection", "perspective_projection",
-           "tangent_basis", "world_pixel_footprint"]
+__all__ = ["CAPTURE_STRATEGIES", "CapturePlan", "CaptureStats", "CaptureStrategy", "EmittedFragment",
+           "FragmentBatch", "ListSink", "RasterConfig", "capture_plan", "ortho_projection", "perspective_projection",
+           "rasterize_triangle", "rasterize_triangles", "tangent_basis", "world_pixel_footprint"]
 
 CAPTURE_STRATEGIES = ("one_view", "three_separate", "three_way_geometry", "normal_space")
 STRATEGY_CODE = {k: i for i, k in enumerate(CAPTURE_STRATEGIES)}
@@ -105,6 +105,18 @@ def tangent_basis(n) -> np.ndarray:
 
 
 @dataclass
+class EmittedFragment:
+    """One fragment (fhv/raster.py:114-121): what ppfl_insert / pofl_insert take."""
+
+    raster_xy: tuple
+    world_position: np.ndarray
+    world_normal: np.ndarray
+    depth: float
+    material_id: int
+    object_id: int
+
+
+@dataclass
 class FragmentBatch:
     """All fragments of one (triangle, pass) job, struct-of-arrays (fhv/raster.py:124-144)."""
 
@@ -118,6 +130,25 @@ class FragmentBatch:
 
     def __len__(self) -> int:
         return len(self.raster_x)
+
+    def fragments(self):
+        for i in range(len(self.raster_x)):
+            yield EmittedFragment((int(self.raster_x[i]), int(self.raster_y[i])), self.world_position[i],
+                                  self.world_normal[i], float(self.depth[i]), self.material_id, self.object_id)
+
+
+class ListSink:
+    """Collects emitted batches (fhv/raster.py:309-320; test/inspection helper)."""
+
+    def __init__(self):
+        self.batches: list = []
+
+    def __call__(self, batch: FragmentBatch) -> None:
+        self.batches.append(batch)
+
+    @property
+    def total(self) -> int:
+        return sum(len(b) for b in self.batches)
 
 
 @dataclass(frozen=True)
@@ -214,3 +245,52 @@ def capture_plan(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig) -> 
         pitch = world_pixel_footprint(cfg)
         n_jobs, passes = T, 1
     return CapturePlan(code, res, float(pitch), proj, n_jobs, passes, scene.n_objects)
+
+
+def rasterize_triangles(scene: Scene, cfg: RasterConfig, device=None) -> dict:
+    """``_raster_screen`` of every triangle of ``scene`` through ``cfg`` on the
+    device (fhv_raster_screen): fragments in (triangle, y, x) order as CUDA
+    tensors ``job`` (triangle index), ``raster_x``, ``raster_y``,
+    ``world_position``, ``world_normal``, ``depth``."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .device import device_scene, host_f64
+    ds = device_scene(scene, device)
+    dev = ds.device
+    lib = _lib.load()
+    cx, st = _lib.ctx(dev), _lib.stream_ptr(dev)
+    proj = host_f64(cfg.projection).reshape(16)
+    w, h = (int(v) for v in cfg.resolution)
+    n = ctypes.c_int64(0)
+    rc = lib.fhv_raster_screen(cx, ds.struct(), proj.ctypes.data, w, h, 0, None, None, None, None, None, None,
+                               ctypes.byref(n), st)
+    _lib.check(rc, "rasterize_triangle")
+    m = int(n.value)
+    job = torch.empty(m, dtype=torch.int64, device=dev)
+    px = torch.empty(m, dtype=torch.int32, device=dev)
+    py = torch.empty(m, dtype=torch.int32, device=dev)
+    wpos = torch.empty((m, 3), dtype=torch.float64, device=dev)
+    wnrm = torch.empty((m, 3), dtype=torch.float64, device=dev)
+    dep = torch.empty(m, dtype=torch.float64, device=dev)
+    if m:
+        rc = lib.fhv_raster_screen(cx, ds.struct(), proj.ctypes.data, w, h, m, _lib.ptr(job), _lib.ptr(px),
+                                   _lib.ptr(py), _lib.ptr(wpos), _lib.ptr(wnrm), _lib.ptr(dep), ctypes.byref(n), st)
+        _lib.check(rc, "rasterize_triangle")
+    return {"job": job, "raster_x": px, "raster_y": py, "world_position": wpos, "world_normal": wnrm, "depth": dep}
+
+
+def rasterize_triangle(tri, cfg: RasterConfig, sink=None, device=None) -> int:
+    """Rasterise one triangle through ``cfg`` (fhv/raster.py:245-252): emits
+    one FragmentBatch (host arrays, the reference's types) to ``sink`` when it
+    covers any pixel; returns the fragment count."""
+    from .scene import Material, Scene
+    out = rasterize_triangles(Scene.from_triangles([tri], [Material()] * (int(tri.material_id) + 1)), cfg, device)
+    n = int(out["job"].numel())
+    if n and sink is not None:
+        sink(FragmentBatch(out["raster_x"].cpu().numpy(), out["raster_y"].cpu().numpy(),
+                           out["world_position"].cpu().numpy(), out["world_normal"].cpu().numpy(),
+                           out["depth"].cpu().numpy(), int(tri.material_id), int(tri.object_id)))
+    return n

@@ -18,10 +18,40 @@ from .device import DeviceShading, host_f64
 from .lights import ImageBuffer
 from .scene import Camera, Material, SceneError
 
-__all__ = ["RAYCAST_MODES", "RaycastConfig", "RaycastStats", "default_raycast_config", "primary_rays",
-           "render_raycast", "render_raycast_rays"]
+__all__ = ["HitRecord", "RAYCAST_MODES", "Ray", "RaycastConfig", "RaycastStats", "default_raycast_config",
+           "gather_ray_hits", "gen_primary_ray", "intersect_fragment", "primary_rays", "raycast_pixel",
+           "render_raycast", "render_raycast_rays", "shadow_transmittance", "traverse_octree"]
 
 RAYCAST_MODES = ("opaque_nearest", "transparency", "transparency_shadows")
+
+
+@dataclass
+class Ray:
+    """A ray with its parameter interval (fhv/raycast.py:42-58); the direction
+    is unit-normalised unless it is already within 1e-9 of unit length."""
+
+    origin: np.ndarray
+    direction: np.ndarray
+    t_min: float = 0.0
+    t_max: float = math.inf
+
+    def __post_init__(self):
+        self.origin = np.asarray(self.origin, dtype=np.float64)
+        self.direction = np.asarray(self.direction, dtype=np.float64)
+        n = float(np.linalg.norm(self.direction))
+        if abs(n - 1.0) > 1e-9:
+            if n == 0.0:
+                raise SceneError("zero ray direction")
+            self.direction = self.direction / n
+        if not self.t_min < self.t_max:
+            raise SceneError("ray needs t_min < t_max")
+
+
+@dataclass
+class HitRecord:
+    t: float
+    fragment_index: int
+    leaf: int
 
 
 @dataclass(frozen=True)
@@ -172,3 +202,185 @@ def render_raycast_rays(fhv, origins: torch.Tensor, dirs: torch.Tensor, eye, lig
                                _lib.stream_ptr(dev))
     _lib.check(rc, "raycast_image")
     return out_rgba, RaycastStats(*counters.cpu().tolist())
+
+
+# ---------------------------------------------------------------------------
+# scalar queries (fhv/raycast.py:129-453) -- each one a small device launch
+# over the resident volume (fhv_ray_probe / fhv_transmittance /
+# fhv_leaf_order / fhv_intersect_points); hit lists come back to the host
+
+
+def gen_primary_ray(camera: Camera, px) -> Ray:
+    """Ray through the centre of pixel (ix, iy) (fhv/raycast.py:129-145)."""
+    ix, iy = px
+    w, h = camera.resolution
+    if not (0 <= ix < w and 0 <= iy < h):
+        raise SceneError(f"pixel {px} outside resolution")
+    r, u, f = camera.basis()
+    ndc_x = (ix + 0.5) / w * 2.0 - 1.0
+    ndc_y = 1.0 - (iy + 0.5) / h * 2.0
+    if camera.kind == "orthographic":
+        half_h = camera.extent_or_fov / 2.0
+        half_w = half_h * camera.aspect
+        origin = camera.eye + ndc_x * half_w * r + ndc_y * half_h * u + camera.near * f
+        return Ray(origin, f.copy())
+    t = math.tan(math.radians(camera.extent_or_fov) / 2.0)
+    direction = f + ndc_x * t * camera.aspect * r + ndc_y * t * u
+    return Ray(camera.eye.copy(), direction)
+
+
+def _dev_ray(ray: Ray, dev):
+    o = torch.from_numpy(np.ascontiguousarray(ray.origin, dtype=np.float64)).to(dev)
+    d = torch.from_numpy(np.ascontiguousarray(ray.direction, dtype=np.float64)).to(dev)
+    return o, d
+
+
+def _merge(stats: RaycastStats | None, c, hits: bool = True) -> None:
+    if stats is None:
+        return
+    stats.visited_leaves += int(c[0])
+    stats.tested_fragments += int(c[1])
+    if hits:
+        stats.hits += int(c[2])
+        stats.early_terminations += int(c[3])
+
+
+def traverse_octree(pyramid, ray: Ray, visit) -> int:
+    """Visit the occupied leaves the ray crosses, nearest entry first
+    (fhv/raycast.py:205-243): ``visit(code, t_enter, t_exit) -> bool``, False
+    stops.  Returns the number of leaves visited.  The device lists the leaf
+    sequence (it does not depend on the visitor); the host replays it."""
+    dev = pyramid.data.device
+    o, d = _dev_ray(ray, dev)
+    lib = _lib.load()
+    cap = 1024
+    while True:
+        codes = torch.empty(cap, dtype=torch.int64, device=dev)
+        te = torch.empty(cap, dtype=torch.float64, device=dev)
+        tx = torch.empty(cap, dtype=torch.float64, device=dev)
+        n = torch.zeros(1, dtype=torch.int64, device=dev)
+        rc = lib.fhv_leaf_order(_lib.ctx(dev), pyramid.leaf_levels, _lib.ptr(pyramid.data), _lib.ptr(o), _lib.ptr(d),
+                                float(ray.t_min), float(ray.t_max), cap, _lib.ptr(codes), _lib.ptr(te), _lib.ptr(tx),
+                                _lib.ptr(n), _lib.stream_ptr(dev))
+        _lib.check(rc, "traverse_octree")
+        total = int(n.item())
+        if total <= cap:
+            break
+        cap = total
+    visited = 0
+    for code, a, b in zip(codes[:total].tolist(), te[:total].tolist(), tx[:total].tolist()):
+        visited += 1
+        if not visit(code, a, b):
+            break
+    return visited
+
+
+def intersect_fragment(ray: Ray, position, radius: float, device=None) -> float | None:
+    """Hit parameter of a point fragment within the splat radius, or None
+    (fhv/raycast.py:246-262)."""
+    from .device import default_device
+    dev = default_device(device)
+    p = torch.from_numpy(np.ascontiguousarray(np.asarray(position, dtype=np.float64).reshape(1, 3))).to(dev)
+    t = torch.empty(1, dtype=torch.float64, device=dev)
+    hit = torch.empty(1, dtype=torch.int8, device=dev)
+    o, dr = host_f64(ray.origin), host_f64(ray.direction)
+    rc = _lib.load().fhv_intersect_points(_lib.ctx(dev), 1, _lib.ptr(p), o.ctypes.data, dr.ctypes.data,
+                                          float(ray.t_min), float(ray.t_max), float(radius), _lib.ptr(t),
+                                          _lib.ptr(hit), _lib.stream_ptr(dev))
+    _lib.check(rc, "intersect_fragment")
+    return float(t.item()) if int(hit.item()) else None
+
+
+def _probe(fhv, ray: Ray, mode: int, radius: float, shading: DeviceShading, cutoff: float, shadow_eps: float,
+           background, eye):
+    dev = fhv.pool.device
+    o, d = _dev_ray(ray, dev)
+    tmin = torch.tensor([float(ray.t_min)], dtype=torch.float64, device=dev)
+    tmax = torch.tensor([float(ray.t_max)], dtype=torch.float64, device=dev)
+    rgba = torch.empty(4, dtype=torch.float64, device=dev)
+    hit_n = torch.zeros(1, dtype=torch.int64, device=dev)
+    stats = torch.zeros(4, dtype=torch.int64, device=dev)
+    bg = host_f64(background)
+    e = None if eye is None else host_f64(eye)
+    lib = _lib.load()
+    cap = 256
+    while True:
+        ht = torch.empty(cap, dtype=torch.float64, device=dev)
+        hi = torch.empty(cap, dtype=torch.int64, device=dev)
+        hl = torch.empty(cap, dtype=torch.int64, device=dev)
+        rc = lib.fhv_ray_probe(_lib.ctx(dev), 1, _lib.ptr(o), _lib.ptr(d), _lib.ptr(tmin), _lib.ptr(tmax),
+                               _volume(fhv), shading.struct(), None if e is None else e.ctypes.data, bg.ctypes.data,
+                               float(radius), float(cutoff), mode, float(shadow_eps), cap, _lib.ptr(rgba),
+                               _lib.ptr(ht), _lib.ptr(hi), _lib.ptr(hl), _lib.ptr(hit_n), _lib.ptr(stats),
+                               _lib.stream_ptr(dev))
+        _lib.check(rc, "raycast_pixel")
+        n = int(hit_n.item())
+        if n <= cap:
+            break
+        cap = n
+    hits = [HitRecord(t, i, c) for t, i, c in zip(ht[:n].tolist(), hi[:n].tolist(), hl[:n].tolist())]
+    return rgba.cpu().numpy(), hits, stats.cpu().tolist()
+
+
+def _shading_for(fhv, materials, lights, dev) -> DeviceShading:
+    if materials is None:
+        materials = fhv.materials or [Material()]
+    if isinstance(materials, dict):
+        return DeviceShading.from_arrays(materials, lights, dev)
+    return DeviceShading(materials, lights, dev)
+
+
+def gather_ray_hits(fhv, ray: Ray, radius: float, stats: RaycastStats | None = None) -> list:
+    """Every hit along a ray, leaf by leaf, sorted by (t, index) inside each
+    leaf (fhv/raycast.py:294-308)."""
+    if fhv.layout not in ("POFA", "POFL"):
+        raise SceneError("ray casting requires a per-octant layout")
+    sh = _shading_for(fhv, None, [], fhv.pool.device)
+    _, hits, c = _probe(fhv, ray, 3, radius, sh, -1.0, 0.0, (0.0, 0.0, 0.0, 0.0), None)
+    _merge(stats, c, hits=False)
+    return hits
+
+
+def raycast_pixel(fhv, ray: Ray, lights, cfg: RaycastConfig, materials=None, background=(0.0, 0.0, 0.0, 0.0),
+                  eye=None, stats: RaycastStats | None = None, hit_out: list | None = None) -> np.ndarray:
+    """Evaluate one ray against a per-octant volume; returns rgba
+    (fhv/raycast.py:351-405).  ``eye`` defaults to the ray origin; ``hit_out``
+    receives the HitRecords composited (opaque_nearest: the first)."""
+    if fhv.layout not in ("POFA", "POFL"):
+        raise SceneError("ray casting requires a per-octant layout")
+    sh = _shading_for(fhv, materials, lights, fhv.pool.device)
+    cutoff = -1.0 if cfg.alpha_cutoff is None else float(cfg.alpha_cutoff)
+    rgba, hits, c = _probe(fhv, ray, RAYCAST_MODES.index(cfg.mode), cfg.splat_radius_world, sh, cutoff,
+                           cfg.shadow_epsilon, background, eye)
+    _merge(stats, c)
+    if hit_out is not None:
+        hit_out.extend(hits)
+    return rgba
+
+
+def shadow_transmittance(fhv, point, light, cfg: RaycastConfig, exclude_object_id: int | None = None,
+                         exclude_cell: int | None = None, stats: RaycastStats | None = None,
+                         alpha_table=None) -> float:
+    """Product of (1 - alpha) over the fragments between a point and a light
+    (fhv/raycast.py:408-453); fragments of the excluded (object id, leaf)
+    pair are skipped when both are given."""
+    dev = fhv.pool.device
+    if alpha_table is not None:
+        a = np.asarray(alpha_table, dtype=np.float64).reshape(-1)
+        z = np.zeros((len(a), 3))
+        sh = DeviceShading.from_arrays({"diffuse": z, "specular": z, "shininess": np.zeros(len(a)), "alpha": a},
+                                       [light], dev)
+    else:
+        sh = _shading_for(fhv, None, [light], dev)
+    p = torch.from_numpy(np.ascontiguousarray(np.asarray(point, dtype=np.float64).reshape(1, 3))).to(dev)
+    ex = exclude_object_id is not None and exclude_cell is not None
+    eo = torch.tensor([int(exclude_object_id)], dtype=torch.int64, device=dev) if ex else None
+    ec = torch.tensor([int(exclude_cell)], dtype=torch.int64, device=dev) if ex else None
+    tau = torch.empty(1, dtype=torch.float64, device=dev)
+    st = torch.zeros(4, dtype=torch.int64, device=dev)
+    rc = _lib.load().fhv_transmittance(_lib.ctx(dev), 1, _lib.ptr(p), 0, _lib.ptr(eo), _lib.ptr(ec), _volume(fhv),
+                                       sh.struct(), float(cfg.splat_radius_world), float(cfg.shadow_epsilon),
+                                       _lib.ptr(tau), _lib.ptr(st), _lib.stream_ptr(dev))
+    _lib.check(rc, "shadow_transmittance")
+    _merge(stats, st.cpu().tolist(), hits=False)
+    return float(tau.item())

@@ -17,8 +17,70 @@ from .scene import Camera, SceneError
 
 __all__ = ["GBuffer", "ImageBuffer", "Light", "composite_over", "deferred_baseline", "front_to_back_accumulate",
            "headlight",
-           "material_arrays", "read_float_dump", "read_ppm", "resolve_over_background", "splat_render",
-           "srgb_encode", "write_float_dump", "write_ppm"]
+           "material_arrays", "project_points", "read_float_dump", "read_ppm", "resolve_over_background", "shade",
+           "shade_many", "splat_render", "srgb_encode", "write_float_dump", "write_ppm"]
+
+
+def _dev_f64(a, dev, cols: int | None = 3) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        t = a.to(device=dev, dtype=torch.float64)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).to(dev)
+    return t.reshape(-1, cols).contiguous() if cols else t.reshape(-1).contiguous()
+
+
+def shade_many(points, normals, material_id, mats, lights, eye, device=None):
+    """Blinn-Phong over fragment arrays, channels clamped to [0, 1]
+    (fhv/render.py:120-156), on the device (fhv_shade).  ``mats`` is a
+    material_arrays() dict or a list of Materials.  NumPy inputs give a
+    NumPy (n, 3) result, CUDA tensors a CUDA tensor."""
+    from .device import default_device
+    on_dev = isinstance(points, torch.Tensor) and points.is_cuda
+    dev = points.device if on_dev else default_device(device)
+    p = _dev_f64(points, dev)
+    q = _dev_f64(normals, dev)
+    m = (material_id.to(device=dev, dtype=torch.int64) if isinstance(material_id, torch.Tensor)
+         else torch.from_numpy(np.ascontiguousarray(np.atleast_1d(np.asarray(material_id)).astype(np.int64))).to(dev))
+    m = m.reshape(-1).contiguous()
+    n = p.shape[0]
+    if q.shape[0] != n or m.numel() != n:
+        raise ValueError("shade_many: points, normals and material_id disagree in length")
+    sh = DeviceShading.from_arrays(mats, lights, dev) if isinstance(mats, dict) else DeviceShading(mats, lights, dev)
+    if n and (int(m.min()) < 0 or int(m.max()) >= sh.n_mats):
+        raise IndexError("shade_many: material id outside the material table")
+    out = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    e = host_f64(eye.cpu() if isinstance(eye, torch.Tensor) else eye).reshape(3)
+    rc = _lib.load().fhv_shade(_lib.ctx(dev), n, _lib.ptr(p), _lib.ptr(q), _lib.ptr(m), sh.n_mats, sh.struct(),
+                               e.ctypes.data, _lib.ptr(out), _lib.stream_ptr(dev))
+    _lib.check(rc, "shade_many")
+    return out if on_dev else out.cpu().numpy()
+
+
+def shade(position, normal, material, light, eye, device=None) -> np.ndarray:
+    """Blinn-Phong for a single fragment and light (fhv/render.py:159-165)."""
+    return shade_many(np.asarray(position, dtype=np.float64), np.asarray(normal, dtype=np.float64), np.array([0]),
+                      material_arrays([material]), [light], np.asarray(eye, dtype=np.float64), device)[0]
+
+
+def project_points(camera: Camera, points, device=None):
+    """Raster coordinates, [0, 1] depth and view distance of world points
+    (fhv/render.py:211-233), on the device (fhv_project_points): returns
+    (xr, yr, depth, zc) like the reference (NumPy in, NumPy out)."""
+    from .device import default_device
+    on_dev = isinstance(points, torch.Tensor) and points.is_cuda
+    dev = points.device if on_dev else default_device(device)
+    one_d = np.ndim(points) == 1 if not on_dev else points.dim() == 1
+    p = _dev_f64(points, dev)
+    n = p.shape[0]
+    outs = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(4)]
+    cam = host_f64(camera.scalars())
+    rc = _lib.load().fhv_project_points(_lib.ctx(dev), n, _lib.ptr(p), cam.ctypes.data, *[_lib.ptr(o) for o in outs],
+                                        _lib.stream_ptr(dev))
+    _lib.check(rc, "project_points")
+    if on_dev:
+        return tuple(o[0] if one_d else o for o in outs)
+    res = [o.cpu().numpy() for o in outs]
+    return tuple(float(r[0]) if one_d else r for r in res)
 
 
 def splat_render(pool, camera: Camera, lights, splat_radius_world: float, materials,

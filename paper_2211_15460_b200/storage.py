@@ -17,7 +17,9 @@ array bit-identical.  ``alloc="atomic"`` is the paper's GPU allocator
 """
 from __future__ import annotations
 
+import ctypes
 import struct
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -30,11 +32,14 @@ from .scene import Material, Scene
 
 __all__ = [
     "FhvError", "FhvPofa", "FhvPofl", "FhvPpfl", "FragmentPool", "FragmentRecord", "MAX_LEVELS",
-    "OccupancyPyramid", "PixelDirectory", "PofaBuildError", "PofaDirectory", "PoflDirectory", "RECORD_DTYPE",
-    "RECORD_SIZE_ALIGNED", "RECORD_SIZE_PACKED", "build_pofl", "build_ppfl", "cell_box", "cell_code", "cell_of",
-    "load_snapshot", "memory_report", "morton_decode", "morton_encode", "pofa_build", "rebuild_pofl_as_pofa",
-    "save_snapshot", "snapshot_bytes",
+    "OccupancyPyramid", "PixelDirectory", "PofaBuildError", "PofaDirectory", "PofaWriteSink", "PoflDirectory",
+    "PoflSink", "PpflSink", "CountingSink", "RECORD_DTYPE", "RECORD_SIZE_ALIGNED", "RECORD_SIZE_PACKED",
+    "build_pofl", "build_ppfl", "cell_box", "cell_code", "cell_of", "chain_indices", "load_snapshot",
+    "memory_report", "morton_decode", "morton_encode", "pofa_build", "pofl_insert", "ppfl_insert",
+    "rebuild_pofl_as_pofa", "save_snapshot", "snapshot_bytes",
 ]
+
+_alloc_lock = threading.Lock()
 
 MAX_LEVELS = 20
 RECORD_DTYPE = np.dtype([("position", "<f4", (3,)), ("normal", "<f4", (3,)), ("material_id", "<u4"),
@@ -184,6 +189,16 @@ class FragmentPool:
         out.in_unit_cube = self.in_unit_cube
         return out
 
+    def alloc_block(self, n: int) -> int:
+        """Reserve n slots (fhv/storage.py:207-213): returns the first index;
+        the counter keeps counting past capacity and sets ``overflowed``."""
+        with _alloc_lock:
+            start = self.next_free
+            self.next_free += int(n)
+            if self.next_free > self.capacity:
+                self.overflowed = True
+            return start
+
     @property
     def stored_count(self) -> int:
         return min(self.next_free, self.capacity)
@@ -230,6 +245,11 @@ class PixelDirectory:
     height: int
     heads: torch.Tensor  # int32 (h*w,), -1 = empty
 
+    @staticmethod
+    def empty(width: int, height: int, device=None) -> "PixelDirectory":
+        return PixelDirectory(width, height, torch.full((width * height,), -1, dtype=torch.int32,
+                                                        device=default_device(device)))
+
     def head(self, x: int, y: int) -> int:
         return int(self.heads[y * self.width + x])
 
@@ -238,6 +258,11 @@ class PixelDirectory:
 class PoflDirectory:
     levels: int
     heads: torch.Tensor  # int32 (8^L,)
+
+    @staticmethod
+    def empty(levels: int, device=None) -> "PoflDirectory":
+        _check_levels(levels)
+        return PoflDirectory(levels, torch.full((8 ** levels,), -1, dtype=torch.int32, device=default_device(device)))
 
 
 @dataclass
@@ -279,6 +304,39 @@ class OccupancyPyramid:
 
     def mask(self, level: int, node: int) -> int:
         return int(self.data[_pyr_offsets(self.leaf_levels)[level] + node])
+
+    def set_paths(self, codes) -> None:
+        """Mark the root paths of leaf codes occupied (fhv/storage.py:294-301), on the device."""
+        dev = self.data.device
+        c = (codes.to(device=dev, dtype=torch.int64) if isinstance(codes, torch.Tensor)
+             else torch.from_numpy(np.ascontiguousarray(np.atleast_1d(np.asarray(codes, dtype=np.int64)))).to(dev))
+        c = c.reshape(-1).contiguous()
+        rc = _lib.load().fhv_set_paths(_lib.ctx(dev), self.leaf_levels, c.numel(), _lib.ptr(c), _lib.ptr(self.data),
+                                       _lib.stream_ptr(dev))
+        if rc == _lib.FHV_BAD_ARGS:
+            raise FhvError("set_paths: leaf code outside [0, 8^levels)")
+        _lib.check(rc, "set_paths")
+
+    @staticmethod
+    def from_leaf_occupancy(occupied, leaf_levels: int, device=None) -> "OccupancyPyramid":
+        """Bottom-up masks from a leaf occupancy vector (fhv/storage.py:316-328)."""
+        _check_levels(leaf_levels)
+        if leaf_levels < 1:
+            raise FhvError("octree needs at least one level")
+        if isinstance(occupied, torch.Tensor) and occupied.is_cuda:
+            dev = occupied.device
+            occ = occupied.to(torch.bool).to(torch.uint8).reshape(-1).contiguous()
+        else:
+            dev = default_device(device)
+            occ = torch.from_numpy(np.ascontiguousarray(np.asarray(occupied, dtype=bool).reshape(-1))).to(dev)
+            occ = occ.to(torch.uint8)
+        if occ.numel() != 8 ** leaf_levels:
+            raise FhvError("occupancy length != 8^levels")
+        pyr = OccupancyPyramid.uninitialized(leaf_levels, dev)
+        rc = _lib.load().fhv_pyramid_from_occupancy(_lib.ctx(dev), leaf_levels, _lib.ptr(occ), _lib.ptr(pyr.data),
+                                                    _lib.stream_ptr(dev))
+        _lib.check(rc, "from_leaf_occupancy")
+        return pyr
 
     def leaf_occupancy(self) -> torch.Tensor:
         last = self.levels[-1].to(torch.int32)
@@ -352,12 +410,30 @@ class FhvPofa:
         return torch.nonzero(self.directory.counts > 0).reshape(-1).to(torch.int64)
 
 
-def _chain(heads, prev, key) -> np.ndarray:
-    out, i = [], int(heads[key])
-    while i >= 0:
-        out.append(i)
-        i = int(prev[i])
-    return np.asarray(out, dtype=np.int64)
+def chain_indices(heads, prev, code: int) -> np.ndarray:
+    """Pool indices reachable from a head, most recent first
+    (fhv/storage.py:479-486); walks the device list (fhv_chain_indices)."""
+    if not (isinstance(heads, torch.Tensor) and heads.is_cuda):
+        raise FhvError("chain_indices: heads must be a CUDA tensor of this package")
+    dev = heads.device
+    h = heads if heads.dtype == torch.int32 and heads.is_contiguous() else heads.to(torch.int32).contiguous()
+    p = prev if prev.dtype == torch.int32 and prev.is_contiguous() else prev.to(dev, torch.int32).contiguous()
+    n = ctypes.c_int64(0)
+    lib = _lib.load()
+    cap = 64
+    while True:
+        out = torch.empty(cap, dtype=torch.int64, device=dev)
+        rc = lib.fhv_chain_indices(_lib.ctx(dev), _lib.ptr(h), h.numel(), _lib.ptr(p), p.numel(), int(code), cap,
+                                   _lib.ptr(out), ctypes.byref(n), _lib.stream_ptr(dev))
+        if rc == _lib.FHV_BAD_ARGS:
+            raise FhvError(f"chain_indices: bad key {code} or corrupt chain")
+        _lib.check(rc, "chain_indices")
+        if n.value <= cap:
+            return out[:n.value].cpu().numpy()
+        cap = int(n.value)
+
+
+_chain = chain_indices
 
 
 # ---------------------------------------------------------------------------
@@ -650,3 +726,155 @@ def load_snapshot(path, materials=None, device=None):
         return FhvPofa(PofaDirectory(levels, dev32(offs).view(torch.uint32), dev32(cnts).view(torch.uint32)),
                        pyramid, pool, h, materials=materials)
     raise FhvError(f"unknown snapshot layout {layout!r}")
+
+
+# ---------------------------------------------------------------------------
+# per-fragment / per-batch insertion (fhv/storage.py:331-476): the sink
+# objects capture_pass can feed and the single-fragment inserts.  Records are
+# written into the device pool; chaining, cursor assignment and occupancy run
+# in the operator kernels (kernels.linked_insert / pofa_scatter, set_paths).
+# The bulk builders above never go through these.
+
+
+def _dev_rows(a, dev, dtype) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a).astype(
+        {torch.float32: np.float32, torch.int64: np.int64}[dtype]))).to(dev)
+
+
+def _store_split(pool: FragmentPool, n: int) -> tuple:
+    start = pool.alloc_block(n)
+    return start, min(n, max(0, pool.capacity - start))
+
+
+def _write_records(pool: FragmentPool, dest, batch, stored: int) -> np.ndarray:
+    """Write batch[:stored] at pool slots ``dest`` (a slice or index tensor); returns f32 positions (host)."""
+    dev = pool.device
+    pos32 = np.asarray(batch.world_position[:stored], dtype=np.float64).astype(np.float32).reshape(-1, 3)
+    nrm32 = np.asarray(batch.world_normal[:stored], dtype=np.float64).astype(np.float32).reshape(-1, 3)
+    pool.position[dest] = torch.from_numpy(pos32).to(dev)
+    pool.normal[dest] = torch.from_numpy(nrm32).to(dev)
+    pool.material_id.view(torch.int32)[dest] = int(np.uint32(batch.material_id).view(np.int32))
+    pool.object_id.view(torch.int32)[dest] = int(np.uint32(batch.object_id).view(np.int32))
+    return pos32
+
+
+class PpflSink:
+    """capture_pass sink into a per-pixel linked-list layout (fhv/storage.py:356-373)."""
+
+    def __init__(self, directory: PixelDirectory, pool: FragmentPool):
+        self.directory = directory
+        self.pool = pool
+        self._lock = threading.Lock()
+
+    def __call__(self, batch) -> None:
+        from . import kernels
+        with self._lock:
+            start, stored = _store_split(self.pool, len(batch))
+            if stored == 0:
+                return
+            _write_records(self.pool, slice(start, start + stored), batch, stored)
+            keys = (np.asarray(batch.raster_y[:stored], dtype=np.int64) * self.directory.width
+                    + np.asarray(batch.raster_x[:stored], dtype=np.int64))
+            kernels.linked_insert(keys, self.directory.heads, self.pool.prev_index, start)
+
+
+class PoflSink:
+    """capture_pass sink into a per-octant linked-list layout (fhv/storage.py:376-395)."""
+
+    def __init__(self, directory: PoflDirectory, pyramid: OccupancyPyramid, pool: FragmentPool):
+        self.directory = directory
+        self.pyramid = pyramid
+        self.pool = pool
+        self._lock = threading.Lock()
+
+    def __call__(self, batch) -> None:
+        from . import kernels
+        with self._lock:
+            start, stored = _store_split(self.pool, len(batch))
+            if stored == 0:
+                return
+            pos32 = _write_records(self.pool, slice(start, start + stored), batch, stored)
+            codes = np.atleast_1d(cell_code(pos32.astype(np.float64), self.directory.levels))
+            kernels.linked_insert(codes, self.directory.heads, self.pool.prev_index, start)
+            self.pyramid.set_paths(codes)
+
+
+class CountingSink:
+    """First POFA pass: fragments per leaf (fhv/storage.py:398-410); ``counts``
+    is an int64 device tensor of 8^levels."""
+
+    def __init__(self, levels: int, device=None):
+        self.levels = levels
+        self.counts = torch.zeros(8 ** levels, dtype=torch.int64, device=default_device(device))
+        self._lock = threading.Lock()
+
+    def __call__(self, batch) -> None:
+        pos32 = np.asarray(batch.world_position, dtype=np.float64).astype(np.float32).reshape(-1, 3)
+        codes = np.atleast_1d(cell_code(pos32.astype(np.float64), self.levels))
+        c = torch.from_numpy(np.ascontiguousarray(codes, dtype=np.int64)).to(self.counts.device)
+        with self._lock:
+            self.counts.index_add_(0, c, torch.ones_like(c))
+
+
+class PofaWriteSink:
+    """Second POFA pass: scatter fragments to their leaf ranges (fhv/storage.py:413-439)."""
+
+    def __init__(self, directory: PofaDirectory, pool: FragmentPool):
+        self.directory = directory
+        self.pool = pool
+        self.cursors = torch.zeros(directory.counts.numel(), dtype=torch.int32,
+                                   device=directory.counts.device).view(torch.uint32)
+        self._lock = threading.Lock()
+
+    def __call__(self, batch) -> None:
+        from . import kernels
+        with self._lock:
+            n = len(batch)
+            pos32 = np.asarray(batch.world_position, dtype=np.float64).astype(np.float32).reshape(-1, 3)
+            codes = np.atleast_1d(cell_code(pos32.astype(np.float64), self.directory.levels))
+            dest = torch.empty(n, dtype=torch.int64, device=self.pool.device)
+            bad = kernels.pofa_scatter(codes, self.directory.offsets, self.directory.counts, self.cursors, dest)
+            if bad >= 0:
+                raise PofaBuildError(f"octant {int(codes[bad])} received more fragments than counted")
+            self.pool.alloc_block(n)
+            _write_records(self.pool, dest, batch, n)
+            self.pool.prev_index[dest] = -1
+
+
+def ppfl_insert(directory: PixelDirectory, pool: FragmentPool, frag) -> int | None:
+    """Insert one fragment; its pool index, or None on overflow (fhv/storage.py:442-458)."""
+    from . import kernels
+    x, y = frag.raster_xy
+    if not (0 <= x < directory.width and 0 <= y < directory.height):
+        raise FhvError(f"raster position {frag.raster_xy} out of range")
+    idx = pool.alloc_block(1)
+    if idx >= pool.capacity:
+        return None
+    _write_records(pool, slice(idx, idx + 1), _One(frag), 1)
+    kernels.linked_insert(np.array([y * directory.width + x], dtype=np.int64), directory.heads, pool.prev_index, idx)
+    return idx
+
+
+def pofl_insert(directory: PoflDirectory, pyramid: OccupancyPyramid, pool: FragmentPool, frag) -> int | None:
+    """Insert one fragment keyed by its Morton leaf; updates occupancy (fhv/storage.py:461-476)."""
+    from . import kernels
+    idx = pool.alloc_block(1)
+    if idx >= pool.capacity:
+        return None
+    pos32 = _write_records(pool, slice(idx, idx + 1), _One(frag), 1)
+    code = int(np.atleast_1d(cell_code(pos32[0].astype(np.float64), directory.levels))[0])
+    kernels.linked_insert(np.array([code], dtype=np.int64), directory.heads, pool.prev_index, idx)
+    pyramid.set_paths(np.array([code], dtype=np.int64))
+    return idx
+
+
+class _One:
+    """An EmittedFragment seen as a one-row batch."""
+
+    def __init__(self, frag):
+        self.world_position = np.asarray(frag.world_position, dtype=np.float64).reshape(1, 3)
+        self.world_normal = np.asarray(frag.world_normal, dtype=np.float64).reshape(1, 3)
+        self.material_id = frag.material_id
+        self.object_id = frag.object_id
