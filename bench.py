@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--composite", default="auto", choices=("auto", "peer", "allreduce"),
                     help="multi-GPU splat composite: peer memory (fhv_splat_peer over NVLink P2P) or NCCL "
                          "all-reduces; auto = peer when the peer mappings can be set up")
+    ap.add_argument("--sync-steps", action="store_true",
+                    help="wait for each pofa_build on the host (default: asynchronous steps, tickets checked)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="few steps, no clocks/e2e/cpu (for ncu)")
     return ap.parse_args()
@@ -498,16 +500,41 @@ def main():
             return vol
     else:
         composite = None
+        # single GPU: after the warm-up every step is enqueued without a host
+        # wait (pofa_build(sync=False): pool sized by the previous exact total,
+        # outcome in a pinned ticket); every ticket of a timed loop is checked
+        # after its closing sync -- a wrong speculation fails the run
+        tickets = torch.zeros((4 * (args.steps + 4), 4), dtype=torch.int64).pin_memory()
+        used: list = []
 
         def step(tris=ds, out=img):
-            vol = fhv.pofa_build(scene, strat, cfg, L, exact_order=args.exact_order, device=dev, tris=tris)
+            asynchronous = not args.sync_steps and len(used) < len(tickets)
+            tk = tickets[len(used)] if asynchronous else None
+            vol = fhv.pofa_build(scene, strat, cfg, L, exact_order=args.exact_order, device=dev, tris=tris,
+                                 sync=not asynchronous, ticket=tk)
+            if vol.pending is not None:
+                used.append(vol.pending[:2])  # the ticket only: volumes are freed step by step
             fhv.splat_render(vol.pool, view, w["lights"], w["radius"], scene.materials, out=out, packed=args.packed,
                              shading=shading)
             return vol
 
+        def check_tickets():
+            torch.cuda.synchronize()
+            for tk, guess in used:
+                rc = fhv.storage.ticket_status(tk, guess)
+                if rc != 0:
+                    raise RuntimeError(f"asynchronous pofa_build step failed its ticket check (status {rc})")
+            n = len(used)
+            used.clear()
+            return n
+
+    if world > 1:
+        def check_tickets():
+            return 0
     for _ in range(args.warmup):
         vol = step()
     torch.cuda.synchronize()
+    check_tickets()
     n_frags = vol.total if world > 1 else vol.pool.next_free
 
     def barrier():
@@ -528,6 +555,7 @@ def main():
             vol = step()
         e1.record(stream)
         barrier()
+    async_checked = check_tickets()
     ms = e0.elapsed_time(e1)
     gpu_launches = _lib.launches(dev) - launches0
     # per-kernel CUDA events on the launching stream (LaunchScope, fhv_abi.cu)
@@ -540,6 +568,7 @@ def main():
         vol = step()
     ep1.record(stream)
     barrier()
+    check_tickets()
     ms_profiled = ep0.elapsed_time(ep1)
     prof = _lib.prof_collect(dev)
     _lib.prof_enable(dev, False)
@@ -661,6 +690,7 @@ def main():
             stream.wait_event(e_out[K - 2])
         e3.record(stream)
         barrier()
+        check_tickets()
         ms_e2e = e2.elapsed_time(e3)
         t2 = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
         if world > 1:
@@ -694,7 +724,9 @@ def main():
                 "config": dict(CONFIG, fragments=n_frags,
                                parallelism=f"morton-range shards x{world} (NCCL)" if world > 1 else "single",
                                composite=composite if world > 1 else None,
-                               exact_order=bool(args.exact_order), splat="packed" if args.packed else "exact"),
+                               exact_order=bool(args.exact_order), splat="packed" if args.packed else "exact",
+                               host="asynchronous steps: pofa_build(sync=False), all %d tickets verified after "
+                                    "the timed loop" % async_checked if async_checked else "synchronous steps"),
                 "novel_view_fps": 1e3 / recon_ms if recon_ms else None,
                 "capture_frag_per_s": n_frags / (capture_ms / 1e3) if capture_ms else None,
                 "step_gbs": step_bytes / (ms_step / 1e3) / 1e9, "step_bytes": step_bytes,

@@ -52,6 +52,8 @@ enum {
   FHV_TOO_MANY = 8,       /* FhvError: >= 2^32 fragments (fhv/storage.py:604-606) */
   FHV_SPLAT_BIG = 9,      /* SceneError: splat footprint > 4096 px (fhv/render.py:285-286) */
   FHV_NEED_POOL = 10,     /* fhv_pofa_build: pool smaller than the exact count; *total says how big */
+  FHV_STALE = 11,         /* fhv_ticket_check: an asynchronous build ran on a wrong speculation (pool size or
+                             work-item plan); its outputs are invalid -- rebuild synchronously */
 };
 
 /* capture flags */
@@ -224,6 +226,22 @@ int fhv_pofa_scatter(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg
 int fhv_pofa_build(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int32_t levels,
                    uint32_t *counts, uint32_t *offsets, uint8_t *pyramid, fhv_pool_t *pool, int32_t flags,
                    int64_t *total, void *stream);
+
+/* pofa_build fully asynchronous: the same pass 1 + directory + pass 2 as
+   fhv_pofa_build, enqueued without any host wait, into a pool whose capacity
+   is the caller's guess of the exact total (e.g. the total of the previous
+   build of the same scene).  The outcome lands in *ticket (pinned host
+   memory, written by a stream-ordered copy); after synchronising the stream,
+   fhv_ticket_check(ticket, pool capacity) returns FHV_OK when the pool holds
+   exactly the build's records, FHV_STALE when the speculation was wrong
+   (outputs invalid: rebuild with fhv_pofa_build), or the build's own error. */
+typedef struct {
+  int64_t status, frags_total, scan_total, alloc;
+} fhv_ticket_t;
+int fhv_pofa_build_async(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int32_t levels,
+                         uint32_t *counts, uint32_t *offsets, uint8_t *pyramid, fhv_pool_t *pool, int32_t flags,
+                         fhv_ticket_t *ticket, void *stream);
+int fhv_ticket_check(const fhv_ticket_t *ticket, int64_t expect_total);
 
 /* rebuild_pofl_as_pofa (fhv/storage.py:624-652): repack the first n records
    of a linked-list pool into per-leaf contiguous ranges (Morton order, pool

@@ -20,6 +20,7 @@ c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, cty
 FHV_OK, FHV_OVERFLOW, FHV_PASS_MISMATCH, FHV_BAD_ARGS, FHV_CUDA_ERROR = 0, 1, 2, 3, 4
 FHV_RANGE, FHV_BASIS, FHV_NOMEM, FHV_TOO_MANY, FHV_SPLAT_BIG = 5, 6, 7, 8, 9
 FHV_NEED_POOL = 10
+FHV_STALE = 11
 FHV_ALLOC_ATOMIC, FHV_EXACT_ORDER = 1, 2
 FHV_SPLAT_PACKED, FHV_SPLAT_NOSYNC = 1, 2
 
@@ -117,6 +118,9 @@ _SIGS = {
                                        _P(c_i64), _P(c_i64), c_vp]),
     "fhv_op_linked_insert": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp]),
     "fhv_op_pofa_scatter": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, _P(c_i64), c_vp]),
+    "fhv_pofa_build_async": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, c_vp, c_vp, c_vp, _P(Pool), c_i32,
+                                            c_vp, c_vp]),
+    "fhv_ticket_check": (ctypes.c_int, [c_vp, c_i64]),
     "fhv_chain_indices": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, _P(c_i64), c_vp]),
     "fhv_set_paths": (ctypes.c_int, [c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "fhv_pyramid_from_occupancy": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp]),

@@ -733,7 +733,11 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
   uint32_t* own_cnt = own_all[wib];
   uint32_t* ijob = ijob_all[wib];
   const unsigned below = (1u << lane) - 1u;
-  if (n_dev && (long long)*n_dev < n_items) n_items = (long long)*n_dev;  // speculative launch (cap >= count)
+  if (n_dev) {  // speculative launch: run the true count, or flag a plan that was too small
+    const long long nd = (long long)*n_dev;
+    if (nd > n_items && blockIdx.x == 0 && threadIdx.x == 0) raise_status(&ctl->status, FHV_RETRY_ITEMS);
+    if (nd < n_items) n_items = nd;
+  }
   const long long n_groups = (n_items + 31) / 32;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   RasterState<kMode, kAtomicAlloc> st;
@@ -908,7 +912,11 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
   CoverS* cs = cs_all[wib];
   uint32_t* own_cnt = own_all[wib];
   uint32_t* ijob = ijob_all[wib];
-  if (n_dev && (long long)*n_dev < n_items) n_items = (long long)*n_dev;
+  if (n_dev) {  // speculative launch: run the true count, or flag a plan that was too small
+    const long long nd = (long long)*n_dev;
+    if (nd > n_items && blockIdx.x == 0 && threadIdx.x == 0) raise_status(&ctl->status, FHV_RETRY_ITEMS);
+    if (nd < n_items) n_items = nd;
+  }
   const long long n_groups = (n_items + 31) / 32;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   RasterState<kMode, kAtomicAlloc> st;
@@ -1852,6 +1860,58 @@ extern "C" int fhv_pofa_build(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_ca
   if (!pool || pool->capacity < ctx->pass1_total) return FHV_NEED_POOL;  // finish with fhv_pofa_scatter
   if (rc != FHV_OK) return rc;
   if ((long long)ctx->ctl_host->alloc != ctx->pass1_total) return FHV_PASS_MISMATCH;
+  return FHV_OK;
+}
+
+namespace fhv {
+namespace {
+// the async build's outcome, staged in ctl->spare[4..7] for the D2H copy
+__global__ void k_ticket(Control* ctl) {
+  ctl->spare[4] = (unsigned long long)(long long)ctl->status;
+  ctl->spare[5] = ctl->frags_total;
+  ctl->spare[6] = ctl->scan_total;
+  ctl->spare[7] = ctl->alloc;
+}
+}  // namespace
+}  // namespace fhv
+
+extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
+                                    int32_t levels, uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
+                                    fhv_pool_t* pool, int32_t flags, fhv_ticket_t* ticket, void* stream) {
+  if (!ctx || !counts || !offsets || !pyramid || !ticket || levels < 1 || levels > 10) return FHV_BAD_ARGS;
+  int rc = validate(tris, cfg);
+  if (rc) return rc;
+  if (!pool || pool->capacity <= 0 || !pool->pos || !pool->nrm || !pool->mat || !pool->obj || !pool->prev)
+    return FHV_BAD_ARGS;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned long long n_leaves = 1ull << (3 * levels);
+  const bool ranks = (flags & FHV_EXACT_ORDER) != 0;
+  CaptureParams p;
+  // speculative item plan when this ctx has one for the job count (else plan() syncs once)
+  if ((rc = pofa_count_async(ctx, tris, cfg, levels, nullptr, counts, s, p, true, ranks))) return rc;
+  if ((rc = fhv_pofa_shard_directory_nocheck(ctx, levels, counts, offsets, pyramid, s))) return rc;
+  if (!ranks && (rc = check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total,
+                                                      sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s))))
+    return rc;
+  if ((rc = pofa_scatter_async(ctx, p, levels, 0, n_leaves, counts, offsets, 0, pool, flags, s))) return rc;
+  {
+    LaunchScope L_(ctx, kStScan, s);
+    k_ticket<<<1, 1, 0, s>>>(ctx->ctl);
+  }
+  if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  // pass-1 bookkeeping for a follow-up fhv_pofa_scatter is not kept: the
+  // ticket is the only result
+  ctx->pass1_levels = -1;
+  return check_cuda(ctx, cudaMemcpyAsync(ticket, &ctx->ctl->spare[4], sizeof(fhv_ticket_t), cudaMemcpyDefault, s));
+}
+
+extern "C" int fhv_ticket_check(const fhv_ticket_t* t, int64_t expect_total) {
+  if (!t) return FHV_BAD_ARGS;
+  if (t->status == FHV_RETRY_ITEMS || t->status == FHV_NEED_POOL) return FHV_STALE;
+  if (t->status) return (int)t->status;
+  if (t->frags_total >= (1LL << 32)) return FHV_TOO_MANY;
+  if (t->scan_total != t->frags_total || t->alloc != t->frags_total) return FHV_PASS_MISMATCH;
+  if (t->frags_total != expect_total) return FHV_STALE;
   return FHV_OK;
 }
 

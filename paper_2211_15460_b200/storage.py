@@ -406,6 +406,25 @@ class FhvPofa:
         off = int(self.directory.offsets[code])
         return np.arange(off, off + int(self.directory.counts[code]), dtype=np.int64)
 
+    pending = None  # (ticket, guessed total, synchronous rebuild) of an asynchronous pofa_build
+
+    def wait(self) -> "FhvPofa":
+        """Finish an asynchronous build: synchronise, check its ticket, and
+        rebuild synchronously in place if the speculation was wrong.  Raises
+        the build's own error otherwise."""
+        if self.pending is None:
+            return self
+        torch.cuda.current_stream(self.pool.device).synchronize()
+        rc = check_ticket(self)
+        rebuild = self.pending[2]
+        self.pending = None
+        if rc == _lib.FHV_STALE:
+            fresh = rebuild()
+            self.directory, self.pyramid, self.pool, self.stats = fresh.directory, fresh.pyramid, fresh.pool, fresh.stats
+        else:
+            _lib.check(rc, "pofa_build")
+        return self
+
     def occupied_leaves(self) -> torch.Tensor:
         return torch.nonzero(self.directory.counts > 0).reshape(-1).to(torch.int64)
 
@@ -501,12 +520,20 @@ def build_pofl(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
 
 
 def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int, threads: int = 1, *,
-               exact_order: bool = False, device=None, tris=None) -> FhvPofa:
+               exact_order: bool = False, device=None, tris=None, sync: bool = True,
+               ticket: torch.Tensor | None = None) -> FhvPofa:
     """Two-pass per-octant arrays (fhv/storage.py:590-621): per-leaf histogram,
     exclusive scan (+ pyramid), exact pool, scatter into leaf ranges.
     ``tris``: a DeviceScene already holding this scene's triangle arrays (e.g.
     one of several buffers a pipelined caller fills asynchronously); default:
-    the scene's cached upload."""
+    the scene's cached upload.
+
+    ``sync=False`` (once a build of the same scene / plan has run): nothing
+    waits for the device -- the pool is sized by the last exact total and the
+    outcome is written to ``ticket`` (pinned int64[4], allocated if omitted);
+    call :meth:`FhvPofa.wait` (or :func:`check_ticket` after a stream sync)
+    before trusting the volume on the host.  ``wait`` rebuilds synchronously
+    in place when the speculation was wrong."""
     if levels < 1:
         raise FhvError("octree needs at least one level")
     if levels > 11:
@@ -529,6 +556,20 @@ def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     guesses = ds.__dict__.setdefault("_pofa_totals", {})
     gkey = (plan.key, levels)
     guess = guesses.get(gkey)
+    if not sync and guess:
+        pool = FragmentPool(guess, dev, fill_prev=False)
+        tk = ticket if ticket is not None else torch.zeros(4, dtype=torch.int64).pin_memory()
+        rc = lib.fhv_pofa_build_async(_lib.ctx(dev), ds.struct(), c, levels, _lib.ptr(counts), _lib.ptr(offsets),
+                                      _lib.ptr(pyr.data), pool.struct(), _lib.FHV_EXACT_ORDER if exact_order else 0,
+                                      c_vp_of(tk), _lib.stream_ptr(dev))
+        _lib.check(rc, "pofa_build")
+        pool.next_free = guess
+        pool.in_unit_cube = True
+        vol = FhvPofa(PofaDirectory(levels, offsets, counts), pyr, pool, int(cfg.resolution[1]), plan.stats(guess),
+                      scene.materials)
+        vol.pending = (tk, guess, lambda: pofa_build(scene, strategy, cfg, levels, threads, exact_order=exact_order,
+                                                     device=device, tris=tris))
+        return vol
     pool = FragmentPool(guess, dev, fill_prev=False) if guess is not None else None  # pass 2 writes every prev
     tr = ds.struct()
     rc = lib.fhv_pofa_build(cx, tr, c, levels, _lib.ptr(counts), _lib.ptr(offsets), _lib.ptr(pyr.data),
@@ -545,6 +586,23 @@ def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     pool.in_unit_cube = True
     return FhvPofa(PofaDirectory(levels, offsets, counts), pyr, pool, int(cfg.resolution[1]),
                    plan.stats(pool.next_free), scene.materials)
+
+
+def c_vp_of(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def check_ticket(vol) -> int:
+    """Status of an asynchronous pofa_build (the stream must have been
+    synchronised): FHV_OK, FHV_STALE (speculation wrong, outputs invalid) or
+    the build's own error code."""
+    tk, guess, _ = vol.pending
+    return ticket_status(tk, guess)
+
+
+def ticket_status(ticket: torch.Tensor, guess: int) -> int:
+    """fhv_ticket_check of one pinned ticket against the pool size it was built with."""
+    return int(_lib.load().fhv_ticket_check(c_vp_of(ticket), int(guess)))
 
 
 def _plan_cfg(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig):

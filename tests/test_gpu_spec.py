@@ -6,6 +6,7 @@ exactly.  Each case alternates small / large windows with equal triangle
 counts and checks the results against the oracle."""
 import numpy as np
 import pytest
+import torch
 
 import paper_2211_15460_b200 as fhv
 from oracle import oracle as orc
@@ -71,3 +72,84 @@ def test_pofa_pool_guess_too_small_is_refilled():
     ref = orc.pofa_build(s, ns, _cfg(s, 256), 5)
     assert a.pool.next_free < b.pool.next_free == ref["next_free"]
     assert np.array_equal(b.directory.offsets.cpu().numpy(), ref["offsets"])
+
+
+def _fresh_ctx(fn):
+    """Run fn in a new host thread: _lib keeps one scratch context per (device,
+    thread), so the speculative item planner starts from nothing."""
+    import threading
+    out = {}
+
+    def run():
+        try:
+            out["v"] = fn()
+        except BaseException as e:  # noqa: BLE001
+            out["e"] = e
+    t = threading.Thread(target=run)
+    t.start()
+    t.join()
+    if "e" in out:
+        raise out["e"]
+    return out["v"]
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_item_plan_too_small_is_retried_on_a_fresh_context(exact):
+    """32 -> 256 with a context that has only ever planned res 32: the
+    speculative plan is short by far; the build must notice and re-plan."""
+    s = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+
+    def run():
+        out = []
+        for res in (32, 256, 32, 256):
+            v = fhv.pofa_build(s, ns, _cfg(s, res), 5, exact_order=exact)
+            out.append((v.pool.next_free, v.directory.counts.cpu().numpy(), v.pool.numpy()))
+        return out
+    got = _fresh_ctx(run)
+    for (n, counts, h), res in zip(got, (32, 256, 32, 256)):
+        ref = orc.pofa_build(s, ns, _cfg(s, res), 5)
+        assert n == ref["next_free"]
+        assert np.array_equal(counts, ref["counts"])
+        if exact:
+            for k in ("position", "normal", "material_id", "object_id", "prev_index"):
+                assert np.array_equal(h[k], ref["pool"][k]), (res, k)
+
+
+def _same(a, b):
+    assert a.pool.next_free == b.pool.next_free
+    assert np.array_equal(a.directory.counts.cpu().numpy(), b.directory.counts.cpu().numpy())
+    assert np.array_equal(a.directory.offsets.cpu().numpy(), b.directory.offsets.cpu().numpy())
+    assert np.array_equal(a.pyramid.data.cpu().numpy(), b.pyramid.data.cpu().numpy())
+    ha, hb = a.pool.numpy(), b.pool.numpy()
+    for k in ("position", "normal", "material_id", "object_id", "prev_index"):
+        assert np.array_equal(ha[k], hb[k]), k
+
+
+def test_async_pofa_build_matches_sync():
+    s = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+    cfg = _cfg(s, 128)
+    ref = fhv.pofa_build(s, ns, cfg, 5, exact_order=True)
+    vols = [fhv.pofa_build(s, ns, cfg, 5, exact_order=True, sync=False) for _ in range(3)]
+    assert all(v.pending is not None for v in vols)
+    for v in vols:
+        v.wait()
+        assert v.pending is None
+        _same(v, ref)
+
+
+@pytest.mark.parametrize("delta", [-7, 5])
+def test_async_pofa_build_wrong_guess_is_rebuilt(delta):
+    s = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+    cfg = _cfg(s, 96)
+    ref = fhv.pofa_build(s, ns, cfg, 5, exact_order=True)
+    ds = fhv.device.device_scene(s)
+    key = next(k for k in ds._pofa_totals if k[1] == 5 and k[0][2] == tuple(cfg.resolution))
+    ds._pofa_totals[key] = ref.pool.next_free + delta  # a wrong speculation
+    v = fhv.pofa_build(s, ns, cfg, 5, exact_order=True, sync=False)
+    torch.cuda.synchronize()
+    assert fhv.storage.check_ticket(v) == fhv._lib.FHV_STALE
+    v.wait()
+    _same(v, ref)
