@@ -612,8 +612,11 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
     pofa_leader = __ffs(pofa_grp) - 1;
     const unsigned long long lc = live ? code - p.cell_lo : 0ull;
     if (live) {
-      pofa_cnt = __ldg(&o.counts[lc]);
+      // count = next offset - offset: the two words share a 32-B sector
+      // almost always, so the counts array is not read at all (the last leaf
+      // of the range has no successor and reads its count)
       pofa_off = __ldg(&o.offsets[lc]);
+      pofa_cnt = lc + 1 < p.cell_hi - p.cell_lo ? __ldg(&o.offsets[lc + 1]) - pofa_off : __ldg(&o.counts[lc]);
     }
     if (live && (int)lane == pofa_leader) pofa_base = atomicAdd(&o.cursors[lc], (uint32_t)__popc(pofa_grp));
   }
