@@ -163,13 +163,15 @@ def load(require_cuda: bool = True):
 
 
 def ctx(device: torch.device):
-    """Scratch context of (device, calling host thread), created on first use.
-    A context is single-threaded (the header's contract), so host threads that
-    share a device -- e.g. the loopback shards of shard.ThreadComm -- each get
-    their own."""
+    """Scratch context of (device, calling host thread, current stream),
+    created on first use.  A context is single-stream (the header's contract:
+    its control block and scratch are reused call after call), so host
+    threads that share a device -- e.g. the loopback shards of
+    shard.ThreadComm -- and work issued on different streams of one thread --
+    e.g. a capture overlapping the previous step's splat -- each get their own."""
     lib = load()
     idx = device.index if device.index is not None else torch.cuda.current_device()
-    key = (idx, threading.get_ident())
+    key = (idx, threading.get_ident(), torch.cuda.current_stream(idx).cuda_stream)
     with _lock:
         c = _ctxs.get(key)
         if c is None:
@@ -177,29 +179,50 @@ def ctx(device: torch.device):
                 c = lib.fhv_ctx_create()
             if not c:
                 raise MemoryError("fhv_ctx_create failed")
+            if _prof_on.get(idx):
+                lib.fhv_prof_enable(c, 1)
             _ctxs[key] = c
     return c
 
 
+_prof_on: dict = {}
+
+
+def _device_ctxs(device: torch.device) -> list:
+    ctx(device)  # at least the current one
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    with _lock:
+        return [c for k, c in _ctxs.items() if k[0] == idx]
+
+
 def launches(device: torch.device) -> int:
-    return int(load().fhv_ctx_launches(ctx(device)))
+    """Kernel launches issued through this library on the device (all contexts)."""
+    lib = load()
+    return int(sum(lib.fhv_ctx_launches(c) for c in _device_ctxs(device)))
 
 
 def prof_enable(device: torch.device, on: bool = True) -> None:
-    load().fhv_prof_enable(ctx(device), 1 if on else 0)
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    _prof_on[idx] = on
+    for c in _device_ctxs(device):
+        load().fhv_prof_enable(c, 1 if on else 0)
 
 
 def prof_collect(device: torch.device) -> dict:
-    """{stage: (total_ms, launches)} since the last collect (syncs)."""
+    """{stage: (total_ms, launches)} since the last collect, over every
+    context of the device (syncs)."""
     import numpy as np
     lib = load()
-    ms = np.zeros(64)
-    cnt = np.zeros(64, dtype=np.int64)
-    n = lib.fhv_prof_collect(ctx(device), ms.ctypes.data, cnt.ctypes.data, 64)
-    out = {}
-    for i in range(n):
-        if cnt[i]:
-            out[lib.fhv_prof_stage_name(i).decode()] = (float(ms[i]), int(cnt[i]))
+    out: dict = {}
+    for c in _device_ctxs(device):
+        ms = np.zeros(64)
+        cnt = np.zeros(64, dtype=np.int64)
+        n = lib.fhv_prof_collect(c, ms.ctypes.data, cnt.ctypes.data, 64)
+        for i in range(n):
+            if cnt[i]:
+                name = lib.fhv_prof_stage_name(i).decode()
+                t, k = out.get(name, (0.0, 0))
+                out[name] = (t + float(ms[i]), k + int(cnt[i]))
     return out
 
 
