@@ -598,16 +598,26 @@ def main():
     if dominant in algo_bytes and world == 1:  # per-kernel bytes below are for the unsharded (N=1) launch
         per_launch_ms = prof[dominant][0] / prof[dominant][1]
         ach = algo_bytes[dominant] / (per_launch_ms / 1e3) / 1e9
-        traffic = None
+        traffic, ncu = None, {}
         tf = os.path.join(ROOT, "profiles", f"ncu_{dominant}.json")
         if os.path.exists(tf):
             try:
-                traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+                ncu = json.load(open(tf))
+                traffic = ncu.get("dram_bytes_per_launch")
             except Exception:
-                traffic = None
+                traffic, ncu = None, {}
         roof = {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "algorithmic_bytes": algo_bytes[dominant],
                 "peak_kind": peak_kind, "ms_per_launch": round(per_launch_ms, 4)}
+        winst = ncu.get("warp_inst_per_launch")
+        if winst:  # the limiter: instruction issue (4 warp instructions / SM / clock)
+            mhz = clk.summary().get("sm_mhz") or 1965
+            n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+            cap = n_sm * 4 * mhz * 1e6 * per_launch_ms / 1e3
+            roof["issue"] = {"warp_inst_per_launch": winst, "peak_warp_inst_per_launch": int(cap),
+                             "frac": round(winst / cap, 4),
+                             "note": "executed warp instructions from the ncu capture in profiles/ncu_<stage>.json "
+                                     "over this run's launch time x SMs x 4 schedulers x SM clock"}
     capture_ms = sum(v for k, v in stage_ms.items() if not k.startswith("splat"))
     recon_ms = sum(v for k, v in stage_ms.items() if k.startswith("splat"))
     step_bytes = (2 * 176 * T + 36 * n_frags + 12 * 8 ** L + (8 ** L - 1) // 7  # POFA capture

@@ -5,7 +5,7 @@
 TAG=${1:-rX}
 mkdir -p gpurun_out
 STAGES="pytest smoke bench ref launches" bash tools/gpu_round.sh $TAG
-NCU_FILTER="--launch-skip 30 -c 12" STAGES="full" bash tools/gpu_round.sh $TAG
+NCU_FILTER="--launch-skip 40 -c 14" STAGES="full" bash tools/gpu_round.sh $TAG
 timeout 900 python bench.py --config C2 --steps 20 --warmup 5 > gpurun_out/${TAG}_bench_C2.jsonl 2> gpurun_out/${TAG}_bench_C2.err
 timeout 900 python bench.py --config C4 --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_C4.jsonl 2> gpurun_out/${TAG}_bench_C4.err
 timeout 900 python bench.py --config C5 --steps 3 --warmup 1 > gpurun_out/${TAG}_bench_C5.jsonl 2> gpurun_out/${TAG}_bench_C5.err
