@@ -446,7 +446,7 @@ __device__ __forceinline__ void interp_nrm(const TriData& d, double l0, double l
   const double len = __dsqrt_rn(e021(v[0], v[1], v[2], v[0], v[1], v[2]));
   if (len > 1e-12) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) out[k] = ddiv_zd(v[k], len);
+    for (int k = 0; k < 3; ++k) out[k] = ddiv_zd_sel(v[k], len);
   } else {
 #pragma unroll
     for (int k = 0; k < 3; ++k) out[k] = d.f[k];
@@ -485,7 +485,7 @@ __device__ __forceinline__ void ds_fragment(const CaptureParams& p, const EmitOu
                                             int px, int py) {
   double f0, f1, f2;
   cover_test(c, px, py, f0, f1, f2);
-  double l0 = ddiv_zd(f0, c.area2), l1 = ddiv_zd(f1, c.area2), l2 = ddiv_zd(f2, c.area2);
+  double l0 = ddiv_zd_sel(f0, c.area2), l1 = ddiv_zd_sel(f1, c.area2), l2 = ddiv_zd_sel(f2, c.area2);
   const JobPersp& jp = p.persp[job];
   const double d = jp.n1 ? fwd3(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]) : g102(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]);
   if (isnan(d)) return;  // np.minimum.at would poison the pixel; no winner either way
@@ -566,9 +566,9 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   if (valid) {
     double f0, f1, f2;
     cover_test(c, px, py, f0, f1, f2);  // the same f64 values the sweep tested
-    l0 = ddiv_zd(f0, c.area2);
-    l1 = ddiv_zd(f1, c.area2);
-    l2 = ddiv_zd(f2, c.area2);
+    l0 = ddiv_zd_sel(f0, c.area2);
+    l1 = ddiv_zd_sel(f1, c.area2);
+    l2 = ddiv_zd_sel(f2, c.area2);
     if (kMode == kList && (p.persp || o.depth)) list_depth(p, item_job_g[k], l0, l1, l2, dep);
     load_tri_pos(p, c.tri, c.swapped, d);
     interp_pos(d, l0, l1, l2, w);

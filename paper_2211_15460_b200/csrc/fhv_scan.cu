@@ -28,6 +28,17 @@ __device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) {
   *reinterpret_cast<volatile uint64_t*>(p) = v;
 }
 
+// dynamic tile ticket (tiles start in ticket order: the decoupled look-back
+// never waits on a tile that has not started).  The block drawing the last
+// of the launch's n tickets puts the counter back to 0 -- every ticket is
+// drawn by then -- so no memset precedes the next scan on this ctx (the
+// counter starts at 0 with the ctx and after every reset_control).
+__device__ __forceinline__ unsigned draw_tile(Control* ctl, unsigned n_launched) {
+  const unsigned t = atomicAdd(&ctl->tile_counter, 1u);
+  if (t == n_launched - 1) atomicExch(&ctl->tile_counter, 0u);
+  return t;
+}
+
 // block-wide exclusive scan of one u64 per thread; returns exclusive value,
 // writes the block total to *total
 template <int BLOCK>
@@ -95,7 +106,7 @@ __global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restri
                                                        const unsigned long long* n_dev) {
   __shared__ unsigned tile_s;
   __shared__ uint64_t prefix_s, total_s;
-  if (threadIdx.x == 0) tile_s = atomicAdd(&ctl->tile_counter, 1u);
+  if (threadIdx.x == 0) tile_s = draw_tile(ctl, n_tiles);
   __syncthreads();
   const unsigned tile = tile_s;
   if (n_dev) {  // speculatively sized launch: tiles past the device count retire at once
@@ -154,7 +165,7 @@ __global__ void __launch_bounds__(BLOCK) k_scan_leaves(const uint4* __restrict__
                                                       uint64_t* status, Control* ctl, unsigned n_tiles) {
   __shared__ unsigned tile_s;
   __shared__ uint64_t prefix_s, total_s;
-  if (threadIdx.x == 0) tile_s = atomicAdd(&ctl->tile_counter, 1u);
+  if (threadIdx.x == 0) tile_s = draw_tile(ctl, n_tiles);
   __syncthreads();
   const unsigned tile = tile_s;
   const int64_t node = (int64_t)tile * BLOCK + threadIdx.x;
@@ -227,7 +238,7 @@ __global__ void __launch_bounds__(32 * WARPS, WARPS <= 16 ? 2 : 1) k_dir_tiles(c
   __shared__ uint8_t lvl_s[2][T::kL3];
   __shared__ int last_s;
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) tile_s = kScan ? atomicAdd(&ctl->tile_counter, 1u) : blockIdx.x;
+  if (threadIdx.x == 0) tile_s = kScan ? draw_tile(ctl, n_tiles) : blockIdx.x;
   __syncthreads();
   const unsigned tile = tile_s;        // tile within the range (scan order)
   const unsigned gtile = tile0 + tile;  // level-(L-K) node in the whole tree
@@ -358,6 +369,7 @@ __global__ void __launch_bounds__(32 * WARPS, WARPS <= 16 ? 2 : 1) k_dir_tiles(c
     __threadfence();
     const unsigned long long done = atomicAdd(&ctl->spare[1], 1ull);
     last_s = done == (unsigned long long)n_tiles - 1;
+    if (last_s) ctl->spare[1] = 0;  // every tile has counted itself: ready for the next pass
   }
   __syncthreads();
   if (!last_s) return;
@@ -430,8 +442,6 @@ int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, i
   if (!st) return FHV_NOMEM;
   int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)tiles * sizeof(uint64_t), s));
   if (rc) return rc;
-  rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->tile_counter, 0, sizeof(unsigned), s));
-  if (rc) return rc;
   {
     LaunchScope L_(ctx, kStScan, s);
     k_scan_u32_u64<B, I><<<tiles, B, 0, s>>>(in, out, n, st, ctx->ctl, tiles, n_dev);
@@ -484,11 +494,7 @@ static int launch_dir_tiles(fhv_ctx* ctx, bool scan, const uint32_t* counts, uin
     if (!st) return FHV_NOMEM;
     int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)tiles * sizeof(uint64_t), s));
     if (rc) return rc;
-    rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->tile_counter, 0, sizeof(unsigned), s));
-    if (rc) return rc;
   }
-  int rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->spare[1], 0, sizeof(unsigned long long), s));
-  if (rc) return rc;
   {
     LaunchScope L_(ctx, scan ? kStScanLeaves : kStPyramid, s);
     if (tl == DirBig::kLeaves)
@@ -508,8 +514,6 @@ int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offs
   uint64_t* st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)tiles * sizeof(uint64_t));
   if (!st) return FHV_NOMEM;
   int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)tiles * sizeof(uint64_t), s));
-  if (rc) return rc;
-  rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->tile_counter, 0, sizeof(unsigned), s));
   if (rc) return rc;
   {
     LaunchScope L_(ctx, kStScanLeaves, s);

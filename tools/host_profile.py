@@ -26,8 +26,14 @@ def main(steps=20):
     img = ImageBuffer(W, H, torch.empty((H, W, 4), dtype=torch.float64, device=dev),
                       torch.empty((H, W), dtype=torch.float64, device=dev))
 
+    asynchronous = os.environ.get("HOSTPROF_ASYNC", "1") != "0"
+    tickets = torch.zeros((4 * (steps + 8), 4), dtype=torch.int64).pin_memory()
+    used = [0]
+
     def step():
-        vol = fhv.pofa_build(scene, strat, cfg, L, device=dev, tris=ds)
+        tk = tickets[used[0] % len(tickets)]
+        used[0] += 1
+        vol = fhv.pofa_build(scene, strat, cfg, L, device=dev, tris=ds, sync=not asynchronous, ticket=tk)
         fhv.splat_render(vol.pool, view, w["lights"], w["radius"], scene.materials, out=img, shading=shading)
 
     for _ in range(5):
@@ -36,8 +42,10 @@ def main(steps=20):
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
+    t1 = time.perf_counter()
     torch.cuda.synchronize()
-    print(f"wall per step {1e3 * (time.perf_counter() - t0) / steps:.3f} ms")
+    print(f"{'asynchronous' if asynchronous else 'synchronous'} steps: host enqueue per step "
+          f"{1e3 * (t1 - t0) / steps:.3f} ms, wall per step {1e3 * (time.perf_counter() - t0) / steps:.3f} ms")
     pr = cProfile.Profile()
     pr.enable()
     for _ in range(steps):
