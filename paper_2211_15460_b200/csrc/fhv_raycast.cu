@@ -214,9 +214,9 @@ __device__ __forceinline__ void expand_node(const RayParams& x, const double o[3
     pl[a][1] = __dadd_rn(lo[a], half);
     pl[a][2] = __dadd_rn(pl[a][1], half);
     const bool dz = d[a] == 0.0;
-    tp[a][0] = (!dz && side_lo[a]) ? ddiv_z(__dsub_rn(pl[a][0], o[a]), d[a]) : 0.0;
-    tp[a][1] = !dz ? ddiv_z(__dsub_rn(pl[a][1], o[a]), d[a]) : 0.0;
-    tp[a][2] = (!dz && side_hi[a]) ? ddiv_z(__dsub_rn(pl[a][2], o[a]), d[a]) : 0.0;
+    tp[a][0] = (!dz && side_lo[a]) ? ddiv_z_sel(__dsub_rn(pl[a][0], o[a]), d[a]) : 0.0;
+    tp[a][1] = !dz ? ddiv_z_sel(__dsub_rn(pl[a][1], o[a]), d[a]) : 0.0;
+    tp[a][2] = (!dz && side_hi[a]) ? ddiv_z_sel(__dsub_rn(pl[a][2], o[a]), d[a]) : 0.0;
   }
   double cte[8];
   int cc[8];
