@@ -348,6 +348,20 @@ struct CoverS {  // per-item coverage state, staged in shared memory
   float inv_bw;  // 1.0f / bw: pixel index -> bbox row without an integer division
 };
 
+// the emission pass's staged item: + recip_of(area2).y, replayed by every
+// fragment's barycentric divisions (div_rn, bit-identical: -2 % emit time).
+// The counting pass keeps CoverS and the plain division (its sweep reads the
+// struct per pixel: a longer stride costs it more than the reciprocal saves)
+struct CoverR : CoverS {
+  double rcp_area2;
+};
+
+// l_i = f_i / area2, correctly rounded (__ddiv_rn's result)
+__device__ __forceinline__ double bary(const CoverS& c, double f) { return ddiv_zd_sel(f, c.area2); }
+__device__ __forceinline__ double bary(const CoverR& c, double f) {
+  return div_rn(f, Recip{c.area2, c.rcp_area2});
+}
+
 __device__ __forceinline__ void make_cover(const JobSetup& js, uint32_t p0, CoverS& c) {
   c.ax = js.ax; c.ay = js.ay; c.bx = js.bx; c.by = js.by; c.cx = js.cx; c.cy = js.cy;
   c.area2 = __dsub_rn(__dmul_rn(__dsub_rn(c.bx, c.ax), __dsub_rn(c.cy, c.ay)),
@@ -364,6 +378,10 @@ __device__ __forceinline__ void make_cover(const JobSetup& js, uint32_t p0, Cove
   c.swapped = js.swapped;
   c.p0 = p0;
   c.inv_bw = 1.0f / (float)(js.bw > 0 ? js.bw : 1);
+}
+__device__ __forceinline__ void make_cover(const JobSetup& js, uint32_t p0, CoverR& c) {
+  make_cover(js, p0, static_cast<CoverS&>(c));
+  c.rcp_area2 = recip_of(c.area2 > 0.0 ? c.area2 : 1.0).y;
 }
 
 // pixel-centre coverage test with the top-left rule; edge functions in f64
@@ -480,12 +498,12 @@ struct RasterState {
 // atomicMin of the job among fragments at that key, then the winner alone
 // interpolates with the perspective-corrected lam (lam / w renormalised,
 // :206-208) and writes the f64 G-buffer.
-template <int kMode>
-__device__ __forceinline__ void ds_fragment(const CaptureParams& p, const EmitOut& o, const CoverS& c, uint32_t job,
+template <int kMode, class Cov>
+__device__ __forceinline__ void ds_fragment(const CaptureParams& p, const EmitOut& o, const Cov& c, uint32_t job,
                                             int px, int py) {
   double f0, f1, f2;
   cover_test(c, px, py, f0, f1, f2);
-  double l0 = ddiv_zd_sel(f0, c.area2), l1 = ddiv_zd_sel(f1, c.area2), l2 = ddiv_zd_sel(f2, c.area2);
+  double l0 = bary(c, f0), l1 = bary(c, f1), l2 = bary(c, f2);
   const JobPersp& jp = p.persp[job];
   const double d = jp.n1 ? fwd3(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]) : g102(l0, l1, l2, jp.z[0], jp.z[1], jp.z[2]);
   if (isnan(d)) return;  // np.minimum.at would poison the pixel; no winner either way
@@ -544,9 +562,9 @@ __device__ __forceinline__ void list_depth(const CaptureParams& p, uint32_t job,
   }
 }
 
-template <int kMode, bool kAtomicAlloc>
+template <int kMode, bool kAtomicAlloc, class Cov>
 __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitOut& o, Control* ctl,
-                                             const CoverS* cs, bool valid, int k, int px, int py,
+                                             const Cov* cs, bool valid, int k, int px, int py,
                                              uint32_t push_local, uint32_t* own_cnt, unsigned long long rank0,
                                              const uint32_t* item_job_g, RasterState<kMode, kAtomicAlloc>& st) {
   if constexpr (kMode == kDsDepth || kMode == kDsIndex || kMode == kDsWrite) {
@@ -557,7 +575,7 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   constexpr bool kOwned = kMode == kCntLeaves || kMode == kPofa;
   const unsigned lane = lane_id();
   const unsigned below = (1u << lane) - 1u;
-  const CoverS& c = cs[k];
+  const Cov& c = cs[k];
   bool live = false;
   TriData d;
   double w[3] = {0.0, 0.0, 0.0};
@@ -566,9 +584,9 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   if (valid) {
     double f0, f1, f2;
     cover_test(c, px, py, f0, f1, f2);  // the same f64 values the sweep tested
-    l0 = ddiv_zd_sel(f0, c.area2);
-    l1 = ddiv_zd_sel(f1, c.area2);
-    l2 = ddiv_zd_sel(f2, c.area2);
+    l0 = bary(c, f0);
+    l1 = bary(c, f1);
+    l2 = bary(c, f2);
     if (kMode == kList && (p.persp || o.depth)) list_depth(p, item_job_g[k], l0, l1, l2, dep);
     load_tri_pos(p, c.tri, c.swapped, d);
     interp_pos(d, l0, l1, l2, w);
@@ -907,12 +925,12 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
   static_assert(kMode == kList || kMode == kPpfl || kMode == kPofl || kMode == kPofa || kMode == kDsDepth ||
                     kMode == kDsIndex || kMode == kDsWrite,
                 "emission modes only");
-  __shared__ CoverS cs_all[kRasterWarps][32];
+  __shared__ CoverR cs_all[kRasterWarps][32];
   __shared__ uint32_t own_all[kRasterWarps][32];
   __shared__ uint32_t ijob_all[kRasterWarps][32];
   const unsigned lane = lane_id();
   const int wib = threadIdx.x >> 5;
-  CoverS* cs = cs_all[wib];
+  CoverR* cs = cs_all[wib];
   uint32_t* own_cnt = own_all[wib];
   uint32_t* ijob = ijob_all[wib];
   if (n_dev) {  // speculative launch: run the true count, or flag a plan that was too small
