@@ -350,8 +350,9 @@ struct CoverS {  // per-item coverage state, staged in shared memory
 
 // the emission pass's staged item: + recip_of(area2).y, replayed by every
 // fragment's barycentric divisions (div_rn, bit-identical: -2 % emit time).
-// The counting pass keeps CoverS and the plain division (its sweep reads the
-// struct per pixel: a longer stride costs it more than the reciprocal saves)
+// The counting pass keeps CoverS as is (its sweep reads the struct per pixel:
+// a longer stride costs more than the reciprocal saves) and stages the
+// reciprocal in a separate shared array (-1.5 % count time)
 struct CoverR : CoverS {
   double rcp_area2;
 };
@@ -566,7 +567,8 @@ template <int kMode, bool kAtomicAlloc, class Cov>
 __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitOut& o, Control* ctl,
                                              const Cov* cs, bool valid, int k, int px, int py,
                                              uint32_t push_local, uint32_t* own_cnt, unsigned long long rank0,
-                                             const uint32_t* item_job_g, RasterState<kMode, kAtomicAlloc>& st) {
+                                             const uint32_t* item_job_g, RasterState<kMode, kAtomicAlloc>& st,
+                                             const double* rcp = nullptr) {
   if constexpr (kMode == kDsDepth || kMode == kDsIndex || kMode == kDsWrite) {
     if (valid) ds_fragment<kMode>(p, o, cs[k], item_job_g[k], px, py);
     return;
@@ -584,9 +586,16 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   if (valid) {
     double f0, f1, f2;
     cover_test(c, px, py, f0, f1, f2);  // the same f64 values the sweep tested
-    l0 = bary(c, f0);
-    l1 = bary(c, f1);
-    l2 = bary(c, f2);
+    if (rcp) {  // the counting pass's per-item reciprocals (a separate shared array)
+      const Recip ra{c.area2, rcp[k]};
+      l0 = div_rn(f0, ra);
+      l1 = div_rn(f1, ra);
+      l2 = div_rn(f2, ra);
+    } else {
+      l0 = bary(c, f0);
+      l1 = bary(c, f1);
+      l2 = bary(c, f2);
+    }
     if (kMode == kList && (p.persp || o.depth)) list_depth(p, item_job_g[k], l0, l1, l2, dep);
     load_tri_pos(p, c.tri, c.swapped, d);
     interp_pos(d, l0, l1, l2, w);
@@ -741,6 +750,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
   static_assert(kMode == kCnt || kMode == kCntLeaves, "k_raster is the counting pass; emission is k_emit");
   constexpr bool kOwned = kMode == kCntLeaves || kMode == kPofa;
   __shared__ CoverS cs_all[kRasterWarps][32];
+  __shared__ double rcp_all[kRasterWarps][32];  // recip_of(area2).y per item (kept out of CoverS: the sweep's stride)
   __shared__ int32_t qpx_all[kRasterWarps][64], qpy_all[kRasterWarps][64];
   __shared__ uint32_t qmeta_all[kRasterWarps][64];
   __shared__ uint32_t own_all[kRasterWarps][32];
@@ -780,6 +790,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
         prefetch_l1(P + 64);
       }
       make_cover(js, p0, cs[lane]);
+      rcp_all[wib][lane] = recip_of(cs[lane].area2 > 0.0 ? cs[lane].area2 : 1.0).y;
       ijob[lane] = jid;
       if (!kOwned && kMode != kCnt && !kAtomicAlloc) rank0 = item_off[item];
       if (kOwned && kMode == kPofa) rank0 = item_off[item];
@@ -856,7 +867,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
         {
           const uint32_t mt = q_meta[lane];
           raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, true, (int)(mt & 31u), q_px[lane], q_py[lane], mt >> 5,
-                                            own_cnt, rank0, ijob, st);
+                                            own_cnt, rank0, ijob, st, rcp_all[wib]);
         }
         __syncwarp();
         if ((int)lane < qn - 32) {
@@ -873,7 +884,7 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
       const bool v = (int)lane < qn;
       const uint32_t mt = v ? q_meta[lane] : 0u;
       raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, v, (int)(mt & 31u), v ? q_px[lane] : 0, v ? q_py[lane] : 0,
-                                        mt >> 5, own_cnt, rank0, ijob, st);
+                                        mt >> 5, own_cnt, rank0, ijob, st, rcp_all[wib]);
     }
     __syncwarp();
     if (item < n_items) {
