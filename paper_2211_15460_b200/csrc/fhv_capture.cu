@@ -464,8 +464,9 @@ __device__ __forceinline__ void interp_nrm(const TriData& d, double l0, double l
     v[k] = __fma_rn(l2, d.n[2][k], __fma_rn(l1, d.n[1][k], add0(__dmul_rn(l0, d.n[0][k]))));
   const double len = __dsqrt_rn(e021(v[0], v[1], v[2], v[0], v[1], v[2]));
   if (len > 1e-12) {
+    const Recip rl = recip_of(len);  // one reciprocal for the three components (bit-identical div_rn)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) out[k] = ddiv_zd_sel(v[k], len);
+    for (int k = 0; k < 3; ++k) out[k] = div_rn(v[k], rl);
   } else {
 #pragma unroll
     for (int k = 0; k < 3; ++k) out[k] = d.f[k];
