@@ -121,7 +121,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            self._stop.wait(0.005)
+            self._stop.wait(0.02)  # sparse: NVML queries take driver locks the launching thread also needs
 
     def __enter__(self):
         if self.nv:
