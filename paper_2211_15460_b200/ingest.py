@@ -25,9 +25,7 @@ import torch
 
 from . import _lib
 from .device import default_device
-from .scene import Material, Scene, SceneError, SceneLoadError
-
-DEFAULT_MATERIAL_NAME = "__default__"
+from .scene import DEFAULT_MATERIAL_NAME, Material, Scene, SceneError, SceneLoadError
 
 __all__ = ["DEFAULT_MATERIAL_NAME", "load_material_table", "load_scene", "save_material_table", "save_scene"]
 

@@ -17,7 +17,7 @@ import numpy as np
 from .scene import Camera, Scene, SceneError, capture_camera
 
 __all__ = ["CAPTURE_STRATEGIES", "CapturePlan", "CaptureStats", "CaptureStrategy", "EmittedFragment",
-           "FragmentBatch", "ListSink", "RasterConfig", "capture_plan", "ortho_projection", "perspective_projection",
+           "FragmentBatch", "ListSink", "capture_pass", "RasterConfig", "capture_plan", "ortho_projection", "perspective_projection",
            "rasterize_triangle", "rasterize_triangles", "tangent_basis", "world_pixel_footprint"]
 
 CAPTURE_STRATEGIES = ("one_view", "three_separate", "three_way_geometry", "normal_space")
@@ -294,3 +294,11 @@ def rasterize_triangle(tri, cfg: RasterConfig, sink=None, device=None) -> int:
                            out["world_position"].cpu().numpy(), out["world_normal"].cpu().numpy(),
                            out["depth"].cpu().numpy(), int(tri.material_id), int(tri.object_id)))
     return n
+
+
+def capture_pass(scene, strategy: CaptureStrategy, cfg: RasterConfig, sink, threads: int = 1, device=None):
+    """fhv.raster.capture_pass (fhv/raster.py:350-388) at its reference module
+    path; the implementation is capture.capture_pass (device rasterisation,
+    host sink calls)."""
+    from .capture import capture_pass as _capture_pass
+    return _capture_pass(scene, strategy, cfg, sink, threads, device=device)

@@ -22,7 +22,7 @@ __all__ = [
     "AXIS_VIEWS", "Aabb", "Camera", "Material", "Scene", "SceneError", "SceneLoadError",
     "SceneTransform", "Triangle", "Vertex", "capture_camera", "make_quad", "make_triangle", "normalize_scene",
     "viewpoint_camera",
-]
+, "DEFAULT_MATERIAL_NAME", "load_material_table", "load_scene", "save_material_table", "save_scene"]
 
 # Capture frames look down the negative axis with a pinned up vector
 # (fhv/scene.py:46-52).
@@ -356,3 +356,28 @@ def look_at_camera(eye, target=(0.5, 0.5, 0.5), up=(0.0, 1.0, 0.0), resolution=(
     eye = _as3(eye)
     d = _as3(target) - eye
     return Camera("perspective", eye, d, _as3(up), fov_deg, resolution, near, far)
+
+
+# scene files at the reference's module path (fhv/scene.py:251-432); the
+# implementation is ingest.py (bulk parse, device normalisation)
+DEFAULT_MATERIAL_NAME = "__default__"
+
+
+def load_material_table(path):
+    from .ingest import load_material_table as f
+    return f(path)
+
+
+def load_scene(path, material_table=None, device=None):
+    from .ingest import load_scene as f
+    return f(path, material_table, device)
+
+
+def save_material_table(materials, names, path) -> None:
+    from .ingest import save_material_table as f
+    return f(materials, names, path)
+
+
+def save_scene(scene, path, material_path=None) -> None:
+    from .ingest import save_scene as f
+    return f(scene, path, material_path)
