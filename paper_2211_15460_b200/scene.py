@@ -21,8 +21,9 @@ import numpy as np
 __all__ = [
     "AXIS_VIEWS", "Aabb", "Camera", "Material", "Scene", "SceneError", "SceneLoadError",
     "SceneTransform", "Triangle", "Vertex", "capture_camera", "make_quad", "make_triangle", "normalize_scene",
-    "viewpoint_camera",
-, "DEFAULT_MATERIAL_NAME", "load_material_table", "load_scene", "save_material_table", "save_scene"]
+    "viewpoint_camera", "DEFAULT_MATERIAL_NAME", "load_material_table", "load_scene", "save_material_table",
+    "save_scene",
+]
 
 # Capture frames look down the negative axis with a pinned up vector
 # (fhv/scene.py:46-52).
