@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = ["fhv_abi.cu", "fhv_scan.cu", "fhv_capture.cu", "fhv_splat.cu", "fhv_raycast.cu", "fhv_ops.cu"]
-HEADERS = ["fhv_common.cuh", "fhv_internal.h"]
+HEADERS = ["fhv_common.cuh", "fhv_internal.h", "fhv_lookback.cuh"]
 OUT = os.path.join(HERE, "libfhv_b200.so")
 
 NVCC_FLAGS = [
