@@ -351,7 +351,11 @@ inline int grid_for(int64_t n, int block) {
 
 int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, int64_t n, cudaStream_t s,
                     const unsigned long long* n_dev) {
-  constexpr int B = 512, I = 16;  // 8192 elements per tile: a short look-back chain
+#ifndef FHV_SCAN_B
+#define FHV_SCAN_B 512
+#define FHV_SCAN_I 16
+#endif
+  constexpr int B = FHV_SCAN_B, I = FHV_SCAN_I;  // 8192 elements per tile: a short look-back chain
   const int64_t per = (int64_t)B * I;
   const unsigned tiles = (unsigned)((n + per - 1) / per);
   if (n <= 0) {
