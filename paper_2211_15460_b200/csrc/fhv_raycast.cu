@@ -20,7 +20,10 @@
 
 namespace fhv {
 
-constexpr int kRayMaxLevels = 12;
+#ifndef FHV_RAY_MAXL
+#define FHV_RAY_MAXL 12
+#endif
+constexpr int kRayMaxLevels = FHV_RAY_MAXL;
 constexpr int kStack = 7 * kRayMaxLevels + 1;
 constexpr int kHitBuf = 8;
 
