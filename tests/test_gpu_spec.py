@@ -153,3 +153,33 @@ def test_async_pofa_build_wrong_guess_is_rebuilt(delta):
     assert fhv.storage.check_ticket(v) == fhv._lib.FHV_STALE
     v.wait()
     _same(v, ref)
+
+
+def test_two_streams_get_separate_contexts():
+    """A splat on a side stream while the next capture runs on the default
+    stream: each stream has its own scratch context (control block, item
+    buffers), so both results equal their one-stream counterparts."""
+    s = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+    cfg = _cfg(s, 192)
+    cam = fhv.viewpoint_camera("+x", (160, 120), "perspective")
+    lights = lights_for("head", cam)
+    ref_vol = fhv.pofa_build(s, ns, cfg, 5, exact_order=True)
+    ref_img = fhv.splat_render(ref_vol.pool, cam, lights, 1.0 / 192, s.materials)
+    ref_px = ref_img.pixels.cpu().numpy()
+    side = torch.cuda.Stream()
+    vols = []
+    for _ in range(3):
+        v = fhv.pofa_build(s, ns, cfg, 5, exact_order=True, sync=False)
+        side.wait_stream(torch.cuda.current_stream())
+        v.pool.position.record_stream(side)
+        with torch.cuda.stream(side):
+            img = fhv.splat_render(v.pool, cam, lights, 1.0 / 192, s.materials)
+        vols.append((v, img))
+    torch.cuda.synchronize()
+    for v, img in vols:
+        v.wait()
+        _same(v, ref_vol)
+        assert np.array_equal(img.pixels.cpu().numpy(), ref_px)
+    ctxs = {k for k in fhv._lib._ctxs if k[0] == torch.cuda.current_device()}
+    assert len({k[2] for k in ctxs}) >= 2  # distinct streams -> distinct contexts
