@@ -481,7 +481,10 @@ enum RasterMode { kCnt = 0, kCntLeaves = 1, kList = 2, kPpfl = 3, kPofl = 4, kPo
 #ifndef FHV_RASTER_MINB
 #define FHV_RASTER_MINB 3  // resident CTAs per SM the raster kernels are register-budgeted for
 #endif
-constexpr int kRasterBlock = 256;
+#ifndef FHV_RASTER_BLOCK
+#define FHV_RASTER_BLOCK 256
+#endif
+constexpr int kRasterBlock = FHV_RASTER_BLOCK;
 constexpr int kRasterWarps = kRasterBlock / 32;
 
 template <int kMode, bool kAtomicAlloc>
