@@ -28,7 +28,7 @@ import torch
 from . import _lib
 from .device import capture_cfg, default_device, device_scene
 from .raster import CaptureStats, CaptureStrategy, RasterConfig, capture_plan
-from .scene import Material, Scene
+from .scene import Scene
 
 __all__ = [
     "FhvError", "FhvPofa", "FhvPofl", "FhvPpfl", "FragmentPool", "FragmentRecord", "MAX_LEVELS",
