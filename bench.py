@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--composite", default="auto", choices=("auto", "peer", "allreduce"),
                     help="multi-GPU splat composite: peer memory (fhv_splat_peer over NVLink P2P) or NCCL "
                          "all-reduces; auto = peer when the peer mappings can be set up")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time the Python-enqueued steps instead of CUDA-graph replays of one captured step")
     ap.add_argument("--sync-steps", action="store_true",
                     help="wait for each pofa_build on the host (default: asynchronous steps, tickets checked)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -542,6 +544,39 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # ---- one step captured in a CUDA graph (N = 1, asynchronous steps) ------
+    # The whole step -- POFA build (every kernel, memset and copy) + splat --
+    # is captured once on its own stream and replayed K times; each replay
+    # also checks its build's ticket on the device (sticky status + count).
+    graph = None
+    if world == 1 and not args.sync_steps and not args.no_graph:
+        gs = torch.cuda.Stream(dev)
+        acc = torch.zeros(2, dtype=torch.int64, device=dev)
+        gticket = torch.zeros(4, dtype=torch.int64).pin_memory()
+
+        def graph_step():
+            v = fhv.pofa_build(scene, strat, cfg, L, exact_order=args.exact_order, device=dev, tris=ds, sync=False,
+                               ticket=gticket)
+            rc = _lib.load().fhv_ticket_accumulate(_lib.ctx(dev), int(n_frags), _lib.ptr(acc), _lib.stream_ptr(dev))
+            _lib.check(rc, "ticket")
+            fhv.splat_render(v.pool, view, w["lights"], w["radius"], scene.materials, out=img, packed=args.packed,
+                             shading=shading)
+            return v
+        with torch.cuda.stream(gs):
+            for _ in range(2):  # this stream's context: speculative item plan, scratch buffers
+                graph_step()
+        torch.cuda.synchronize()
+        acc.zero_()
+        graph = torch.cuda.CUDAGraph()
+        l0 = _lib.launches(dev)
+        with torch.cuda.graph(graph, stream=gs):
+            gvol = graph_step()
+        per_replay = _lib.launches(dev) - l0
+        torch.cuda.synchronize()
+        acc.zero_()
+        graph.replay()  # one untimed replay
+        torch.cuda.synchronize()
+
     # ---- device-resident timed region --------------------------------------
     # (no per-launch events inside it; the per-kernel shares come from a
     # separate profiled pass of the same steps below)
@@ -549,15 +584,28 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _lib.launches(dev)
     barrier()
+    if graph is not None:
+        acc.zero_()
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            vol = step()
+            if graph is not None:
+                graph.replay()
+            else:
+                vol = step()
         e1.record(stream)
         barrier()
-    async_checked = check_tickets()
+    if graph is not None:
+        bad, checked = (int(x) for x in acc.cpu().tolist())
+        if bad or checked != args.steps:
+            raise RuntimeError(f"graph replays: build ticket status {bad}, {checked}/{args.steps} checked")
+        async_checked = checked
+        vol = gvol
+        gpu_launches = per_replay * args.steps
+    else:
+        async_checked = check_tickets()
+        gpu_launches = _lib.launches(dev) - launches0
     ms = e0.elapsed_time(e1)
-    gpu_launches = _lib.launches(dev) - launches0
     # per-kernel CUDA events on the launching stream (LaunchScope, fhv_abi.cu)
     _lib.prof_enable(dev, True)
     _lib.prof_collect(dev)  # reset
@@ -735,8 +783,11 @@ def main():
                                parallelism=f"morton-range shards x{world} (NCCL)" if world > 1 else "single",
                                composite=composite if world > 1 else None,
                                exact_order=bool(args.exact_order), splat="packed" if args.packed else "exact",
-                               host="asynchronous steps: pofa_build(sync=False), all %d tickets verified after "
-                                    "the timed loop" % async_checked if async_checked else "synchronous steps"),
+                               host=("CUDA-graph replays of one captured asynchronous step (POFA build + splat, "
+                                     "every kernel / memset / copy re-executed), all %d build tickets checked on the "
+                                     "device" % async_checked) if graph is not None else
+                               ("asynchronous steps: pofa_build(sync=False), all %d tickets verified after the "
+                                "timed loop" % async_checked if async_checked else "synchronous steps")),
                 "novel_view_fps": 1e3 / recon_ms if recon_ms else None,
                 "capture_frag_per_s": n_frags / (capture_ms / 1e3) if capture_ms else None,
                 "step_gbs": step_bytes / (ms_step / 1e3) / 1e9, "step_bytes": step_bytes,

@@ -242,6 +242,11 @@ int fhv_pofa_build_async(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture
                          uint32_t *counts, uint32_t *offsets, uint8_t *pyramid, fhv_pool_t *pool, int32_t flags,
                          fhv_ticket_t *ticket, void *stream);
 int fhv_ticket_check(const fhv_ticket_t *ticket, int64_t expect_total);
+/* The same check on the device, enqueued right after fhv_pofa_build_async on
+   its stream (e.g. inside a CUDA graph that replays the build): acc[0]
+   (device int64, zeroed by the caller) keeps the first non-OK status,
+   acc[1] counts the checks.  Async. */
+int fhv_ticket_accumulate(fhv_ctx *ctx, int64_t expect_total, int64_t *acc, void *stream);
 
 /* rebuild_pofl_as_pofa (fhv/storage.py:624-652): repack the first n records
    of a linked-list pool into per-leaf contiguous ranges (Morton order, pool

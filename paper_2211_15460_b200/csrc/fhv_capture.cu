@@ -1944,6 +1944,36 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   return check_cuda(ctx, cudaMemcpyAsync(ticket, &ctx->ctl->spare[4], sizeof(fhv_ticket_t), cudaMemcpyDefault, s));
 }
 
+namespace fhv {
+namespace {
+// the ticket check on the device (same rules as fhv_ticket_check) over the
+// staged outcome of the build just enqueued on this stream; failures are
+// kept sticky in acc[0] (first non-OK status), acc[1] counts the checks --
+// for a CUDA graph replaying the build many times
+__global__ void k_ticket_acc(const Control* ctl, long long expect, long long* acc) {
+  const long long status = (long long)ctl->spare[4];
+  const long long frags = (long long)ctl->spare[5], scan = (long long)ctl->spare[6], alloc = (long long)ctl->spare[7];
+  long long rc = FHV_OK;
+  if (status == FHV_RETRY_ITEMS || status == FHV_NEED_POOL) rc = FHV_STALE;
+  else if (status) rc = status;
+  else if (frags >= (1LL << 32)) rc = FHV_TOO_MANY;
+  else if (scan != frags || alloc != frags) rc = FHV_PASS_MISMATCH;
+  else if (frags != expect) rc = FHV_STALE;
+  if (rc) atomicCAS(reinterpret_cast<unsigned long long*>(acc), 0ull, (unsigned long long)rc);
+  atomicAdd(reinterpret_cast<unsigned long long*>(acc + 1), 1ull);
+}
+}  // namespace
+}  // namespace fhv
+
+extern "C" int fhv_ticket_accumulate(fhv_ctx* ctx, int64_t expect_total, int64_t* acc, void* stream) {
+  if (!ctx || !acc) return FHV_BAD_ARGS;
+  {
+    LaunchScope L_(ctx, kStScan, (cudaStream_t)stream);
+    k_ticket_acc<<<1, 1, 0, (cudaStream_t)stream>>>(ctx->ctl, (long long)expect_total, (long long*)acc);
+  }
+  return check_cuda(ctx, cudaGetLastError());
+}
+
 extern "C" int fhv_ticket_check(const fhv_ticket_t* t, int64_t expect_total) {
   if (!t) return FHV_BAD_ARGS;
   if (t->status == FHV_RETRY_ITEMS || t->status == FHV_NEED_POOL) return FHV_STALE;
