@@ -183,3 +183,47 @@ def test_two_streams_get_separate_contexts():
         assert np.array_equal(img.pixels.cpu().numpy(), ref_px)
     ctxs = {k for k in fhv._lib._ctxs if k[0] == torch.cuda.current_device()}
     assert len({k[2] for k in ctxs}) >= 2  # distinct streams -> distinct contexts
+
+
+@pytest.mark.parametrize("delta", [0, 9])
+def test_async_build_in_a_cuda_graph(delta):
+    """pofa_build(sync=False) + the device-side ticket check captured in a
+    CUDA graph: every replay re-runs the whole build and is checked
+    (acc = [first bad status, replays checked])."""
+    s = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+    cfg = _cfg(s, 160)
+    ref = fhv.pofa_build(s, ns, cfg, 5, exact_order=True)
+    ds = fhv.device.device_scene(s)
+    key = next(k for k in ds._pofa_totals if k[1] == 5 and k[0][2] == tuple(cfg.resolution))
+    guess = ref.pool.next_free + delta
+    ds._pofa_totals[key] = guess
+    gs = torch.cuda.Stream()
+    acc = torch.zeros(2, dtype=torch.int64, device="cuda")
+    tk = torch.zeros(4, dtype=torch.int64).pin_memory()
+    lib = fhv._lib.load()
+
+    def step():
+        v = fhv.pofa_build(s, ns, cfg, 5, exact_order=True, sync=False, ticket=tk)
+        assert lib.fhv_ticket_accumulate(fhv._lib.ctx(v.pool.device), guess, fhv._lib.ptr(acc),
+                                         fhv._lib.stream_ptr(v.pool.device)) == 0
+        return v
+    with torch.cuda.stream(gs):
+        step()
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=gs):
+        v = step()
+    acc.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    bad, n = acc.cpu().tolist()
+    assert n == 3
+    if delta == 0:
+        assert bad == 0
+        _same(v, ref)
+    else:
+        assert bad == fhv._lib.FHV_STALE
+    ds._pofa_totals[key] = ref.pool.next_free
