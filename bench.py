@@ -2,26 +2,33 @@
 """Benchmark of the FHV hot path on B200: capture + novel-view reconstruction.
 
 Workload (default --config C3): ``scatter1M`` -- 48
-icospheres, 983,040 triangles, synthetic (seeded), captured with the
-NormalSpace strategy at pitch 1/1080 into a POFA octree of depth 8 (two-pass
-count / scan / scatter), then one 1920x1080 perspective novel view
-reconstructed by exact z-tested point splatting.  One step = capture + one
-reconstruct.  ``value`` = fragments captured per second of step time
-(inputs resident in HBM); ``e2e`` = the same through the public API with the
-scene copied host->device (pinned) and the image copied back every step.
+icospheres, 983,040 triangles, synthetic (seeded; byte-identical to the same
+field built by the reference's own ``icosphere`` / ``make_triangle``,
+tests/test_scene_pinning.py), captured with the NormalSpace strategy at
+pitch 1/1080 into a POFA octree of depth 8 (two-pass count / scan / scatter,
+the reference's exact in-leaf order by default), then one 1920x1080
+perspective novel view reconstructed by exact z-tested point splatting.  One
+step = capture + one reconstruct.  ``value`` = fragments captured per second
+of step time (inputs resident in HBM); ``e2e`` = the same through the public
+API with the scene copied host->device (pinned) and the image copied back
+every step; ``parity`` = the last timed step's pool and image against the
+oracle port on the same inputs.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--fast-order]
 
 --impl reference times the reference algorithm's CPU implementation (the
-oracle port, oracle/fhv_oracle.c, threads=1 like the reference's fastest
-setting) on the same workload and prints the same JSON line shape.
+oracle port, oracle/fhv_oracle.c, bit-identical to the reference's golden
+vectors) on ALL the host's threads (the port parallelises the capture and
+splat without changing their results; the shipped reference is fastest at
+threads=1 and is ~200x slower still: profiles/r02_shipped_reference.json) on
+the same workload and prints the same JSON line shape and ``config``.
 Multi-GPU (torchrun, N>1): the same scene is partitioned by Morton range
 (paper_2211_15460_b200/shard.py): each rank bins the
 triangles of its leaf range, captures its slice of the POFA (one all_gather of
 a fragment total per rank for the global offsets) and splats its fragments;
-the frame is composited by depth with NCCL all-reduces (MIN keys, MIN
-winners, SUM pixels).  Strong scaling: fixed total work; time = max over
-ranks; value = all fragments / that time.
+the frame is composited by depth (NVLink peer-memory slabs, or NCCL
+all-reduces).  Strong scaling: fixed total work; time = max over ranks;
+value = all fragments / that time.
 """
 from __future__ import annotations
 
@@ -48,7 +55,10 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--config", default="C3", choices=("C3", "C2", "C4", "C5"),
                     help="C3 = the headline workload; C2 / C4 / C5 = the other BASELINE configs (1 GPU)")
-    ap.add_argument("--exact-order", action="store_true", help="bit-identical in-leaf order (extra fix-up pass)")
+    ap.add_argument("--fast-order", dest="exact_order", action="store_false",
+                    help="the paper's atomic in-leaf POFA order (per-leaf multiset equal) instead of the reference's "
+                         "exact order (default: exact, byte-identical pool)")
+    ap.add_argument("--exact-order", dest="exact_order", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--packed", action="store_true", help="packed 64-bit splat z-test")
     ap.add_argument("--composite", default="auto", choices=("auto", "peer", "allreduce"),
                     help="multi-GPU splat composite: peer memory (fhv_splat_peer over NVLink P2P) or NCCL "
@@ -155,17 +165,21 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_run(w, threads: int = 1):
+def cpu_run(w, threads: int = 1, keep: bool = False):
     """One full C3 step on the host with the oracle port: POFA capture + the
     1080p splat, on ``threads`` host threads (threads=1 is the reference's
-    sequential order; more threads keep the directory and image identical)."""
+    sequential order; more threads keep the directory and image identical).
+    ``keep``: also return (volume, rgba, depth) for the parity check."""
     from oracle import oracle as orc
     with orc.threads(threads):
         t0 = time.perf_counter()
         vol = orc.pofa_build(w["scene"], w["strategy"], w["cfg"], w["levels"])
         t1 = time.perf_counter()
-        orc.splat(vol["pool"], vol["next_free"], w["view"], w["lights"], w["radius"], w["scene"].materials)
+        rgba, depth, _ = orc.splat(vol["pool"], vol["next_free"], w["view"], w["lights"], w["radius"],
+                                   w["scene"].materials)
         t2 = time.perf_counter()
+    if keep:
+        return vol["next_free"], t1 - t0, t2 - t1, (vol, rgba, depth)
     return vol["next_free"], t1 - t0, t2 - t1
 
 
@@ -549,13 +563,17 @@ def main():
     # is captured once on its own stream and replayed K times; each replay
     # also checks its build's ticket on the device (sticky status + count).
     graph = None
-    if world == 1 and not args.sync_steps and not args.no_graph:
+    acc = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def make_graph(exact: bool):
+        """One step -- POFA build (every kernel, memset and copy) + splat --
+        captured on its own stream; each replay also checks its build ticket
+        on the device (sticky status + count)."""
         gs = torch.cuda.Stream(dev)
-        acc = torch.zeros(2, dtype=torch.int64, device=dev)
         gticket = torch.zeros(4, dtype=torch.int64).pin_memory()
 
         def graph_step():
-            v = fhv.pofa_build(scene, strat, cfg, L, exact_order=args.exact_order, device=dev, tris=ds, sync=False,
+            v = fhv.pofa_build(scene, strat, cfg, L, exact_order=exact, device=dev, tris=ds, sync=False,
                                ticket=gticket)
             rc = _lib.load().fhv_ticket_accumulate(_lib.ctx(dev), int(n_frags), _lib.ptr(acc), _lib.stream_ptr(dev))
             _lib.check(rc, "ticket")
@@ -567,20 +585,38 @@ def main():
                 graph_step()
         torch.cuda.synchronize()
         acc.zero_()
-        graph = torch.cuda.CUDAGraph()
+        g = torch.cuda.CUDAGraph()
         l0 = _lib.launches(dev)
-        with torch.cuda.graph(graph, stream=gs):
-            gvol = graph_step()
-        per_replay = _lib.launches(dev) - l0
+        with torch.cuda.graph(g, stream=gs):
+            gv = graph_step()
+        n_launch = _lib.launches(dev) - l0
         torch.cuda.synchronize()
         acc.zero_()
-        graph.replay()  # one untimed replay
+        g.replay()  # one untimed replay
         torch.cuda.synchronize()
+        return g, gv, n_launch, gs
+
+    def time_graph(g, k):
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        acc.zero_()
+        torch.cuda.synchronize()
+        ea.record(stream)
+        for _ in range(k):
+            g.replay()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        bad_, checked_ = (int(x) for x in acc.cpu().tolist())
+        if bad_ or checked_ != k:
+            raise RuntimeError(f"graph replays: build ticket status {bad_}, {checked_}/{k} checked")
+        return ea.elapsed_time(eb) / k
+
+    stream = torch.cuda.current_stream(dev)
+    if world == 1 and not args.sync_steps and not args.no_graph:
+        graph, gvol, per_replay, gstream = make_graph(args.exact_order)
 
     # ---- device-resident timed region --------------------------------------
     # (no per-launch events inside it; the per-kernel shares come from a
     # separate profiled pass of the same steps below)
-    stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _lib.launches(dev)
     barrier()
@@ -606,6 +642,14 @@ def main():
         async_checked = check_tickets()
         gpu_launches = _lib.launches(dev) - launches0
     ms = e0.elapsed_time(e1)
+    # what the last timed step produced, for the parity check against the oracle
+    shot = None
+    if world == 1 and not args.profile_only:
+        hp = vol.pool.numpy()
+        shot = {"depth": img.depth.cpu().numpy().copy(), "rgba": img.pixels.cpu().numpy().copy(),
+                "pool": {k: hp[k].copy() for k in ("position", "normal", "material_id", "object_id",
+                                                    "prev_index")},
+                "offsets": vol.directory.offsets.cpu().numpy().copy()}
     # per-kernel CUDA events on the launching stream (LaunchScope, fhv_abi.cu)
     _lib.prof_enable(dev, True)
     _lib.prof_collect(dev)  # reset
@@ -620,6 +664,13 @@ def main():
     ms_profiled = ep0.elapsed_time(ep1)
     prof = _lib.prof_collect(dev)
     _lib.prof_enable(dev, False)
+    # the other in-leaf order, same graph-replay timing (exact <-> fast)
+    other = None
+    if graph is not None and not args.profile_only:
+        g2, _, _, _ = make_graph(not args.exact_order)
+        ms2 = time_graph(g2, args.steps)
+        other = {"exact_order": not args.exact_order, "ms_per_step": ms2, "value": n_frags / (ms2 / 1e3)}
+        del g2
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         t_max = all_max(t_max)
@@ -765,11 +816,33 @@ def main():
         e2e = None
 
     cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.profile_only:
+        import numpy as np
+        nt = host_threads()
+        # threads=1: the reference's sequential (canonical) order -- a threaded
+        # oracle run keeps counts / offsets / image but not the in-leaf order
+        n, tc, ts, (rv, rrgba, rdepth) = cpu_run(w, 1, keep=True)
+        single = (n, tc, ts)
+        parity = {"vs": "oracle port (oracle/fhv_oracle.c, pinned to the reference's golden vectors) on the same "
+                        "inputs: the last timed step's image and pool",
+                  "fragments_equal": int(n) == int(n_frags),
+                  "offsets_bit_exact": bool(np.array_equal(shot["offsets"], rv["offsets"])),
+                  "depth_bit_exact": bool(np.array_equal(shot["depth"], rdepth)),
+                  "rgba_max_abs_err": float(np.max(np.abs(shot["rgba"] - rrgba))),
+                  "rgba_tol": 1e-12}
+        if args.exact_order:
+            parity["pool_bit_exact"] = all(np.array_equal(shot["pool"][k], rv["pool"][k]) for k in shot["pool"])
+        else:
+            parity["pool"] = "fast order: per-leaf multiset (records not compared)"
+        parity["ok"] = bool(parity["fragments_equal"] and parity["offsets_bit_exact"] and parity["depth_bit_exact"]
+                            and parity["rgba_max_abs_err"] <= 1e-12 and parity.get("pool_bit_exact", True))
+        del rv, rrgba, rdepth
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
         nt = host_threads()
         cpu_run(w, nt)  # warm-up (page faults, thread start)
         n, tc, ts = cpu_run(w, nt)
-        n1, tc1, ts1 = cpu_run(w, 1)
+        n1, tc1, ts1 = single if parity is not None else cpu_run(w, 1)
         cpu = {"value": n / (tc + ts), "unit": "frag/s", "cores": nt, "kind": "port",
                "sample": f"one full C3 step on the host (oracle/fhv_oracle.c, {nt} threads): capture {tc:.2f} s + "
                          f"splat {ts:.2f} s",
@@ -779,7 +852,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "frag/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded icosphere field, no dataset)",
-                "config": dict(CONFIG, fragments=n_frags,
+                "config": CONFIG,  # the workload; identical to the reference arm's
+                "run": dict(fragments=n_frags,
                                parallelism=f"morton-range shards x{world} (NCCL)" if world > 1 else "single",
                                composite=composite if world > 1 else None,
                                exact_order=bool(args.exact_order), splat="packed" if args.packed else "exact",
@@ -795,6 +869,7 @@ def main():
                 "gap_ms_per_step": round(ms_profiled / args.steps - sum(stage_ms.values()), 4),
                 "ms_per_step_profiled": round(ms_profiled / args.steps, 4),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+                "parity": parity, "other_order": other,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

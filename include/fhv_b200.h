@@ -159,6 +159,10 @@ fhv_ctx *fhv_ctx_create(void);
 void fhv_ctx_destroy(fhv_ctx *ctx);
 /* kernels launched by this context since creation (for launch accounting) */
 int64_t fhv_ctx_launches(const fhv_ctx *ctx);
+/* diagnostics of the last SYNCHRONISED call on this context: out[0] = leaves
+   the EXACT_ORDER POFA tile fix-up re-sorted, out[1] = 0 (reserved), out[2] =
+   long leaves handed to the per-leaf pass; returns the words written (3) */
+int fhv_ctx_counters(const fhv_ctx *ctx, int64_t *out, int n);
 
 /* per-kernel CUDA-event timing on the launching stream (off by default).
    fhv_prof_collect synchronises the recorded events, writes accumulated

@@ -71,6 +71,7 @@ _SIGS = {
     "fhv_ctx_create": (c_vp, []),
     "fhv_ctx_destroy": (None, [c_vp]),
     "fhv_ctx_launches": (c_i64, [c_vp]),
+    "fhv_ctx_counters": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int]),
     "fhv_prof_enable": (ctypes.c_int, [c_vp, ctypes.c_int]),
     "fhv_prof_collect": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int]),
     "fhv_prof_stage_name": (ctypes.c_char_p, [ctypes.c_int]),
@@ -183,7 +184,46 @@ def ctx(device: torch.device):
             if _prof_on.get(idx):
                 lib.fhv_prof_enable(c, 1)
             _ctxs[key] = c
+            if threading.current_thread() is not threading.main_thread() and not hasattr(_tls, "reaper"):
+                _tls.reaper = _ThreadReaper(threading.get_ident())
     return c
+
+
+_tls = threading.local()
+_retired: dict = {}  # device index -> launches of destroyed contexts (launch accounting survives release)
+
+
+def release(device: torch.device | None = None, thread_id: int | None = None, stream=None) -> int:
+    """Destroy the scratch contexts matching (device, host thread, stream)
+    (None = any) and free their grow-only scratch; returns how many.  Contexts
+    of a worker thread are released automatically when the thread ends."""
+    idx = None
+    if device is not None:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+    sptr = stream.cuda_stream if stream is not None and hasattr(stream, "cuda_stream") else stream
+    lib = load(require_cuda=False)
+    with _lock:
+        keys = [k for k in _ctxs if (idx is None or k[0] == idx) and (thread_id is None or k[1] == thread_id)
+                and (sptr is None or k[2] == sptr)]
+        gone = [(k, _ctxs.pop(k)) for k in keys]
+    for k, c in gone:
+        _retired[k[0]] = _retired.get(k[0], 0) + int(lib.fhv_ctx_launches(c))
+        lib.fhv_ctx_destroy(c)
+    return len(gone)
+
+
+class _ThreadReaper:
+    """Thread-local sentinel: collected when its thread exits, releasing the
+    contexts that thread created."""
+
+    def __init__(self, tid: int):
+        self.tid = tid
+
+    def __del__(self):
+        try:
+            release(thread_id=self.tid)
+        except Exception:  # interpreter shutdown
+            pass
 
 
 _prof_on: dict = {}
@@ -199,7 +239,18 @@ def _device_ctxs(device: torch.device) -> list:
 def launches(device: torch.device) -> int:
     """Kernel launches issued through this library on the device (all contexts)."""
     lib = load()
-    return int(sum(lib.fhv_ctx_launches(c) for c in _device_ctxs(device)))
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    return int(sum(lib.fhv_ctx_launches(c) for c in _device_ctxs(device))) + _retired.get(idx, 0)
+
+
+def counters(device: torch.device) -> tuple:
+    """(re-sorted by the tile pass, reserved, long leaves listed for the
+    per-leaf pass) of the last synchronised EXACT_ORDER POFA build on the
+    calling thread's current context (fhv_ctx_counters)."""
+    import numpy as np
+    out = np.zeros(3, dtype=np.int64)
+    load().fhv_ctx_counters(ctx(device), out.ctypes.data, 3)
+    return tuple(int(v) for v in out)
 
 
 def prof_enable(device: torch.device, on: bool = True) -> None:

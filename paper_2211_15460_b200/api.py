@@ -16,21 +16,23 @@ __all__ = ["capture", "reconstruct"]
 
 
 def capture(scene, variant: str = "POFA", resolution=(1920, 1080), levels: int = 8, strategy=None,
-            capacity=None, overalloc: float = 10.0, exact_order: bool = False, device=None):
+            capacity=None, overalloc: float = 10.0, exact_order: bool | None = None, device=None):
     """Capture a scene into an FHV store.  ``variant`` in {PPFL, POFL, POFA};
     ``resolution`` is the RasterConfig resolution (the capture grid is
-    resolution[1]^2, fhv/raster.py:359)."""
+    resolution[1]^2, fhv/raster.py:359).  ``exact_order`` defaults to each
+    builder's own default (POFA: the reference's exact order)."""
+    order = {} if exact_order is None else {"exact_order": exact_order}
     variant = variant.upper()
     cam = capture_camera(scene, "+z", int(resolution[1]))
     cfg = RasterConfig(tuple(resolution), RasterConfig.from_camera(cam).projection, extent=1.0)
     if variant == "PPFL":
-        return build_ppfl(scene, cfg, strategy or CaptureStrategy.one_view(), capacity, overalloc,
-                          exact_order=exact_order, device=device)
+        return build_ppfl(scene, cfg, strategy or CaptureStrategy.one_view(), capacity, overalloc, device=device,
+                          **order)
     strategy = strategy or CaptureStrategy.normal_space()
     if variant == "POFL":
-        return build_pofl(scene, strategy, cfg, levels, capacity, overalloc, exact_order=exact_order, device=device)
+        return build_pofl(scene, strategy, cfg, levels, capacity, overalloc, device=device, **order)
     if variant == "POFA":
-        return pofa_build(scene, strategy, cfg, levels, exact_order=exact_order, device=device)
+        return pofa_build(scene, strategy, cfg, levels, device=device, **order)
     raise ValueError(f"unknown variant {variant!r}")
 
 

@@ -46,11 +46,27 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     if out is None and not force and up_to_date():
         return OUT
     out = out or OUT
-    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out] + \
-        [os.path.join(HERE, "csrc", f) for f in SOURCES]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True, cwd=HERE)
+    # one nvcc per translation unit, in parallel, then one link
+    import concurrent.futures
+    import tempfile
+    tmp = tempfile.mkdtemp(prefix="fhv_build_")
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    objs = [os.path.join(tmp, f.replace(".cu", ".o")) for f in SOURCES]
+
+    def compile_one(src_obj):
+        src, obj = src_obj
+        cmd = [_nvcc(), *flags, *[f"-D{d}" for d in defines], "-c", "-o", obj,
+               os.path.join(HERE, "csrc", src)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.run(cmd, check=True, cwd=HERE)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(compile_one, zip(SOURCES, objs)))
+    subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs],
+                   check=True, cwd=HERE)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(tmp)
     return out
 
 

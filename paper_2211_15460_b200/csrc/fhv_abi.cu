@@ -81,7 +81,7 @@ LaunchScope::~LaunchScope() {
 static const char* kStageNames[kNumStages] = {
     "job_setup", "scan", "item_expand", "count", "count_leaves", "emit_list", "emit_ppfl", "emit_pofl",
     "emit_pofa", "chain_order", "leaf_order", "scan_leaves", "pyramid", "splat_depth", "splat_index",
-    "splat_resolve", "raycast", "face_normals", "deferred", "ops", "scalar"};
+    "splat_resolve", "raycast", "face_normals", "deferred", "ops", "scalar", "leaf_sort"};
 
 }  // namespace fhv
 
@@ -151,6 +151,12 @@ extern "C" void fhv_ctx_destroy(fhv_ctx* ctx) {
 }
 
 extern "C" int64_t fhv_ctx_launches(const fhv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" int fhv_ctx_counters(const fhv_ctx* ctx, int64_t* out, int n) {
+  if (!ctx || !out || n < 3) return -FHV_BAD_ARGS;
+  for (int k = 0; k < 3; ++k) out[k] = (int64_t)ctx->ctl_host->leaf_n[k];
+  return 3;
+}
 
 // self-test of the shared-divisor division (fhv_common.cuh div_rn) against
 // __ddiv_rn: fast[i] = div_rn(x[i], recip_of(d[i])), ref[i] = __ddiv_rn(x[i], d[i])

@@ -40,6 +40,10 @@ static_assert(sizeof(JobSetup) == 80, "JobSetup layout");
 
 constexpr uint32_t kItemPix = 128;
 
+// internal EmitOut flag (above the public FHV_* bits): park EXACT_ORDER ranks
+// with a segment-start bit (pools < 2^31 records), for the tile fix-up
+constexpr int kSegFlags = 1 << 16;
+
 // per-job screen data of the deferred pass (strategy kScreen): clip w and
 // ndc z of the vertices in winding order, and whether the job's batch holds
 // exactly one fragment (numpy's gemv takes the ddot path then)
@@ -640,6 +644,7 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   // normal interpolation, so their L2/DRAM round trip overlaps the FP64 work
   unsigned pofa_grp = 0;
   int pofa_leader = 0;
+  bool leaf_first = false;  // this record takes its leaf's first slot
   uint32_t pofa_base = 0, pofa_cnt = 0, pofa_off = 0;
   if (kMode == kPofa) {
     pofa_grp = __match_any_sync(0xffffffffu, code);
@@ -679,6 +684,7 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
     const uint32_t base = __shfl_sync(0xffffffffu, pofa_base, pofa_leader);
     if (live) {
       const uint32_t cur = base + (uint32_t)__popc(pofa_grp & below);
+      leaf_first = cur == 0;
       if (cur >= pofa_cnt) {
         st.bad_pass = true;
       } else {
@@ -741,8 +747,12 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
     o.mat[s32] = d.mat;
     o.obj[s32] = d.obj;
     // POFA: prev_index = -1; under EXACT_ORDER the emission rank is parked
-    // here until k_leaf_order restores the reference's in-leaf order
-    if (kMode == kPofa) o.prev[s32] = (o.flags & FHV_EXACT_ORDER) ? (int32_t)(uint32_t)rank : -1;
+    // here until the fix-up restores the reference's in-leaf order; with
+    // kSegFlags its bit 31 marks the leaf's first slot (segment start)
+    if (kMode == kPofa)
+      o.prev[s32] = (o.flags & FHV_EXACT_ORDER)
+                        ? (int32_t)((uint32_t)rank | ((o.flags & kSegFlags) && leaf_first ? 0x80000000u : 0u))
+                        : -1;
   }
 }
 
@@ -1156,6 +1166,247 @@ __global__ void k_leaf_order(const uint32_t* __restrict__ offsets, const uint32_
       rk[j + 1] = r;
     }
     for (uint32_t i = 0; i < n; ++i) prev[off + i] = -1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// EXACT_ORDER for a POFA pool, over SLOTS (the pass-2 path the bench times).
+// Pass 2 parked every record's emission rank in prev, bit 31 set on the first
+// slot of its leaf (a segment start: the group leader's cursor returned 0).
+// The in-leaf order only breaks where a leaf took fragments from more than
+// one warp: a warp enumerates its fragments in emission order and a
+// same-leaf group takes consecutive cursor slots in lane order.
+//   k_leaf_fix   a warp per tile of 128 slots (+96 look-ahead): segment
+//                starts by ballots, a segment with a rank below its
+//                predecessor's is re-sorted by rank-by-count through per-warp
+//                shared memory, coalesced loads and stores.  Segments starting
+//                in the tile that do not end inside the look-ahead are listed
+//                for k_leaf_fix_big.
+//   k_leaf_fix_big  a CTA per listed segment: end by a flag search, sorted
+//                check, bitonic sort of (rank, index) keys in shared memory
+//                (<= 4096) or scratch, records gathered through scratch.
+//   prev := -1   one memset (fhv/storage.py:439).
+// No directory access at all; when nothing is out of order the cost is one
+// coalesced read of the ranks.  Result: records of each leaf in ascending
+// emission rank -- pofa_scatter's stable order (fhv/_ckern.pyx:135-142).
+
+constexpr int kSortSmem = 4096;
+constexpr uint32_t kSegBit = 0x80000000u;
+
+struct PoolRefs {
+  float* pos;
+  float* nrm;
+  uint32_t* mat;
+  uint32_t* obj;
+  uint32_t* rank;  // = prev, still holding the parked ranks (+ segment bits)
+};
+
+__device__ __forceinline__ void stage_record(const PoolRefs& pl, uint32_t* __restrict__ R, long long s) {
+  R[0] = __float_as_uint(pl.pos[3 * s]); R[1] = __float_as_uint(pl.pos[3 * s + 1]);
+  R[2] = __float_as_uint(pl.pos[3 * s + 2]); R[3] = __float_as_uint(pl.nrm[3 * s]);
+  R[4] = __float_as_uint(pl.nrm[3 * s + 1]); R[5] = __float_as_uint(pl.nrm[3 * s + 2]);
+  R[6] = pl.mat[s]; R[7] = pl.obj[s]; R[8] = pl.rank[s];
+}
+
+// the segment bit belongs to the SLOT, not the record: a moved record takes
+// the destination slot's bit (slot bits never change, so concurrent tiles
+// reading their look-ahead always see stable segment starts)
+__device__ __forceinline__ void unstage_record(const PoolRefs& pl, const uint32_t* __restrict__ R, long long t,
+                                               uint32_t slot_bit) {
+  pl.pos[3 * t] = __uint_as_float(R[0]); pl.pos[3 * t + 1] = __uint_as_float(R[1]);
+  pl.pos[3 * t + 2] = __uint_as_float(R[2]); pl.nrm[3 * t] = __uint_as_float(R[3]);
+  pl.nrm[3 * t + 1] = __uint_as_float(R[4]); pl.nrm[3 * t + 2] = __uint_as_float(R[5]);
+  pl.mat[t] = R[6]; pl.obj[t] = R[7]; pl.rank[t] = (R[8] & ~kSegBit) | slot_bit;
+}
+
+// k_leaf_fix: a WARP per tile of 128 slots (+ 96 look-ahead = 7 chunks of
+// 32), no block barriers.  Ranks in registers (coalesced), segment starts by
+// ballots, segment bounds by bit scans, disorder by a shuffle of the previous
+// rank; the elements of a disordered segment are ranked by counting over the
+// segment's ranks (per-warp shared memory) and staged at their destination in
+// per-warp shared memory, then stored back (coalesced).
+constexpr int kFixChunks = 7;
+constexpr int kFixWarpTile = 128;                     // segments starting here are this warp's
+constexpr int kFixWarpRegion = 32 * kFixChunks;       // 224
+constexpr int kFixWarps = 4;                          // warps per CTA
+
+struct FixWarpSmem {
+  uint32_t rk[kFixWarpRegion];
+  uint8_t dis[kFixWarpRegion];
+  uint8_t dst_set[kFixWarpRegion];
+  float pos[kFixWarpRegion][3], nrm[kFixWarpRegion][3];
+  uint32_t mat[kFixWarpRegion], obj[kFixWarpRegion], rank[kFixWarpRegion];
+};
+
+__global__ void __launch_bounds__(32 * kFixWarps) k_leaf_fix(PoolRefs pl, const unsigned long long* __restrict__ n_dev,
+                                                             long long cap, unsigned long long* big_list,
+                                                             unsigned long long* n_big, unsigned long long big_cap,
+                                                             unsigned long long* n_fixed_total, int* status) {
+  __shared__ FixWarpSmem smem_all[kFixWarps];
+  FixWarpSmem& S = smem_all[threadIdx.x >> 5];
+  const unsigned lane = lane_id();
+  const unsigned below = (1u << lane) - 1u;
+  long long n = (long long)*n_dev;
+  if (n > cap) n = cap;  // a short speculative pool is rebuilt by the caller anyway
+  unsigned fixed = 0;
+  const long long nwarps = (long long)gridDim.x * kFixWarps;
+  for (long long t0 = ((long long)blockIdx.x * kFixWarps + (threadIdx.x >> 5)) * kFixWarpTile; t0 < n;
+       t0 += nwarps * kFixWarpTile) {
+    const int len = (int)min((long long)kFixWarpRegion, n - t0);  // valid elements of the region
+    const bool at_end = t0 + kFixWarpRegion >= n;
+    uint32_t r[kFixChunks], fl[kFixChunks];
+#pragma unroll
+    for (int k = 0; k < kFixChunks; ++k) {
+      const int i = 32 * k + (int)lane;
+      r[k] = i < len ? pl.rank[t0 + i] : kSegBit;  // past the end: sentinel starts
+      fl[k] = __ballot_sync(0xffffffffu, (r[k] & kSegBit) != 0u);
+      S.rk[i] = r[k] & ~kSegBit;
+      S.dis[i] = 0;
+      S.dst_set[i] = 0;
+    }
+    // last start before chunk k / first start after chunk k (warp-uniform)
+    int last_before[kFixChunks], first_after[kFixChunks];
+    {
+      int lb = -1;
+#pragma unroll
+      for (int k = 0; k < kFixChunks; ++k) {
+        last_before[k] = lb;
+        if (fl[k]) lb = 32 * k + 31 - __clz(fl[k]);
+      }
+      int fa = kFixWarpRegion;
+#pragma unroll
+      for (int k = kFixChunks - 1; k >= 0; --k) {
+        first_after[k] = fa;
+        if (fl[k]) fa = 32 * k + __ffs(fl[k]) - 1;
+      }
+    }
+    int st[kFixChunks], en[kFixChunks];
+    bool own[kFixChunks];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kFixChunks; ++k) {
+      const int i = 32 * k + (int)lane;
+      const unsigned upto = fl[k] & (below | (1u << lane));    // starts at or before me in this chunk
+      const unsigned after = fl[k] & ~(below | (1u << lane));  // starts after me in this chunk
+      st[k] = upto ? 32 * k + 31 - __clz(upto) : last_before[k];
+      en[k] = after ? 32 * k + __ffs(after) - 1 : first_after[k];
+      // previous element's rank (lane 31 of the previous chunk for lane 0)
+      uint32_t prev = __shfl_up_sync(0xffffffffu, r[k], 1);
+      if (k > 0) {
+        const uint32_t carry = __shfl_sync(0xffffffffu, r[k > 0 ? k - 1 : 0], 31);
+        if (lane == 0) prev = carry;
+      }
+      own[k] = false;
+      if (i >= len || st[k] < 0 || st[k] >= kFixWarpTile) continue;
+      if (!(en[k] < kFixWarpRegion || at_end)) {  // runs past the look-ahead: the long pass sorts it
+        if (i == st[k]) {
+          const unsigned long long q = atomicAdd(n_big, 1ull);
+          if (q < big_cap)
+            big_list[q] = (unsigned long long)(t0 + i);
+          else
+            raise_status(status, FHV_NOMEM);
+        }
+        continue;
+      }
+      own[k] = true;
+      if (i > st[k] && (r[k] & ~kSegBit) < (prev & ~kSegBit)) S.dis[st[k]] = 1;
+    }
+    __syncwarp();
+    // disordered segments: rank by counting, stage at the destination
+#pragma unroll
+    for (int k = 0; k < kFixChunks; ++k) {
+      const int i = 32 * k + (int)lane;
+      const bool mv = own[k] && S.dis[st[k]];
+      if (!mv) continue;
+      if (i == st[k]) ++fixed;
+      const int lo = st[k], hi = min(en[k], len);
+      const uint32_t rr = r[k] & ~kSegBit;
+      int d = lo;
+      for (int j = lo; j < hi; ++j) d += S.rk[j] < rr ? 1 : 0;
+      const long long s_ = t0 + i;
+      S.pos[d][0] = pl.pos[3 * s_]; S.pos[d][1] = pl.pos[3 * s_ + 1]; S.pos[d][2] = pl.pos[3 * s_ + 2];
+      S.nrm[d][0] = pl.nrm[3 * s_]; S.nrm[d][1] = pl.nrm[3 * s_ + 1]; S.nrm[d][2] = pl.nrm[3 * s_ + 2];
+      S.mat[d] = pl.mat[s_];
+      S.obj[d] = pl.obj[s_];
+      S.rank[d] = rr;
+      S.dst_set[d] = 1;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kFixChunks; ++k) {
+      const int d = 32 * k + (int)lane;
+      if (d >= len || !S.dst_set[d]) continue;
+      const long long t = t0 + d;
+      pl.pos[3 * t] = S.pos[d][0]; pl.pos[3 * t + 1] = S.pos[d][1]; pl.pos[3 * t + 2] = S.pos[d][2];
+      pl.nrm[3 * t] = S.nrm[d][0]; pl.nrm[3 * t + 1] = S.nrm[d][1]; pl.nrm[3 * t + 2] = S.nrm[d][2];
+      pl.mat[t] = S.mat[d];
+      pl.obj[t] = S.obj[d];
+      pl.rank[t] = S.rank[d] | (r[k] & kSegBit);  // the segment bit stays with the slot
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fixed += __shfl_xor_sync(0xffffffffu, fixed, o);
+  if (lane == 0 && fixed) atomicAdd(n_fixed_total, (unsigned long long)fixed);
+}
+
+// long segments (did not end inside a tile's look-ahead): a CTA per segment
+__global__ void __launch_bounds__(1024) k_leaf_fix_big(PoolRefs pl, const unsigned long long* __restrict__ n_dev,
+                                                       long long cap, const unsigned long long* __restrict__ big_list,
+                                                       const unsigned long long* __restrict__ n_big,
+                                                       unsigned long long big_cap,
+                                                       unsigned long long* __restrict__ kscr,
+                                                       uint32_t* __restrict__ rscr) {
+  __shared__ unsigned long long sk[kSortSmem];
+  __shared__ long long s_end;
+  __shared__ int s_dis;
+  long long n = (long long)*n_dev;
+  if (n > cap) n = cap;
+  const unsigned long long nl = *n_big < big_cap ? *n_big : big_cap;
+  for (long long w = blockIdx.x; w < (long long)nl; w += gridDim.x) {
+    const long long off = (long long)big_list[w];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_end = n;
+      s_dis = 0;
+    }
+    __syncthreads();
+    // end: the next segment start after off (chunks of blockDim, first hit wins)
+    for (long long base = off + 1; base < n; base += blockDim.x) {
+      const long long i = base + threadIdx.x;
+      if (i < n && (pl.rank[i] & kSegBit)) atomicMin(reinterpret_cast<unsigned long long*>(&s_end),
+                                                      (unsigned long long)i);
+      __syncthreads();
+      if (s_end < n) break;
+    }
+    const long long cnt = s_end - off;
+    for (long long i = off + 1 + threadIdx.x; i < off + cnt; i += blockDim.x)
+      if ((pl.rank[i] & ~kSegBit) < (pl.rank[i - 1] & ~kSegBit)) s_dis = 1;
+    __syncthreads();
+    if (!s_dis) continue;
+    long long np2 = 1;
+    while (np2 < cnt) np2 <<= 1;
+    unsigned long long* K = np2 <= kSortSmem ? sk : kscr + 2 * off;
+    for (long long i = threadIdx.x; i < np2; i += blockDim.x)
+      K[i] = i < cnt ? ((unsigned long long)(pl.rank[off + i] & ~kSegBit) << 32) | (unsigned long long)i : ~0ull;
+    for (long long i = threadIdx.x; i < cnt; i += blockDim.x) stage_record(pl, rscr + 9 * (off + i), off + i);
+    __syncthreads();
+    for (long long k = 2; k <= np2; k <<= 1)
+      for (long long j = k >> 1; j > 0; j >>= 1) {
+        for (long long i = threadIdx.x; i < np2; i += blockDim.x) {
+          const long long l = i ^ j;
+          if (l <= i) continue;
+          const unsigned long long a = K[i], b = K[l];
+          if ((a > b) == ((i & k) == 0)) {
+            K[i] = b;
+            K[l] = a;
+          }
+        }
+        __syncthreads();
+      }
+    for (long long i = threadIdx.x; i < cnt; i += blockDim.x)
+      unstage_record(pl, rscr + 9 * (off + (long long)(K[i] & 0xffffffffull)), off + i, i == 0 ? kSegBit : 0u);
+    __syncthreads();
   }
 }
 
@@ -1783,17 +2034,22 @@ extern "C" int fhv_pofa_shard_directory(fhv_ctx* ctx, int32_t levels, const fhv_
 }
 
 // pass 2 of a POFA build, enqueued only: cursors, scatter, EXACT_ORDER fix-up
+// clear_status: the standalone scatter (fhv_pofa_scatter / shard scatter after
+// an FHV_NEED_POOL build) drops the leftover FHV_NEED_POOL / retry code; the
+// fused build keeps pass 1's status (job-setup errors such as FHV_BASIS must
+// survive into the result, fhv/raster.py:147-163).  n_frags_dev: device-side
+// fragment total (async build), else n_frags_host.
 static int pofa_scatter_async(fhv_ctx* ctx, const CaptureParams& p, int32_t levels, unsigned long long lo,
                               unsigned long long hi, const uint32_t* counts_local, const uint32_t* offsets_local,
-                              uint64_t base, fhv_pool_t* pool, int32_t flags, cudaStream_t s) {
+                              uint64_t base, fhv_pool_t* pool, int32_t flags, cudaStream_t s, bool clear_status,
+                              const unsigned long long* n_frags_dev, long long n_frags_host) {
   const unsigned long long n_local = hi - lo;
   uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_local * 4);
   if (!cursors) return FHV_NOMEM;
   int rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_local * 4, s)))) return rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->alloc, 0, 8, s)))) return rc;
-  // a retry after a speculative pass leaves its FHV_NEED_POOL behind
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->status, 0, sizeof(int), s)))) return rc;
+  if (clear_status && (rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->status, 0, sizeof(int), s)))) return rc;
   EmitOut o = empty_out();
   set_pool(o, pool);
   o.levels = levels;
@@ -1801,17 +2057,48 @@ static int pofa_scatter_async(fhv_ctx* ctx, const CaptureParams& p, int32_t leve
   o.counts = counts_local;
   o.cursors = cursors;
   o.base = base;
-  o.flags = flags;
+  // pools below 2^31 records park the rank with a segment-start bit for the
+  // tile fix-up; bigger ones keep the per-leaf walk (k_leaf_order)
+  const bool tile_fix = (flags & FHV_EXACT_ORDER) && pool->capacity > 0 && pool->capacity < (1LL << 31);
+  o.flags = flags | (tile_fix ? kSegFlags : 0);
   if ((rc = emit<kPofa>(ctx, p, o, false, s))) return rc;
-  if (flags & FHV_EXACT_ORDER) {
+  if ((flags & FHV_EXACT_ORDER) && pool->capacity > 0 && !tile_fix) {
+    LaunchScope L_(ctx, kStLeafOrder, s);
+    k_leaf_order<<<grid_for((long long)n_local, 128, 32), 128, 0, s>>>(offsets_local, counts_local, (long long)n_local,
+                                                                     base, (unsigned long long)pool->capacity,
+                                                                     pool->pos, pool->nrm, pool->mat, pool->obj,
+                                                                     pool->prev);
+    if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  }
+  if (tile_fix) {
+    const long long cap = pool->capacity;
+    const unsigned long long big_cap = (unsigned long long)(cap / kFixWarpTile + 1);
+    auto* big = (unsigned long long*)scratch(ctx, kLeafList, (size_t)big_cap * 8);
+    auto* keys = (unsigned long long*)scratch(ctx, kLeafKeys, (size_t)cap * 16);
+    auto* recs = (uint32_t*)scratch(ctx, kLeafRecs, (size_t)cap * 36);
+    auto* nn = (unsigned long long*)scratch(ctx, kTmp1, 8);
+    if (!big || !keys || !recs || !nn) return FHV_NOMEM;
+    if ((rc = check_cuda(ctx, cudaMemsetAsync(ctx->ctl->leaf_n, 0, sizeof(ctx->ctl->leaf_n), s)))) return rc;
+    if (!n_frags_dev) {
+      const unsigned long long nh = (unsigned long long)n_frags_host;
+      if ((rc = check_cuda(ctx, cudaMemcpyAsync(nn, &nh, 8, cudaMemcpyHostToDevice, s)))) return rc;
+      if ((rc = check_cuda(ctx, cudaStreamSynchronize(s)))) return rc;  // nh lives on this stack frame
+      n_frags_dev = nn;
+    }
+    PoolRefs pl{pool->pos, pool->nrm, pool->mat, pool->obj, reinterpret_cast<uint32_t*>(pool->prev)};
     {
       LaunchScope L_(ctx, kStLeafOrder, s);
-      k_leaf_order<<<grid_for((long long)n_local, 128, 32), 128, 0, s>>>(offsets_local, counts_local, (long long)n_local,
-                                                                       base, (unsigned long long)pool->capacity,
-                                                                       pool->pos, pool->nrm, pool->mat, pool->obj,
-                                                                       pool->prev);
+      const long long tiles = (cap + kFixWarpTile - 1) / kFixWarpTile;  // one warp each
+      const long long ctas = (tiles + kFixWarps - 1) / kFixWarps;
+      k_leaf_fix<<<(int)(ctas < 148LL * 12 ? ctas : 148LL * 12), 32 * kFixWarps, 0, s>>>(
+          pl, n_frags_dev, cap, big, &ctx->ctl->leaf_n[2], big_cap, &ctx->ctl->leaf_n[0], &ctx->ctl->status);
+    }
+    {
+      LaunchScope L_(ctx, kStLeafSort, s);
+      k_leaf_fix_big<<<148, 1024, 0, s>>>(pl, n_frags_dev, cap, big, &ctx->ctl->leaf_n[2], big_cap, keys, recs);
     }
     if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+    if ((rc = check_cuda(ctx, cudaMemsetAsync(pool->prev, 0xff, (size_t)cap * 4, s)))) return rc;
   }
   return FHV_OK;
 }
@@ -1837,7 +2124,9 @@ extern "C" int fhv_pofa_shard_scatter(fhv_ctx* ctx, const fhv_tris_t* tris, cons
   cudaStream_t s = (cudaStream_t)stream;
   CaptureParams p;
   if ((rc = shard_params(ctx, tris, cfg, levels, shard, false, p, s))) return rc;
-  if ((rc = pofa_scatter_async(ctx, p, levels, lo, hi, counts_local, offsets_local, base, pool, flags, s))) return rc;
+  if ((rc = pofa_scatter_async(ctx, p, levels, lo, hi, counts_local, offsets_local, base, pool, flags, s, true, nullptr,
+                                ctx->pass1_total)))
+    return rc;
   if ((rc = sync_control(ctx, s))) return rc;
   // cursors <= counts elementwise (checked per insert) and equal totals
   // imply cursors == counts (fhv/storage.py:614-619)
@@ -1886,7 +2175,8 @@ extern "C" int fhv_pofa_build(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_ca
                                               sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s))))
       return rc;
     if (pool && pool->capacity > 0 &&
-        (rc = pofa_scatter_async(ctx, p, levels, 0, n_leaves, counts, offsets, 0, pool, flags, s)))
+        (rc = pofa_scatter_async(ctx, p, levels, 0, n_leaves, counts, offsets, 0, pool, flags, s, false,
+                                 &ctx->ctl->frags_total, 0)))
       return rc;
     rc = sync_control(ctx, s);
     if (rc != FHV_RETRY_ITEMS) break;
@@ -1932,7 +2222,9 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   if (!ranks && (rc = check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total,
                                                       sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s))))
     return rc;
-  if ((rc = pofa_scatter_async(ctx, p, levels, 0, n_leaves, counts, offsets, 0, pool, flags, s))) return rc;
+  if ((rc = pofa_scatter_async(ctx, p, levels, 0, n_leaves, counts, offsets, 0, pool, flags, s, false,
+                                &ctx->ctl->frags_total, 0)))
+    return rc;
   {
     LaunchScope L_(ctx, kStScan, s);
     k_ticket<<<1, 1, 0, s>>>(ctx->ctl);

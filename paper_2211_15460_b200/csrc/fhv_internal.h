@@ -29,6 +29,7 @@ struct Control {
   unsigned int tile_counter;      // decoupled look-back tile ticket
   unsigned int pad2;
   unsigned long long spare[8];
+  unsigned long long leaf_n[3];  // EXACT_ORDER POFA: leaves listed for re-sorting (small, mid, big)
 };
 
 struct DevBuf {
@@ -43,7 +44,7 @@ namespace fhv {
 enum Stage {
   kStJobSetup = 0, kStScan, kStItemExpand, kStCount, kStCountLeaves, kStEmitList, kStEmitPpfl, kStEmitPofl,
   kStEmitPofa, kStChainOrder, kStLeafOrder, kStScanLeaves, kStPyramid, kStSplatDepth, kStSplatIndex,
-  kStSplatResolve, kStRaycast, kStFaceNormals, kStDeferred, kStOps, kStScalar, kNumStages
+  kStSplatResolve, kStRaycast, kStFaceNormals, kStDeferred, kStOps, kStScalar, kStLeafSort, kNumStages
 };
 struct PendingEvent {
   int stage;
@@ -58,7 +59,7 @@ struct fhv_ctx {
   std::vector<cudaEvent_t> event_pool;
   double stage_ms[fhv::kNumStages] = {};
   long long stage_count[fhv::kNumStages] = {};
-  fhv::DevBuf bufs[24];
+  fhv::DevBuf bufs[32];  // >= kNumBufs
   fhv::Control* ctl = nullptr;       // device
   fhv::Control* ctl_host = nullptr;  // pinned mirror
   int64_t launches = 0;
@@ -81,7 +82,7 @@ namespace fhv {
 enum BufId {
   kJobs = 0, kJobItems, kJobItemOff, kItemJob, kItemP0, kItemCnt, kItemOff, kScanStatus,
   kCursors, kChainScratch, kSplatKey, kSplatWin, kSplatBox, kRays, kTmp0, kTmp1, kTriFlag, kTriOff, kTriIndex,
-  kShardBoxes, kItemMask, kJobPersp, kNumBufs
+  kShardBoxes, kItemMask, kJobPersp, kLeafList, kLeafKeys, kLeafRecs, kNumBufs
 };
 
 // Counts a launch and, when profiling is on, brackets it with CUDA events on

@@ -108,70 +108,88 @@ def load_scene(path, material_table=None, device=None) -> Scene:
     current_material = None
     default_material = None
     n_pos = n_nrm = 0
+    pending = None  # the first SceneLoadError: faces before its line still build (and may raise first)
     with open(path, "r", encoding="utf-8") as fh:
-        for line_no, raw in enumerate(fh, start=1):
-            line = raw.strip()
-            if not line or line[0] == "#":
-                continue
-            key, *parts = line.split()
-            if key == "f":
-                if len(parts) < 3:
-                    raise SceneLoadError(path, line_no, "face needs >= 3 vertices")
-                for token in parts:
-                    fields = token.split("/")
-                    nf = len(fields)
-                    if (nf != 1 and nf != 3) or (nf == 3 and fields[1]):
-                        raise SceneLoadError(path, line_no, f"bad face token {token!r}")
-                    try:
-                        vi = int(fields[0])
-                        ni = int(fields[2]) if nf == 3 and fields[2] else None
-                    except ValueError:
-                        raise SceneLoadError(path, line_no, f"bad face token {token!r}") from None
-                    if not 1 <= vi <= n_pos:
-                        raise SceneLoadError(path, line_no, f"vertex index {vi} out of range")
-                    if ni is not None and not 1 <= ni <= n_nrm:
-                        raise SceneLoadError(path, line_no, f"normal index {ni} out of range")
-                    corner_v.append(vi - 1)
-                    corner_n.append(-1 if ni is None else ni - 1)
-                face_len.append(len(parts))
-                if current_material is not None:
-                    mat_id = current_material
+        try:
+            for line_no, raw in enumerate(fh, start=1):
+                line = raw.strip()
+                if not line or line[0] == "#":
+                    continue
+                key, *parts = line.split()
+                if key == "f":
+                    if len(parts) < 3:
+                        raise SceneLoadError(path, line_no, "face needs >= 3 vertices")
+                    for token in parts:
+                        fields = token.split("/")
+                        nf = len(fields)
+                        if (nf != 1 and nf != 3) or (nf == 3 and fields[1]):
+                            raise SceneLoadError(path, line_no, f"bad face token {token!r}")
+                        try:
+                            vi = int(fields[0])
+                            ni = int(fields[2]) if nf == 3 and fields[2] else None
+                        except ValueError:
+                            raise SceneLoadError(path, line_no, f"bad face token {token!r}") from None
+                        if not 1 <= vi <= n_pos:
+                            raise SceneLoadError(path, line_no, f"vertex index {vi} out of range")
+                        if ni is not None and not 1 <= ni <= n_nrm:
+                            raise SceneLoadError(path, line_no, f"normal index {ni} out of range")
+                        corner_v.append(vi - 1)
+                        corner_n.append(-1 if ni is None else ni - 1)
+                    face_len.append(len(parts))
+                    if current_material is not None:
+                        mat_id = current_material
+                    else:
+                        if default_material is None:
+                            default_material = len(materials)
+                            materials.append(Material())
+                            mat_names[DEFAULT_MATERIAL_NAME] = default_material
+                        mat_id = default_material
+                    face_mat.append(mat_id)
+                    obj = object_ids.get(current_group)
+                    if obj is None:
+                        obj = object_ids[current_group] = len(object_ids)
+                    face_obj.append(obj)
+                elif key == "v":
+                    if len(parts) != 3:
+                        raise SceneLoadError(path, line_no, "v needs 3 coordinates")
+                    v_vals += _floats(parts, path, line_no)
+                    n_pos += 1
+                elif key == "vn":
+                    if len(parts) != 3:
+                        raise SceneLoadError(path, line_no, "vn needs 3 coordinates")
+                    x, y, z = _floats(parts, path, line_no)
+                    # np.linalg.norm == 0 exactly when every square rounds to 0 (the
+                    # ddot's terms are non-negative): checked here, in file order
+                    if x * x == 0.0 and y * y == 0.0 and z * z == 0.0:
+                        raise SceneLoadError(path, line_no, "zero-length normal")
+                    vn_vals += (x, y, z)
+                    n_nrm += 1
+                elif key == "g":
+                    current_group = parts[0] if parts else ""
+                elif key == "usemtl":
+                    if len(parts) != 1:
+                        raise SceneLoadError(path, line_no, "usemtl needs a name")
+                    if parts[0] not in mat_names:
+                        raise SceneLoadError(path, line_no, f"unknown material {parts[0]!r}")
+                    current_material = mat_names[parts[0]]
                 else:
-                    if default_material is None:
-                        default_material = len(materials)
-                        materials.append(Material())
-                        mat_names[DEFAULT_MATERIAL_NAME] = default_material
-                    mat_id = default_material
-                face_mat.append(mat_id)
-                obj = object_ids.get(current_group)
-                if obj is None:
-                    obj = object_ids[current_group] = len(object_ids)
-                face_obj.append(obj)
-            elif key == "v":
-                if len(parts) != 3:
-                    raise SceneLoadError(path, line_no, "v needs 3 coordinates")
-                v_vals += _floats(parts, path, line_no)
-                n_pos += 1
-            elif key == "vn":
-                if len(parts) != 3:
-                    raise SceneLoadError(path, line_no, "vn needs 3 coordinates")
-                x, y, z = _floats(parts, path, line_no)
-                # np.linalg.norm == 0 exactly when every square rounds to 0 (the
-                # ddot's terms are non-negative): checked here, in file order
-                if x * x == 0.0 and y * y == 0.0 and z * z == 0.0:
-                    raise SceneLoadError(path, line_no, "zero-length normal")
-                vn_vals += (x, y, z)
-                n_nrm += 1
-            elif key == "g":
-                current_group = parts[0] if parts else ""
-            elif key == "usemtl":
-                if len(parts) != 1:
-                    raise SceneLoadError(path, line_no, "usemtl needs a name")
-                if parts[0] not in mat_names:
-                    raise SceneLoadError(path, line_no, f"unknown material {parts[0]!r}")
-                current_material = mat_names[parts[0]]
-            else:
-                raise SceneLoadError(path, line_no, f"unknown keyword {key!r}")
+                    raise SceneLoadError(path, line_no, f"unknown keyword {key!r}")
+        except SceneLoadError as err:
+            pending = err
+    vn_raw = np.asarray(vn_vals, dtype=np.float64).reshape(-1, 3)
+    # a vn whose squared norm overflows normalises to 0 at load (n / inf);
+    # make_triangle's _unit then raises SceneError at the first face (file
+    # order) using it (fhv/scene.py:75-78) -- before any later line is parsed,
+    # so before a pending SceneLoadError of a later line
+    if len(vn_raw):
+        cn_all = np.asarray(corner_n[:sum(face_len)], dtype=np.int64)  # corners of completed faces
+        with np.errstate(over="ignore"):
+            zero_row = np.isinf(np.einsum("ij,ij->i", vn_raw, vn_raw))
+        bad = (cn_all >= 0) & zero_row[np.maximum(cn_all, 0)]
+        if bad.any():
+            raise SceneError("zero-length direction")
+    if pending is not None:
+        raise pending
     if not face_len:
         raise SceneLoadError(path, 0, "empty scene (no faces)")
     if not materials:
@@ -179,7 +197,6 @@ def load_scene(path, material_table=None, device=None) -> Scene:
     dev = default_device(device)
     P = np.asarray(v_vals, dtype=np.float64).reshape(-1, 3)
     # vn normalisation at load (n / np.linalg.norm(n)); zero rows were rejected above
-    vn_raw = np.asarray(vn_vals, dtype=np.float64).reshape(-1, 3)
     vn, zero = _unit_rows(vn_raw, dev)
     assert zero < 0
     # make_triangle's _unit of each given normal (per distinct normal: deterministic)

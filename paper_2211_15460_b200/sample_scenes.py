@@ -7,7 +7,9 @@ golden vectors taken from the reference.  The bench scenes (SURVEY.md
 section 8(d), configs C1-C5) are defined here; the large ones are built
 struct-of-arrays instead of one ``make_triangle`` call per triangle, with the
 same arithmetic (``np.vecdot`` reproduces the BLAS ddot norm used by
-``make_triangle`` -- checked in tests/test_scene.py).
+``make_triangle``): byte-identical to the same fields built by the
+reference's own ``icosphere`` / ``make_triangle`` (tests/test_scene_pinning.py
+against tests/golden/scenes_big.json).
 """
 from __future__ import annotations
 

@@ -326,7 +326,7 @@ def _shard_struct(lo: int, hi: int, levels: int) -> _lib.Shard:
 
 
 def pofa_build_shard(scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int, comm: Comm,
-                     ranges: list | None = None, balance: bool = True, exact_order: bool = False,
+                     ranges: list | None = None, balance: bool = True, exact_order: bool = True,
                      device=None, tris=None) -> FhvPofaShard:
     """This rank's share of ``pofa_build(scene, strategy, cfg, levels)``."""
     if levels < 4:

@@ -407,6 +407,7 @@ class FhvPofa:
         return np.arange(off, off + int(self.directory.counts[code]), dtype=np.int64)
 
     pending = None  # (ticket, guessed total, synchronous rebuild) of an asynchronous pofa_build
+    done = None     # CUDA event recorded after the asynchronous build's ticket copy
 
     def wait(self) -> "FhvPofa":
         """Finish an asynchronous build: synchronise, check its ticket, and
@@ -414,7 +415,10 @@ class FhvPofa:
         the build's own error otherwise."""
         if self.pending is None:
             return self
-        torch.cuda.current_stream(self.pool.device).synchronize()
+        if self.done is not None:  # the build's stream, whichever stream is current now
+            self.done.synchronize()
+        else:
+            torch.cuda.current_stream(self.pool.device).synchronize()
         rc = check_ticket(self)
         rebuild = self.pending[2]
         self.pending = None
@@ -520,10 +524,14 @@ def build_pofl(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
 
 
 def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int, threads: int = 1, *,
-               exact_order: bool = False, device=None, tris=None, sync: bool = True,
+               exact_order: bool = True, device=None, tris=None, sync: bool = True,
                ticket: torch.Tensor | None = None) -> FhvPofa:
     """Two-pass per-octant arrays (fhv/storage.py:590-621): per-leaf histogram,
     exclusive scan (+ pyramid), exact pool, scatter into leaf ranges.
+    ``exact_order`` (default, the reference's pool byte for byte): records of a
+    leaf in emission order, restored by a slot-order fix-up that re-sorts only
+    the leaves several warps wrote; ``exact_order=False`` keeps the paper's
+    atomic in-leaf order (per-leaf multiset equal).
     ``tris``: a DeviceScene already holding this scene's triangle arrays (e.g.
     one of several buffers a pipelined caller fills asynchronously); default:
     the scene's cached upload.
@@ -536,8 +544,9 @@ def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     in place when the speculation was wrong."""
     if levels < 1:
         raise FhvError("octree needs at least one level")
-    if levels > 11:
-        raise FhvError(f"levels {levels}: dense POFA directories beyond L=11 exceed device memory")
+    if levels > 10:
+        raise FhvError(f"levels {levels}: dense POFA directories beyond L=10 (8^10 leaves, 4 GiB of offsets + counts) "
+                       "are not supported on the device")
     plan, c = _plan_cfg(scene, strategy, cfg)
     ds = tris if tris is not None else device_scene(scene, device)
     dev = ds.device
@@ -569,6 +578,10 @@ def pofa_build(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
                       scene.materials)
         vol.pending = (tk, guess, lambda: pofa_build(scene, strategy, cfg, levels, threads, exact_order=exact_order,
                                                      device=device, tris=tris))
+        if not torch.cuda.is_current_stream_capturing():
+            done = torch.cuda.Event()  # after the ticket copy, on the build's own stream
+            done.record(torch.cuda.current_stream(dev))
+            vol.done = done
         return vol
     pool = FragmentPool(guess, dev, fill_prev=False) if guess is not None else None  # pass 2 writes every prev
     tr = ds.struct()
@@ -597,6 +610,8 @@ def check_ticket(vol) -> int:
     synchronised): FHV_OK, FHV_STALE (speculation wrong, outputs invalid) or
     the build's own error code."""
     tk, guess, _ = vol.pending
+    if getattr(vol, "done", None) is not None:
+        vol.done.synchronize()
     return ticket_status(tk, guess)
 
 

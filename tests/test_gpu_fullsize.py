@@ -13,7 +13,7 @@ import torch
 
 import paper_2211_15460_b200 as fhv
 from oracle import oracle as orc
-from paper_2211_15460_b200 import sample_scenes
+from paper_2211_15460_b200 import _lib, sample_scenes
 from paper_2211_15460_b200.device import DeviceScene
 from paper_2211_15460_b200.lights import headlight
 from paper_2211_15460_b200.render import image_numpy
@@ -62,8 +62,16 @@ def test_c3_full_size_pofa_and_splat_bit_exact():
     h = gpu.pool.numpy()
     for k in ("position", "normal", "material_id", "object_id", "prev_index"):
         assert np.array_equal(h[k], ref["pool"][k]), k
-    # the fast (bench) mode: same directory, same records per leaf (any order)
-    fast = fhv.pofa_build(s, ns, cfg, 8)
+    fixed, _, long_ = _lib.counters(torch.device("cuda", 0))  # leaves the slot-order fix-up re-sorted
+    print(f"exact-order fix-up: {fixed} leaves re-sorted by the tile pass, {long_} long leaves listed")
+    # the bench's step: asynchronous build (pool sized by the last total, outcome
+    # in a ticket), EXACT_ORDER -- byte-identical records
+    av = fhv.pofa_build(s, ns, cfg, 8, exact_order=True, sync=False).wait()
+    ha = av.pool.numpy()
+    for k in ("position", "normal", "material_id", "object_id", "prev_index"):
+        assert np.array_equal(ha[k], ref["pool"][k]), k
+    # the paper's atomic in-leaf order (--fast-order): same directory, same records per leaf (any order)
+    fast = fhv.pofa_build(s, ns, cfg, 8, exact_order=False)
     assert torch.equal(fast.directory.offsets, gpu.directory.offsets)
     fp = fast.pool.position.cpu().numpy()
     srt = lambda a: a[np.lexsort(a.T[::-1])]  # noqa: E731

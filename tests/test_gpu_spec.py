@@ -227,3 +227,23 @@ def test_async_build_in_a_cuda_graph(delta):
     else:
         assert bad == fhv._lib.FHV_STALE
     ds._pofa_totals[key] = ref.pool.next_free
+
+
+@pytest.mark.parametrize("exact", (False, True))
+def test_job_setup_error_survives_pool_guess(exact):
+    """A pipelined ``tris=`` buffer that already holds a pool guess: a scene
+    whose face normal is not unit must still raise ValueError (tangent_basis,
+    fhv/raster.py:147-163) -- pass 1's job-setup status is not cleared before
+    pass 2 (the fused fhv_pofa_build path, synchronous and asynchronous)."""
+    good = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+    cfg = _cfg(good, 64)
+    ds = fhv.device.DeviceScene(good, torch.device("cuda", 0))
+    fhv.pofa_build(good, ns, cfg, 4, exact_order=exact, tris=ds)  # stores the guess on ds
+    bad_fn = good.face_normals.copy()
+    bad_fn[5] *= 2.0
+    ds.fnrm.copy_(torch.from_numpy(bad_fn))
+    with pytest.raises(ValueError):
+        fhv.pofa_build(good, ns, cfg, 4, exact_order=exact, tris=ds)
+    with pytest.raises(ValueError):
+        fhv.pofa_build(good, ns, cfg, 4, exact_order=exact, tris=ds, sync=False).wait()
