@@ -160,8 +160,9 @@ void fhv_ctx_destroy(fhv_ctx *ctx);
 /* kernels launched by this context since creation (for launch accounting) */
 int64_t fhv_ctx_launches(const fhv_ctx *ctx);
 /* diagnostics of the last SYNCHRONISED call on this context: out[0] = leaves
-   the EXACT_ORDER POFA tile fix-up re-sorted, out[1] = 0 (reserved), out[2] =
-   long leaves handed to the per-leaf pass; returns the words written (3) */
+   the EXACT_ORDER POFA tile fix-up re-sorted, out[1] = fragments the raster
+   passes sent through the exact (uncertified) path, out[2] = long leaves
+   handed to the per-leaf pass; returns the words written (3) */
 int fhv_ctx_counters(const fhv_ctx *ctx, int64_t *out, int n);
 
 /* per-kernel CUDA-event timing on the launching stream (off by default).

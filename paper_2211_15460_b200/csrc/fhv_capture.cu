@@ -24,6 +24,8 @@
 // (-fmad=false + explicit __fma_rn where NumPy/OpenBLAS fuse), so the covered
 // set, counts and octant ranges are bit-exact; interpolated attributes follow
 // the same operation order and match bit for bit as well.
+#include <cstdlib>
+
 #include "fhv_common.cuh"
 #include "fhv_internal.h"
 
@@ -43,6 +45,9 @@ constexpr uint32_t kItemPix = 128;
 // internal EmitOut flag (above the public FHV_* bits): park EXACT_ORDER ranks
 // with a segment-start bit (pools < 2^31 records), for the tile fix-up
 constexpr int kSegFlags = 1 << 16;
+// internal EmitOut flag: emission through the all-exact per-fragment path
+// (k_emit) instead of the certified fast path (k_emit_fast) -- A/B testing
+constexpr int kExactMath = 1 << 17;
 
 // per-job screen data of the deferred pass (strategy kScreen): clip w and
 // ndc z of the vertices in winding order, and whether the job's batch holds
@@ -490,6 +495,10 @@ enum RasterMode { kCnt = 0, kCntLeaves = 1, kList = 2, kPpfl = 3, kPofl = 4, kPo
 #endif
 constexpr int kRasterBlock = FHV_RASTER_BLOCK;
 constexpr int kRasterWarps = kRasterBlock / 32;
+#ifndef FHV_EMIT_FAST_WARPS
+#define FHV_EMIT_FAST_WARPS 8
+#endif
+constexpr int kEmitFastWarps = FHV_EMIT_FAST_WARPS;
 
 template <int kMode, bool kAtomicAlloc>
 struct RasterState {
@@ -756,7 +765,337 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   }
 }
 
-template <int kMode, bool kAtomicAlloc>
+// ---------------------------------------------------------------------------
+// Certified fast path for the f32 record fields (POFA / POFL / PPFL records
+// and the POFA counting pass's leaf keys).
+//
+// The reference computes, per fragment, l_i = f_i / area2 (correctly rounded
+// f64 edge functions), pos = lam @ V as an fma chain, f32(pos); nrm = lam @ N,
+// / sqrt(einsum), f32.  Every one of those values is the f64 rounding of an
+// AFFINE function of the pixel, so per item (one lane each) we build planes
+// value(X, Y) = A + B X + C Y over the job's bbox (X = px - x0, Y = py - y0)
+// and a bound E on |plane - reference| that holds for every pixel of the item
+// (rounding of the reference's own chain + of the plane coefficients + of the
+// evaluation; derivation in DESIGN.md section 4).  A fragment evaluates the
+// planes with 2 fmas per component and rounds [v - E, v + E] to f32: when
+// both ends give the same nonzero float, that float IS the reference's f32 --
+// rounding is monotone.  Otherwise (a value within E of an f32 rounding
+// boundary, or of zero) the fragment takes the exact path.  Components that
+// are zero at all three vertices are +0.0 in the reference (the chain starts
+// 0 + l0 * 0) and are written directly.  Normals: unit vector of the plane
+// value through rsqrt + one Newton step whose own residual bounds its error.
+// Bit-identical records either way; ~3x fewer instructions per fragment.
+
+constexpr double kU53 = 1.1102230246251565e-16;  // 2^-53, unit roundoff
+constexpr uint32_t kPlanesBad = 0x80000000u;      // zmask bit: planes unusable -> exact path
+
+struct __align__(16) PosPlanes {  // the counting pass: positions only
+  double A[3], B[3], C[3];
+  double ep;
+  int32_t x0, y0;
+  uint32_t zmask;
+  uint32_t pad;
+};
+
+struct __align__(16) ItemFast {  // the emission pass: positions + vertex normals, enumeration fields
+  double A[6], B[6], C[6];
+  double ep, en;
+  int32_t x0, y0, bw;
+  uint32_t p0;
+  float inv_bw;
+  uint32_t zmask;  // bits 0-2 position, 3-5 normal components zero at all vertices; kPlanesBad
+  uint32_t mat, obj;
+};
+
+// shared per-item quantities of the planes: edge-function values at the bbox
+// origin pixel centre, 1/area2, and K = sum_i (|e_ix| Hd + |e_iy| Wd) / area2
+// (bounds |F_i|/area2-weighted sums over every pixel of the bbox)
+struct PlaneBasis {
+  double f00[3];
+  double ex[3], ey[3];
+  double r, K, er;  // r ~ 1/area2 with relative error <= er
+  bool ok;
+};
+
+__device__ __forceinline__ PlaneBasis plane_basis(const CoverS& c) {
+  PlaneBasis b;
+  const double sx0 = (double)c.x0 + 0.5, sy0 = (double)c.y0 + 0.5;
+  // F_0 is based at vertex 1 (b), F_1 at vertex 2 (c), F_2 at vertex 0 (a) -- cover_test's forms
+  b.ex[0] = c.e0x; b.ey[0] = c.e0y;
+  b.ex[1] = c.e1x; b.ey[1] = c.e1y;
+  b.ex[2] = c.e2x; b.ey[2] = c.e2y;
+  b.f00[0] = __fma_rn(c.e0x, sy0 - c.by, -(c.e0y * (sx0 - c.bx)));
+  b.f00[1] = __fma_rn(c.e1x, sy0 - c.cy, -(c.e1y * (sx0 - c.cx)));
+  b.f00[2] = __fma_rn(c.e2x, sy0 - c.ay, -(c.e2y * (sx0 - c.ax)));
+  const double wd = (fmax(c.ax, fmax(c.bx, c.cx)) - fmin(c.ax, fmin(c.bx, c.cx))) + 1.0;
+  const double hd = (fmax(c.ay, fmax(c.by, c.cy)) - fmin(c.ay, fmin(c.by, c.cy))) + 1.0;
+  // 1/area2 by rcp.approx + one Newton step; its residual bounds its error
+  double r0;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(c.area2));
+  const double e0 = __fma_rn(-c.area2, r0, 1.0);
+  b.r = __fma_rn(r0, e0, r0);
+  b.er = fabs(__fma_rn(-c.area2, b.r, 1.0)) + 4.0 * kU53;
+  b.K = __fma_rn(fabs(c.e0x) + fabs(c.e1x) + fabs(c.e2x), hd, (fabs(c.e0y) + fabs(c.e1y) + fabs(c.e2y)) * wd) * b.r;
+  b.ok = c.area2 > 1e-300 && isfinite(b.K);
+  return b;
+}
+
+// planes of one 3-component attribute (vertex values W[i][k], winding order)
+__device__ __forceinline__ void attr_planes(const PlaneBasis& b, const double W[3][3], double* A, double* B, double* C,
+                                            double& err, uint32_t& zbits, bool& ok) {
+  double M = 0.0;
+  zbits = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    A[k] = __fma_rn(b.f00[2], W[2][k], __fma_rn(b.f00[1], W[1][k], b.f00[0] * W[0][k])) * b.r;
+    B[k] = -__fma_rn(b.ey[2], W[2][k], __fma_rn(b.ey[1], W[1][k], b.ey[0] * W[0][k])) * b.r;
+    C[k] = __fma_rn(b.ex[2], W[2][k], __fma_rn(b.ex[1], W[1][k], b.ex[0] * W[0][k])) * b.r;
+    M = fmax(M, fmax(fabs(W[0][k]), fmax(fabs(W[1][k]), fabs(W[2][k]))));
+    zbits |= (W[0][k] == 0.0 && W[1][k] == 0.0 && W[2][k] == 0.0) ? 1u << k : 0u;
+  }
+  // reference rounding u M (6 + 3K), coefficient rounding ~21 u M K, evaluation
+  // ~5 u M K, the interval ends' own rounding ~3 u M K: x2 margin; plus the
+  // relative error of r on the three plane terms (<= 3 M K)
+  err = M * __fma_rn(kU53 * 64.0 + 4.0 * b.er, b.K, kU53 * 16.0);
+  ok = ok && isfinite(err);  // non-finite vertex data -> M non-finite -> exact path
+}
+
+__device__ __forceinline__ bool cert_f32(double x, double e, float& out) {
+  const float lo = __double2float_rn(__dsub_rn(x, e));
+  const float hi = __double2float_rn(__dadd_rn(x, e));
+  out = lo;
+  return lo == hi && lo != 0.0f;  // NaN fails; a zero would leave its sign undecided
+}
+
+__device__ __forceinline__ bool fast_pos(const double* A, const double* B, const double* C, double ep, uint32_t zbits,
+                                         int X, int Y, float out[3]) {
+  const double xd = (double)X, yd = (double)Y;
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float f;
+    const bool c = cert_f32(__fma_rn(C[k], yd, __fma_rn(B[k], xd, A[k])), ep, f);
+    const bool z = (zbits >> k) & 1u;
+    out[k] = z ? 0.0f : f;
+    ok = ok && (z || c);
+  }
+  return ok;
+}
+
+__device__ __forceinline__ bool fast_nrm(const double* A, const double* B, const double* C, double en, uint32_t zbits,
+                                         int X, int Y, float out[3]) {
+  const double xd = (double)X, yd = (double)Y;
+  double v[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double t = __fma_rn(C[k], yd, __fma_rn(B[k], xd, A[k]));
+    v[k] = ((zbits >> k) & 1u) ? 0.0 : t;
+  }
+  const double q = __fma_rn(v[2], v[2], __fma_rn(v[1], v[1], __dmul_rn(v[0], v[0])));
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(q));
+  const double e = __fma_rn(-__dmul_rn(q, y0), y0, 1.0);
+  const double y = __fma_rn(y0, __dmul_rn(0.5, e), y0);
+  // |y sqrt(q) - 1| <= 3/8 e^2 + rounding; the reference's own normalisation
+  // and the plane error (x 2 sqrt(3) / |v|), doubled
+  const double eo = __fma_rn(7.0 * en, y, __fma_rn(e, e, 16.0 * kU53));
+  bool ok = q > 1e-20;  // the reference's 1e-12 face-normal fallback region (and NaN) -> exact path
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float f;
+    const bool c = cert_f32(__dmul_rn(v[k], y), eo, f);
+    const bool z = (zbits >> k) & 1u;
+    out[k] = z ? 0.0f : f;
+    ok = ok && (z || c);
+  }
+  return ok;
+}
+
+// the exact path of one fragment (rare): f64 edge functions, correctly rounded
+// barycentrics, the reference's fma chains, sqrt + divisions; f32 record fields
+struct Rec6 {
+  float w[3], n[3];
+};
+
+__device__ __noinline__ Rec6 exact_record(const double* __restrict__ gpos, const double* __restrict__ gvnrm,
+                                          const double* __restrict__ gfnrm, const JobSetup* __restrict__ job, int px,
+                                          int py, bool want_nrm) {
+  Rec6 out;
+  float* fw = out.w;
+  float* fn = out.n;
+  fn[0] = fn[1] = fn[2] = 0.f;
+  const JobSetup js = *job;
+  CoverS c;
+  make_cover(js, 0u, c);
+  double f0, f1, f2;
+  cover_test(c, px, py, f0, f1, f2);
+  const double l0 = ddiv_zd_sel(f0, c.area2), l1 = ddiv_zd_sel(f1, c.area2), l2 = ddiv_zd_sel(f2, c.area2);
+  const int o[3] = {0, c.swapped ? 2 : 1, c.swapped ? 1 : 2};
+  TriData d;
+  const double* P = gpos + 9 * (long long)c.tri;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d.v[i][k] = P[3 * o[i] + k];
+  double w[3];
+  interp_pos(d, l0, l1, l2, w);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) fw[k] = __double2float_rn(w[k]);
+  if (!want_nrm) return out;
+  const double* N = gvnrm + 9 * (long long)c.tri;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d.n[i][k] = N[3 * o[i] + k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) d.f[k] = gfnrm[3 * (long long)c.tri + k];
+  double nn[3];
+  interp_nrm(d, l0, l1, l2, nn);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) fn[k] = __double2float_rn(nn[k]);
+  return out;
+}
+
+// one batch of <= 32 fragments through the certified fast path (modes
+// kCntLeaves, kPpfl, kPofl, kPofa); the store logic mirrors raster_batch
+template <int kMode, bool kAtomicAlloc, class Pl>
+__device__ __forceinline__ void raster_batch_fast(const CaptureParams& p, const EmitOut& o, Control* ctl,
+                                                  const JobSetup* __restrict__ jobs, const Pl* planes, bool valid,
+                                                  int k, int px, int py, uint32_t push_local, uint32_t* own_cnt,
+                                                  unsigned long long rank0, const uint32_t* item_job_g,
+                                                  RasterState<kMode, kAtomicAlloc>& st) {
+  static_assert(kMode == kCntLeaves || kMode == kPpfl || kMode == kPofl || kMode == kPofa, "fast modes");
+  constexpr bool kKeyed = kMode == kCntLeaves || kMode == kPofl || kMode == kPofa;
+  constexpr bool kOwned = kMode == kCntLeaves || kMode == kPofa;
+  constexpr bool kNrm = kMode != kCntLeaves;
+  const unsigned lane = lane_id();
+  const unsigned below = (1u << lane) - 1u;
+  bool live = false;
+  float fw[3] = {0.f, 0.f, 0.f}, fn[3] = {0.f, 0.f, 0.f};
+  uint32_t rmat = 0, robj = 0;
+  uint64_t code = ~0ull;
+  if (valid) {
+    const Pl& P = planes[k];
+    const int X = px - P.x0, Y = py - P.y0;
+    bool ok = !(P.zmask & kPlanesBad) && fast_pos(P.A, P.B, P.C, P.ep, P.zmask, X, Y, fw);
+    if constexpr (kNrm) {
+      ok = ok && fast_nrm(P.A + 3, P.B + 3, P.C + 3, P.en, P.zmask >> 3, X, Y, fn);
+      rmat = P.mat;
+      robj = P.obj;
+    }
+    if (!ok) {
+      atomicAdd(&ctl->leaf_n[1], 1ull);  // diagnostics: fragments through the exact path
+      const Rec6 r = exact_record(p.pos, p.vnrm, p.fnrm, jobs + item_job_g[k], px, py, kNrm);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        fw[q] = r.w[q];
+        fn[q] = r.n[q];
+      }
+    }
+    live = true;
+    if (kKeyed) {
+      if (!cell_code(fw[0], fw[1], fw[2], o.levels, &code)) {
+        st.bad_range = true;
+        live = false;
+        code = ~0ull;
+      } else if (code < p.cell_lo || code >= p.cell_hi) {  // another shard's leaf
+        live = false;
+        code = ~0ull;
+      }
+    }
+    if (kNrm && live) ++st.emitted;
+  }
+  uint32_t local = push_local;
+  const bool whole = p.cell_lo == 0 && p.cell_hi >= (1ull << (3 * o.levels));
+  if (kOwned && !whole) {
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    const unsigned grp = __match_any_sync(0xffffffffu, valid ? k : -1);
+    local = own_cnt[k] + (uint32_t)__popc(grp & m & below);
+    __syncwarp();
+    if (valid && (int)lane == 31 - __clz(grp)) own_cnt[k] += (uint32_t)__popc(grp & m);
+    __syncwarp();
+  }
+  const unsigned long long rank = __shfl_sync(0xffffffffu, rank0, k) + local;
+  if (kMode == kCntLeaves) {
+    const unsigned grp = __match_any_sync(0xffffffffu, code);
+    if (live && (int)lane == __ffs(grp) - 1) atomicAdd(&o.leaf_counts[code - p.cell_lo], (uint32_t)__popc(grp));
+    return;
+  }
+  long long slot = -1;
+  bool leaf_first = false;
+  if (kMode == kPofa) {
+    const unsigned grp = __match_any_sync(0xffffffffu, code);
+    const int leader = __ffs(grp) - 1;
+    const unsigned long long lc = live ? code - p.cell_lo : 0ull;
+    uint32_t off = 0, cnt = 0, base = 0;
+    if (live) {
+      off = __ldg(&o.offsets[lc]);
+      cnt = lc + 1 < p.cell_hi - p.cell_lo ? __ldg(&o.offsets[lc + 1]) - off : __ldg(&o.counts[lc]);
+    }
+    if (live && (int)lane == leader) base = atomicAdd(&o.cursors[lc], (uint32_t)__popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (live) {
+      const uint32_t cur = base + (uint32_t)__popc(grp & below);
+      leaf_first = cur == 0;
+      if (cur >= cnt) {
+        st.bad_pass = true;
+      } else {
+        slot = (long long)(off - o.base) + cur;
+        if (slot >= o.capacity) {  // speculative pool smaller than the exact count
+          st.short_pool = true;
+          slot = -1;
+        }
+      }
+    }
+  } else {
+    if (kAtomicAlloc) {
+      const unsigned m = __ballot_sync(0xffffffffu, live);
+      unsigned long long base = 0;
+      if (m && lane == (unsigned)(__ffs(m) - 1)) base = atomicAdd(&ctl->alloc, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, m ? __ffs(m) - 1 : 0);
+      if (live) slot = (long long)(base + __popc(m & below));
+    } else if (live) {
+      slot = (long long)rank;
+    }
+    if (slot >= o.capacity) slot = -1;
+    uint64_t key = ~0ull;
+    if (slot >= 0) {
+      if (kMode == kPpfl) {
+        key = (uint64_t)py * (uint64_t)o.width + (uint64_t)px;
+        if ((long long)key >= o.n_keys) {
+          st.bad_key = true;
+          slot = -1;
+          key = ~0ull;
+        }
+      } else {
+        key = code;
+      }
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const int last = 31 - __clz(grp);
+    int32_t old = -1;
+    if (slot >= 0 && (int)lane == last) old = atomicExch(&o.heads[key], (int32_t)slot);
+    old = __shfl_sync(0xffffffffu, old, last);
+    const unsigned lower = grp & below;
+    const int32_t prev_slot = __shfl_sync(0xffffffffu, (int32_t)slot, lower ? 31 - __clz(lower) : (int)lane);
+    if (slot >= 0) o.prev[slot] = lower ? prev_slot : old;
+  }
+  if (slot >= 0) {
+    const uint32_t s32 = (uint32_t)slot;
+    float* pp = o.pos + 3ull * s32;
+    float* np = o.nrm + 3ull * s32;
+    pp[0] = fw[0]; pp[1] = fw[1]; pp[2] = fw[2];
+    np[0] = fn[0]; np[1] = fn[1]; np[2] = fn[2];
+    o.mat[s32] = rmat;
+    o.obj[s32] = robj;
+    if (kMode == kPofa)
+      o.prev[s32] = (o.flags & FHV_EXACT_ORDER)
+                        ? (int32_t)((uint32_t)rank | ((o.flags & kSegFlags) && leaf_first ? 0x80000000u : 0u))
+                        : -1;
+  }
+}
+
+template <int kMode, bool kAtomicAlloc, bool kFast = false>
 __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(CaptureParams p, const JobSetup* __restrict__ jobs,
                                                          const uint32_t* __restrict__ item_job,
                                                          const uint32_t* __restrict__ item_p0,
@@ -767,13 +1106,15 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
   static_assert(kMode == kCnt || kMode == kCntLeaves, "k_raster is the counting pass; emission is k_emit");
   constexpr bool kOwned = kMode == kCntLeaves || kMode == kPofa;
   __shared__ CoverS cs_all[kRasterWarps][32];
-  __shared__ double rcp_all[kRasterWarps][32];  // recip_of(area2).y per item (kept out of CoverS: the sweep's stride)
   __shared__ int32_t qpx_all[kRasterWarps][64], qpy_all[kRasterWarps][64];
   __shared__ uint32_t qmeta_all[kRasterWarps][64];
+  __shared__ double rcp_all[kRasterWarps][32];  // recip_of(area2).y per item (kept out of CoverS: the sweep's stride)
   __shared__ uint32_t own_all[kRasterWarps][32];
   __shared__ uint32_t ijob_all[kRasterWarps][32];
+  extern __shared__ __align__(16) unsigned char raster_dyn[];  // kFast: PosPlanes[kRasterWarps][32]
   const unsigned lane = lane_id();
   const int wib = threadIdx.x >> 5;
+  PosPlanes* pp = reinterpret_cast<PosPlanes*>(raster_dyn) + 32 * wib;
   CoverS* cs = cs_all[wib];
   int32_t* q_px = qpx_all[wib];
   int32_t* q_py = qpy_all[wib];
@@ -801,13 +1142,27 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
       const uint32_t p0 = item_p0[item];
       const unsigned long long pe = (unsigned long long)js.bw * (unsigned long long)js.bh;
       npix = (unsigned long long)p0 + kItemPix < pe ? kItemPix : (uint32_t)(pe - p0);
-      if (kMode == kCntLeaves) {  // the positions the keying batches read
+      make_cover(js, p0, cs[lane]);
+      if (kMode == kCntLeaves && !kFast) {  // the positions the keying batches read; their shared reciprocal
         const char* P = reinterpret_cast<const char*>(p.pos + 9 * (long long)js.tri);
         prefetch_l1(P);
         prefetch_l1(P + 64);
+        rcp_all[wib][lane] = recip_of(cs[lane].area2 > 0.0 ? cs[lane].area2 : 1.0).y;
       }
-      make_cover(js, p0, cs[lane]);
-      rcp_all[wib][lane] = recip_of(cs[lane].area2 > 0.0 ? cs[lane].area2 : 1.0).y;
+      if (kMode == kCntLeaves && kFast) {  // position planes of my item (certified fast keys)
+        TriData d;
+        load_tri_pos(p, js.tri, js.swapped, d);
+        const PlaneBasis b = plane_basis(cs[lane]);
+        PosPlanes& P = pp[lane];
+        bool ok = b.ok;
+        uint32_t z = 0;
+        double e = 0.0;
+        attr_planes(b, d.v, P.A, P.B, P.C, e, z, ok);
+        P.ep = e;
+        P.x0 = js.x0;
+        P.y0 = js.y0;
+        P.zmask = z | (ok ? 0u : kPlanesBad);
+      }
       ijob[lane] = jid;
       if (!kOwned && kMode != kCnt && !kAtomicAlloc) rank0 = item_off[item];
       if (kOwned && kMode == kPofa) rank0 = item_off[item];
@@ -883,8 +1238,12 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
         __syncwarp();
         {
           const uint32_t mt = q_meta[lane];
-          raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, true, (int)(mt & 31u), q_px[lane], q_py[lane], mt >> 5,
-                                            own_cnt, rank0, ijob, st, rcp_all[wib]);
+          if constexpr (kMode == kCntLeaves && kFast)
+            raster_batch_fast<kMode, kAtomicAlloc>(p, o, ctl, jobs, pp, true, (int)(mt & 31u), q_px[lane],
+                                                   q_py[lane], mt >> 5, own_cnt, rank0, ijob, st);
+          else if constexpr (kMode == kCntLeaves)
+            raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, true, (int)(mt & 31u), q_px[lane], q_py[lane], mt >> 5,
+                                              own_cnt, rank0, ijob, st, rcp_all[wib]);
         }
         __syncwarp();
         if ((int)lane < qn - 32) {
@@ -900,8 +1259,12 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_raster(Captur
       __syncwarp();
       const bool v = (int)lane < qn;
       const uint32_t mt = v ? q_meta[lane] : 0u;
-      raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, v, (int)(mt & 31u), v ? q_px[lane] : 0, v ? q_py[lane] : 0,
-                                        mt >> 5, own_cnt, rank0, ijob, st, rcp_all[wib]);
+      if constexpr (kMode == kCntLeaves && kFast)
+        raster_batch_fast<kMode, kAtomicAlloc>(p, o, ctl, jobs, pp, v, (int)(mt & 31u), v ? q_px[lane] : 0,
+                                               v ? q_py[lane] : 0, mt >> 5, own_cnt, rank0, ijob, st);
+      else if constexpr (kMode == kCntLeaves)
+        raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, v, (int)(mt & 31u), v ? q_px[lane] : 0, v ? q_py[lane] : 0,
+                                          mt >> 5, own_cnt, rank0, ijob, st, rcp_all[wib]);
     }
     __syncwarp();
     if (item < n_items) {
@@ -1050,6 +1413,173 @@ __global__ void __launch_bounds__(kRasterBlock, FHV_RASTER_MINB) k_emit(CaptureP
         py = c.y0 + (int)r;
       }
       raster_batch<kMode, kAtomicAlloc>(p, o, ctl, cs, valid, k, px, py, local, own_cnt, rank0, ijob, st);
+    }
+    __syncwarp();
+  }
+  if (kMode == kPofa) {
+    // pass-2 emitted count (compared with pass 1, fhv/storage.py:614-617)
+    unsigned long long e = st.emitted;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+    if (lane == 0 && e) atomicAdd(&ctl->alloc, e);
+  }
+  if (st.bad_range) raise_status(&ctl->status, FHV_RANGE);
+  if (st.bad_pass) raise_status(&ctl->status, FHV_PASS_MISMATCH);
+  if (st.bad_key) raise_status(&ctl->status, FHV_BAD_ARGS);
+  if (st.short_pool) raise_status(&ctl->status, FHV_NEED_POOL);
+}
+
+// emission pass through the certified fast path (POFA / POFL / PPFL): the
+// same mask enumeration as k_emit, per-item planes (ItemFast) in dynamic
+// shared memory instead of the coverage state, exact fallback per fragment
+#ifndef FHV_EMIT_FAST_MINB
+#define FHV_EMIT_FAST_MINB 3
+#endif
+template <int kMode, bool kAtomicAlloc>
+__global__ void __launch_bounds__(32 * kEmitFastWarps, FHV_EMIT_FAST_MINB)
+    k_emit_fast(CaptureParams p, const JobSetup* __restrict__ jobs, const uint32_t* __restrict__ item_job,
+                const uint32_t* __restrict__ item_p0, const unsigned long long* __restrict__ item_off,
+                const uint4* __restrict__ item_mask, long long n_items, const unsigned long long* n_dev, EmitOut o,
+                Control* ctl) {
+  static_assert(kMode == kPpfl || kMode == kPofl || kMode == kPofa, "record-emitting modes");
+  extern __shared__ __align__(16) unsigned char emit_dyn[];  // ItemFast[warps][32]
+  __shared__ uint32_t own_all[kEmitFastWarps][32];
+  __shared__ uint32_t ijob_all[kEmitFastWarps][32];
+  const unsigned lane = lane_id();
+  const int wib = threadIdx.x >> 5;
+  ItemFast* fast = reinterpret_cast<ItemFast*>(emit_dyn) + 32 * wib;
+  uint32_t* own_cnt = own_all[wib];
+  uint32_t* ijob = ijob_all[wib];
+  if (n_dev) {  // speculative launch: run the true count, or flag a plan that was too small
+    const long long nd = (long long)*n_dev;
+    if (nd > n_items && blockIdx.x == 0 && threadIdx.x == 0) raise_status(&ctl->status, FHV_RETRY_ITEMS);
+    if (nd < n_items) n_items = nd;
+  }
+  const long long n_groups = (n_items + 31) / 32;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  RasterState<kMode, kAtomicAlloc> st;
+  for (long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; g < n_groups; g += nw) {
+    const long long item = g * 32 + lane;
+    uint4 mk = make_uint4(0u, 0u, 0u, 0u);
+    unsigned long long rank0 = 0;
+    if (item < n_items) {
+      const uint32_t jid = item_job[item];
+      mk = item_mask[item];
+      if (!kAtomicAlloc && (kMode != kPofa || (o.flags & FHV_EXACT_ORDER))) rank0 = item_off[item];
+      const JobSetup js = jobs[jid];
+      const uint32_t p0 = item_p0[item];
+      ItemFast& F = fast[lane];
+      F.x0 = js.x0;
+      F.y0 = js.y0;
+      F.bw = js.bw;
+      F.p0 = p0;
+      F.inv_bw = 1.0f / (float)(js.bw > 0 ? js.bw : 1);
+      ijob[lane] = jid;
+      if (mk.x | mk.y | mk.z | mk.w) {  // planes of my item's positions and vertex normals
+        PlaneBasis b;
+        {
+          CoverS c;
+          make_cover(js, p0, c);
+          b = plane_basis(c);
+        }
+        bool ok = b.ok;
+        uint32_t zp = 0, zn = 0;
+        double ep = 0.0, en = 0.0;
+        const int o3[3] = {0, js.swapped ? 2 : 1, js.swapped ? 1 : 2};
+        {
+          double W[3][3];
+          const double* P = p.pos + 9 * (long long)js.tri;
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) W[i][q] = __ldg(&P[3 * o3[i] + q]);
+          attr_planes(b, W, F.A, F.B, F.C, ep, zp, ok);
+        }
+        {
+          double W[3][3];
+          const double* N = p.vnrm + 9 * (long long)js.tri;
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) W[i][q] = __ldg(&N[3 * o3[i] + q]);
+          attr_planes(b, W, F.A + 3, F.B + 3, F.C + 3, en, zn, ok);
+        }
+        F.ep = ep;
+        F.en = en;
+        F.zmask = zp | (zn << 3) | (ok ? 0u : kPlanesBad);
+        F.mat = __ldg(&p.mat[js.tri]);
+        F.obj = __ldg(&p.obj[js.tri]);
+      }
+    }
+    {  // the next group's item records
+      const long long nx = item + nw * 32;
+      if (nx < n_items) {
+        prefetch_l1(item_job + nx);
+        prefetch_l1(item_mask + nx);
+        prefetch_l1(item_p0 + nx);
+        if (!kAtomicAlloc && (kMode != kPofa || (o.flags & FHV_EXACT_ORDER))) prefetch_l1(item_off + nx);
+      }
+    }
+    own_cnt[lane] = 0;
+    const uint32_t cnt = (uint32_t)(__popc(mk.x) + __popc(mk.y) + __popc(mk.z) + __popc(mk.w));
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= (unsigned)d) inc += y;
+    }
+    const uint32_t E = inc - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    __syncwarp();
+    for (uint32_t s0 = 0; s0 < total; s0 += 32) {
+      const uint32_t f = s0 + lane;
+      const bool valid = f < total;
+      int k = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t Ec = __shfl_sync(0xffffffffu, E, k + step);
+        if (valid && Ec <= f) k += step;
+      }
+      const uint32_t local = f - __shfl_sync(0xffffffffu, E, k);
+      const uint32_t m0 = __shfl_sync(0xffffffffu, mk.x, k), m1 = __shfl_sync(0xffffffffu, mk.y, k);
+      const uint32_t m2 = __shfl_sync(0xffffffffu, mk.z, k), m3 = __shfl_sync(0xffffffffu, mk.w, k);
+      int px = 0, py = 0;
+      if (valid) {
+        uint32_t rem = local, wv = m0, word = 0;
+        const uint32_t c0 = (uint32_t)__popc(m0);
+        if (rem >= c0) {
+          rem -= c0;
+          wv = m1;
+          word = 1;
+          const uint32_t c1 = (uint32_t)__popc(m1);
+          if (rem >= c1) {
+            rem -= c1;
+            wv = m2;
+            word = 2;
+            const uint32_t c2 = (uint32_t)__popc(m2);
+            if (rem >= c2) {
+              rem -= c2;
+              wv = m3;
+              word = 3;
+            }
+          }
+        }
+        const ItemFast& F = fast[k];
+        const uint32_t q = F.p0 + 32u * word + nth_set_bit(wv, rem);
+        const uint32_t bw = (uint32_t)F.bw;
+        uint32_t r;
+        if (q < (1u << 22)) {  // |float estimate - q / bw| <= 2^-23 q < 1/2 here; fix it up exactly
+          r = (uint32_t)__fmul_rn((float)q, F.inv_bw);
+          const int rm = (int)(q - r * bw);
+          r = rm < 0 ? r - 1 : (rm >= (int)bw ? r + 1 : r);
+        } else {
+          r = q / bw;
+        }
+        px = F.x0 + (int)(q - r * bw);
+        py = F.y0 + (int)r;
+      }
+      raster_batch_fast<kMode, kAtomicAlloc>(p, o, ctl, jobs, fast, valid, k, px, py, local, own_cnt, rank0, ijob,
+                                             st);
     }
     __syncwarp();
   }
@@ -1677,6 +2207,40 @@ int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s, bool allow_spec =
 // device-side item count of a speculative plan (nullptr: ctx->n_items is exact)
 inline const unsigned long long* items_dev(fhv_ctx* ctx) { return ctx->spec ? &ctx->ctl->items_total : nullptr; }
 
+// dynamic shared memory of the fast raster kernels (opt-in above 48 KB total)
+constexpr int kRasterDyn = kRasterWarps * 32 * (int)sizeof(PosPlanes);
+constexpr int kEmitFastDyn = kEmitFastWarps * 32 * (int)sizeof(ItemFast);
+template <class K>
+void smem_opt_in(K kernel, int bytes) {
+  static const void* seen[16] = {};  // kernels already opted in (per process)
+  static int n_seen = 0;
+  const void* f = reinterpret_cast<const void*>(kernel);
+  for (int i = 0; i < n_seen; ++i)
+    if (seen[i] == f) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (n_seen < 16) seen[n_seen++] = f;
+}
+
+// Which per-fragment arithmetic the raster passes use.  The certified plane
+// path (k_emit_fast, k_raster<.., kFast>) builds per-item planes (~300
+// instructions per item) to cut the per-fragment work: it wins when items
+// carry many fragments (C4: PPFL emission 1.88 -> 1.41 ms) and loses on tiny
+// triangles (C3, ~4.6 fragments per item: 187 -> 208 us).  The choice follows
+// the fragments-per-item of the last synchronised capture on this context
+// (speculation like the pool-size guess; graph captures replay the choice made
+// at capture time).  FHV_FAST_MATH=0/1 forces it; FHV_FAST_MIN_FPI sets the
+// threshold (default 16 fragments per item).
+inline int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+inline bool use_fast_math(const fhv_ctx* ctx) {
+  static const int force = env_int("FHV_FAST_MATH", -1);
+  static const int min_fpi = env_int("FHV_FAST_MIN_FPI", 16);
+  if (force >= 0) return force != 0;
+  return ctx->frags_per_item >= (double)min_fpi;
+}
+
 // counts per item (+ leaf histogram) and their scan (fragment ranks); async
 int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_t* leaf_counts, cudaStream_t s,
           bool ranks = true) {
@@ -1695,10 +2259,16 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
     o.levels = levels;
     o.leaf_counts = leaf_counts;
     const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
+    const bool fast = leaves && use_fast_math(ctx);
+    if (fast) smem_opt_in(k_raster<kCntLeaves, false, true>, kRasterDyn);
     {
       LaunchScope L_(ctx, leaves ? kStCountLeaves : kStCount, s);
-      if (leaves)
-        k_raster<kCntLeaves, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, nd, item_cnt, item_mask,
+      if (fast)
+        k_raster<kCntLeaves, false, true><<<grid, kRasterBlock, kRasterDyn, s>>>(p, jobs, ij, ip, nullptr, n, nd,
+                                                                                  item_cnt, item_mask, o, ctx->ctl);
+      else if (leaves)
+        k_raster<kCntLeaves, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, nd, item_cnt,
+                                                                   item_mask,
                                                                    o, ctx->ctl);
       else
         k_raster<kCnt, false><<<grid, kRasterBlock, 0, s>>>(p, jobs, ij, ip, nullptr, n, nd, item_cnt, item_mask, o,
@@ -1723,6 +2293,21 @@ int emit(fhv_ctx* ctx, const CaptureParams& p, const EmitOut& o, bool atomic_all
   const auto* io = (const unsigned long long*)ctx->bufs[kItemOff].ptr;
   const auto* im = (const uint4*)ctx->bufs[kItemMask].ptr;
   const unsigned long long* nd = items_dev(ctx);
+  if constexpr (kMode == kPpfl || kMode == kPofl || kMode == kPofa) {
+    if (!(o.flags & kExactMath) && use_fast_math(ctx)) {
+      const int gridf = grid_for((n + 31) / 32 * 32, 32 * kEmitFastWarps);
+      smem_opt_in(k_emit_fast<kMode, true>, kEmitFastDyn);
+      smem_opt_in(k_emit_fast<kMode, false>, kEmitFastDyn);
+      LaunchScope L_(ctx, kStEmitList + (kMode - kList), s);
+      if (atomic_alloc)
+        k_emit_fast<kMode, true><<<gridf, 32 * kEmitFastWarps, kEmitFastDyn, s>>>(p, jobs, ij, ip, io, im, n, nd, o,
+                                                                                ctx->ctl);
+      else
+        k_emit_fast<kMode, false><<<gridf, 32 * kEmitFastWarps, kEmitFastDyn, s>>>(p, jobs, ij, ip, io, im, n, nd, o,
+                                                                                 ctx->ctl);
+      return check_cuda(ctx, cudaGetLastError());
+    }
+  }
   const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
   {
     LaunchScope L_(ctx, kMode >= kDsDepth ? kStDeferred : kStEmitList + (kMode - kList), s);
@@ -1893,6 +2478,7 @@ static int build_linked(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_
     if (rc != FHV_RETRY_ITEMS) break;
   }
   const long long total = (long long)(atomic_alloc ? ctx->ctl_host->alloc : ctx->ctl_host->scan_total);
+  if (ctx->ctl_host->items_total > 0) ctx->frags_per_item = (double)total / (double)ctx->ctl_host->items_total;
   if (next_free) *next_free = total;
   if (rc == FHV_OK && total > pool->capacity) rc = FHV_OVERFLOW;
   return rc;
@@ -1994,6 +2580,7 @@ int pofa_count_done(fhv_ctx* ctx, const fhv_tris_t* tris, int32_t levels, const 
   const long long frags = (long long)ctx->ctl_host->frags_total;
   if (frags >= (1LL << 32)) return FHV_TOO_MANY;
   ctx->pass1_total = frags;
+  if (ctx->ctl_host->items_total > 0) ctx->frags_per_item = (double)frags / (double)ctx->ctl_host->items_total;
   ctx->pass1_levels = levels;
   ctx->pass1_tris = tris->n_tri;
   ctx->pass1_lo = p.cell_lo;
@@ -2078,7 +2665,8 @@ static int pofa_scatter_async(fhv_ctx* ctx, const CaptureParams& p, int32_t leve
     auto* recs = (uint32_t*)scratch(ctx, kLeafRecs, (size_t)cap * 36);
     auto* nn = (unsigned long long*)scratch(ctx, kTmp1, 8);
     if (!big || !keys || !recs || !nn) return FHV_NOMEM;
-    if ((rc = check_cuda(ctx, cudaMemsetAsync(ctx->ctl->leaf_n, 0, sizeof(ctx->ctl->leaf_n), s)))) return rc;
+    if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->leaf_n[0], 0, 8, s)))) return rc;
+    if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->leaf_n[2], 0, 8, s)))) return rc;
     if (!n_frags_dev) {
       const unsigned long long nh = (unsigned long long)n_frags_host;
       if ((rc = check_cuda(ctx, cudaMemcpyAsync(nn, &nh, 8, cudaMemcpyHostToDevice, s)))) return rc;

@@ -74,6 +74,9 @@ struct fhv_ctx {
   // the last exact plan with the same job count; spec = current plan is one
   int64_t item_cap = 0, last_n_jobs = -1;
   bool spec = false;
+  // fragments per work item of the last synchronised capture (selects the
+  // raster passes' arithmetic path, fhv_capture.cu use_fast_math)
+  double frags_per_item = 0.0;
   int last_cuda_error = 0;
 };
 

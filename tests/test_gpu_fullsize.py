@@ -62,8 +62,9 @@ def test_c3_full_size_pofa_and_splat_bit_exact():
     h = gpu.pool.numpy()
     for k in ("position", "normal", "material_id", "object_id", "prev_index"):
         assert np.array_equal(h[k], ref["pool"][k]), k
-    fixed, _, long_ = _lib.counters(torch.device("cuda", 0))  # leaves the slot-order fix-up re-sorted
-    print(f"exact-order fix-up: {fixed} leaves re-sorted by the tile pass, {long_} long leaves listed")
+    fixed, slow, long_ = _lib.counters(torch.device("cuda", 0))  # leaves the slot-order fix-up re-sorted
+    print(f"exact-order fix-up: {fixed} leaves re-sorted by the tile pass, {long_} long leaves listed; "
+          f"{slow} fragments (both passes) through the exact arithmetic path")
     # the bench's step: asynchronous build (pool sized by the last total, outcome
     # in a ticket), EXACT_ORDER -- byte-identical records
     av = fhv.pofa_build(s, ns, cfg, 8, exact_order=True, sync=False).wait()
