@@ -691,6 +691,7 @@ def main():
         "splat_index": 12 * n_frags + 8 * P,
         "splat_resolve": 8 * P + 4 * P + 40 * P,
         "job_setup": (72 + 24 + 80 + 4) * T,
+        "leaf_order": 4 * n_frags,  # the ranks read; moved records are the fix-up's own traffic
     }
     peak, peak_kind = peaks()
     roof = None
@@ -717,6 +718,29 @@ def main():
                              "frac": round(winst / cap, 4),
                              "note": "executed warp instructions from the ncu capture in profiles/ncu_<stage>.json "
                                      "over this run's launch time x SMs x 4 schedulers x SM clock"}
+    # atomic / reduction throughput of the atomic-bound stages (north star:
+    # "achieved HBM GB/s ... and atomic throughput"): L2 atomic requests per
+    # launch from the committed ncu capture (profiles/ncu_<stage>.json) over
+    # this run's per-launch time, and the L1 RED / ATOM pipe utilisation ncu saw
+    atomics = None
+    if world == 1:
+        atomics = {}
+        for st_name, kind in (("count_leaves", "red"), ("emit_pofa", "atom"), ("splat_depth", "red"),
+                              ("splat_index", "red")):
+            tf = os.path.join(ROOT, "profiles", f"ncu_{st_name}.json")
+            if st_name not in prof or not os.path.exists(tf):
+                continue
+            try:
+                a = json.load(open(tf)).get("atomics") or {}
+            except Exception:
+                continue
+            req = a.get(f"{kind}_requests_l2")
+            if not req:
+                continue
+            per_launch = prof[st_name][0] / prof[st_name][1] / 1e3
+            atomics[st_name] = {"op": "RED" if kind == "red" else "ATOM", "l2_requests_per_launch": int(req),
+                                "l2_requests_per_s": req / per_launch,
+                                "l1_pipe_pct_ncu": a.get(f"{kind}_l1_pipe_pct")}
     capture_ms = sum(v for k, v in stage_ms.items() if not k.startswith("splat"))
     recon_ms = sum(v for k, v in stage_ms.items() if k.startswith("splat"))
     step_bytes = (2 * 176 * T + 36 * n_frags + 12 * 8 ** L + (8 ** L - 1) // 7  # POFA capture
@@ -869,7 +893,7 @@ def main():
                 "gap_ms_per_step": round(ms_profiled / args.steps - sum(stage_ms.values()), 4),
                 "ms_per_step_profiled": round(ms_profiled / args.steps, 4),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
-                "parity": parity, "other_order": other,
+                "parity": parity, "other_order": other, "atomics": atomics,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

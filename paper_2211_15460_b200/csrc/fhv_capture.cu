@@ -1706,7 +1706,7 @@ __global__ void k_leaf_order(const uint32_t* __restrict__ offsets, const uint32_
 // The in-leaf order only breaks where a leaf took fragments from more than
 // one warp: a warp enumerates its fragments in emission order and a
 // same-leaf group takes consecutive cursor slots in lane order.
-//   k_leaf_fix   a warp per tile of 128 slots (+96 look-ahead): segment
+//   k_leaf_fix   a warp per tile of 128 slots (+64 look-ahead): segment
 //                starts by ballots, a segment with a rank below its
 //                predecessor's is re-sorted by rank-by-count through per-warp
 //                shared memory, coalesced loads and stores.  Segments starting
@@ -1749,21 +1749,22 @@ __device__ __forceinline__ void unstage_record(const PoolRefs& pl, const uint32_
   pl.mat[t] = R[6]; pl.obj[t] = R[7]; pl.rank[t] = (R[8] & ~kSegBit) | slot_bit;
 }
 
-// k_leaf_fix: a WARP per tile of 128 slots (+ 96 look-ahead = 7 chunks of
+// k_leaf_fix: a WARP per tile of 128 slots (+ 64 look-ahead = 6 chunks of
 // 32), no block barriers.  Ranks in registers (coalesced), segment starts by
 // ballots, segment bounds by bit scans, disorder by a shuffle of the previous
 // rank; the elements of a disordered segment are ranked by counting over the
 // segment's ranks (per-warp shared memory) and staged at their destination in
 // per-warp shared memory, then stored back (coalesced).
-constexpr int kFixChunks = 7;
+constexpr int kFixChunks = 6;
 constexpr int kFixWarpTile = 128;                     // segments starting here are this warp's
-constexpr int kFixWarpRegion = 32 * kFixChunks;       // 224
+constexpr int kFixWarpRegion = 32 * kFixChunks;       // 192
 constexpr int kFixWarps = 4;                          // warps per CTA
 
 struct FixWarpSmem {
   uint32_t rk[kFixWarpRegion];
   uint8_t dis[kFixWarpRegion];
   uint8_t dst_set[kFixWarpRegion];
+  uint8_t mv_i[kFixWarpRegion], mv_lo[kFixWarpRegion], mv_hi[kFixWarpRegion];
   float pos[kFixWarpRegion][3], nrm[kFixWarpRegion][3];
   uint32_t mat[kFixWarpRegion], obj[kFixWarpRegion], rank[kFixWarpRegion];
 };
@@ -1842,15 +1843,30 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_leaf_fix(PoolRefs pl, const 
       if (i > st[k] && (r[k] & ~kSegBit) < (prev & ~kSegBit)) S.dis[st[k]] = 1;
     }
     __syncwarp();
-    // disordered segments: rank by counting, stage at the destination
+    // the elements of disordered segments, compacted (so the rank counting
+    // below runs ~#moving / 32 rounds, not one per chunk), then ranked by
+    // counting over their segment and staged at the destination
+    int nmv = 0;
 #pragma unroll
     for (int k = 0; k < kFixChunks; ++k) {
       const int i = 32 * k + (int)lane;
       const bool mv = own[k] && S.dis[st[k]];
-      if (!mv) continue;
-      if (i == st[k]) ++fixed;
-      const int lo = st[k], hi = min(en[k], len);
-      const uint32_t rr = r[k] & ~kSegBit;
+      const unsigned bal = __ballot_sync(0xffffffffu, mv);
+      if (mv) {
+        const int q = nmv + __popc(bal & below);
+        S.mv_i[q] = (uint8_t)i;
+        S.mv_lo[q] = (uint8_t)st[k];
+        S.mv_hi[q] = (uint8_t)min(en[k], len);
+        if (i == st[k]) ++fixed;
+      }
+      nmv += __popc(bal);
+    }
+    __syncwarp();
+    for (int b0 = 0; b0 < nmv; b0 += 32) {
+      const int q = b0 + (int)lane;
+      if (q >= nmv) continue;
+      const int i = S.mv_i[q], lo = S.mv_lo[q], hi = S.mv_hi[q];
+      const uint32_t rr = S.rk[i];
       int d = lo;
       for (int j = lo; j < hi; ++j) d += S.rk[j] < rr ? 1 : 0;
       const long long s_ = t0 + i;
