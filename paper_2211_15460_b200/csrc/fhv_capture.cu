@@ -90,6 +90,7 @@ struct EmitOut {
   int levels;
   // POFA (indexed by code - cell_lo)
   uint32_t* leaf_counts;
+  uint32_t* tile_sums;  // counting pass: per directory tile (kDirSumShift) totals, or null
   const uint32_t* offsets;
   const uint32_t* counts;
   uint32_t* cursors;
@@ -647,6 +648,11 @@ __device__ __forceinline__ void raster_batch(const CaptureParams& p, const EmitO
   if (kMode == kCntLeaves) {
     const unsigned grp = __match_any_sync(0xffffffffu, code);
     if (live && (int)lane == __ffs(grp) - 1) atomicAdd(&o.leaf_counts[code - p.cell_lo], (uint32_t)__popc(grp));
+    if (o.tile_sums) {  // directory tile totals: the directory pass then needs no look-back chain
+      const uint32_t tkey = live ? (uint32_t)((code - p.cell_lo) >> kDirSumShift) : 0xffffffffu;
+      const unsigned gt = __match_any_sync(0xffffffffu, tkey);
+      if (live && (int)lane == __ffs(gt) - 1) atomicAdd(&o.tile_sums[tkey], (uint32_t)__popc(gt));
+    }
     return;
   }
   // POFA: the leaf's cursor atomic (and its range loads) go out BEFORE the
@@ -1019,6 +1025,11 @@ __device__ __forceinline__ void raster_batch_fast(const CaptureParams& p, const 
   if (kMode == kCntLeaves) {
     const unsigned grp = __match_any_sync(0xffffffffu, code);
     if (live && (int)lane == __ffs(grp) - 1) atomicAdd(&o.leaf_counts[code - p.cell_lo], (uint32_t)__popc(grp));
+    if (o.tile_sums) {  // directory tile totals: the directory pass then needs no look-back chain
+      const uint32_t tkey = live ? (uint32_t)((code - p.cell_lo) >> kDirSumShift) : 0xffffffffu;
+      const unsigned gt = __match_any_sync(0xffffffffu, tkey);
+      if (live && (int)lane == __ffs(gt) - 1) atomicAdd(&o.tile_sums[tkey], (uint32_t)__popc(gt));
+    }
     return;
   }
   long long slot = -1;
@@ -2259,7 +2270,7 @@ inline bool use_fast_math(const fhv_ctx* ctx) {
 
 // counts per item (+ leaf histogram) and their scan (fragment ranks); async
 int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_t* leaf_counts, cudaStream_t s,
-          bool ranks = true) {
+          bool ranks = true, uint32_t* tile_sums = nullptr) {
   const long long n = ctx->n_items;
   uint32_t* item_cnt = (uint32_t*)scratch(ctx, kItemCnt, (size_t)(n > 0 ? n : 1) * 4);
   auto* item_off = (unsigned long long*)scratch(ctx, kItemOff, (size_t)(n > 0 ? n : 1) * 8);
@@ -2274,6 +2285,7 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
     std::memset(&o, 0, sizeof(o));
     o.levels = levels;
     o.leaf_counts = leaf_counts;
+    o.tile_sums = tile_sums;
     const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
     const bool fast = leaves && use_fast_math(ctx);
     if (fast) smem_opt_in(k_raster<kCntLeaves, false, true>, kRasterDyn);
@@ -2586,7 +2598,18 @@ int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg
   const unsigned long long n_local = p.cell_hi - p.cell_lo;
   if ((rc = plan(ctx, p, s, spec))) return rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(counts_local, 0, (size_t)n_local * 4, s)))) return rc;
-  if ((rc = count(ctx, p, true, levels, counts_local, s, ranks))) return rc;
+  // whole-directory builds also total the fragments per directory tile, so
+  // the directory pass (scan_leaves_and_pyramid) needs no look-back chain
+  uint32_t* tile_sums = nullptr;
+  ctx->dir_sums_levels = -1;
+  if (p.cell_lo == 0 && n_local == (1ull << (3 * levels)) && levels >= 5) {
+    const size_t nt = (size_t)(n_local >> kDirSumShift);
+    tile_sums = (uint32_t*)scratch(ctx, kTileSums, nt * 4);
+    if (!tile_sums) return FHV_NOMEM;
+    if ((rc = check_cuda(ctx, cudaMemsetAsync(tile_sums, 0, nt * 4, s)))) return rc;
+    ctx->dir_sums_levels = levels;
+  }
+  if ((rc = count(ctx, p, true, levels, counts_local, s, ranks, tile_sums))) return rc;
   if (!ranks) return FHV_OK;  // the total comes from the directory scan (caller)
   return check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total, sizeof(unsigned long long),
                                          cudaMemcpyDeviceToDevice, s));
@@ -2969,6 +2992,7 @@ extern "C" int fhv_rebuild_pofa(fhv_ctx* ctx, int32_t levels, const fhv_pool_t* 
     k_pool_leaf_hist<<<grid_for(n, 256), 256, 0, s>>>(src->pos, n, levels, counts, &ctx->ctl->status);
   }
   if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  ctx->dir_sums_levels = -1;  // no counting-pass tile totals for a repack
   if ((rc = scan_leaves_and_pyramid(ctx, counts, offsets, pyramid, levels, s))) return rc;
   if (n > 0) {
     {

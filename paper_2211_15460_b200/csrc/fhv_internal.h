@@ -13,6 +13,9 @@
 
 namespace fhv {
 
+// directory tiles of the POFA offsets pass: 2^14 leaves (fhv_scan.cu k_dir_tma)
+constexpr int kDirSumShift = 14;
+
 // internal status: a speculatively planned capture's item buffers were too
 // small (never returned to callers: the capture re-plans with a sync)
 constexpr int FHV_RETRY_ITEMS = 100;
@@ -30,6 +33,7 @@ struct Control {
   unsigned int pad2;
   unsigned long long spare[8];
   unsigned long long leaf_n[3];  // EXACT_ORDER POFA: leaves listed for re-sorting (small, mid, big)
+  unsigned int dir_ticket, dir_done;  // k_dir_stream: tile tickets, CTAs finished (zeroed before each launch)
 };
 
 struct DevBuf {
@@ -77,6 +81,9 @@ struct fhv_ctx {
   // fragments per work item of the last synchronised capture (selects the
   // raster passes' arithmetic path, fhv_capture.cu use_fast_math)
   double frags_per_item = 0.0;
+  // levels of the directory tile totals the last counting pass left in
+  // bufs[kTileSums] (-1: none; consumed by scan_leaves_and_pyramid)
+  int dir_sums_levels = -1;
   int last_cuda_error = 0;
 };
 
@@ -85,7 +92,7 @@ namespace fhv {
 enum BufId {
   kJobs = 0, kJobItems, kJobItemOff, kItemJob, kItemP0, kItemCnt, kItemOff, kScanStatus,
   kCursors, kChainScratch, kSplatKey, kSplatWin, kSplatBox, kRays, kTmp0, kTmp1, kTriFlag, kTriOff, kTriIndex,
-  kShardBoxes, kItemMask, kJobPersp, kLeafList, kLeafKeys, kLeafRecs, kNumBufs
+  kShardBoxes, kItemMask, kJobPersp, kLeafList, kLeafKeys, kLeafRecs, kTileSums, kNumBufs
 };
 
 // Counts a launch and, when profiling is on, brackets it with CUDA events on

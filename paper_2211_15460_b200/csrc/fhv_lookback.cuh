@@ -95,5 +95,53 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, unsigned til
   return prefix;
 }
 
+// decoupled look-back with the whole block: every thread inspects one
+// predecessor, so one step covers BLOCK tiles (a tile of the first wave walks
+// back to tile 0 in n / BLOCK round trips instead of n / 32).  Called by all
+// threads; returns the exclusive prefix in every thread.
+template <int BLOCK>
+__device__ __forceinline__ uint64_t lookback_block(uint64_t* status, unsigned tile, uint64_t agg) {
+  __shared__ uint64_t red_s[BLOCK / 32];
+  __shared__ int near_s[BLOCK / 32];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  if (tile == 0) {
+    if (threadIdx.x == 0) st_volatile(&status[0], kFlagPre | agg);
+    return 0;
+  }
+  if (threadIdx.x == 0) st_volatile(&status[tile], kFlagAgg | agg);
+  uint64_t prefix = 0;
+  long long top = (long long)tile - 1;  // the highest predecessor of this step
+  while (true) {
+    const long long k = top - (long long)threadIdx.x;
+    uint64_t s = kFlagPre;  // before tile 0: an inclusive prefix of 0
+    if (k >= 0) {
+      do { s = ld_volatile(&status[k]); } while ((s & ~kValMask) == 0);
+    }
+    // the nearest inclusive prefix among this step's predecessors (lowest thread index)
+    const bool pre = (s & ~kValMask) == kFlagPre;
+    const unsigned bal = __ballot_sync(0xffffffffu, pre);
+    if (lane == 0) near_s[warp] = bal ? (int)(32 * warp + __ffs(bal) - 1) : BLOCK;
+    __syncthreads();
+    int near = BLOCK;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) near = min(near, near_s[w]);
+    // sum of the values from the step's top down to (and including) the nearest inclusive
+    uint64_t v = (int)threadIdx.x <= near ? (s & kValMask) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red_s[warp] = v;
+    __syncthreads();
+    uint64_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) tot += red_s[w];
+    prefix += tot;
+    __syncthreads();  // red_s / near_s reused by the next step
+    if (near < BLOCK) break;
+    top -= BLOCK;
+  }
+  if (threadIdx.x == 0) st_volatile(&status[tile], kFlagPre | ((prefix + agg) & kValMask));
+  return prefix;
+}
+
 }  // namespace
 }  // namespace fhv

@@ -10,6 +10,11 @@
 //    bottom mask level in the same sweep: 8 B/leaf + 1/8 B/leaf of HBM.
 //  * pyramid_from_heads: POFL occupancy (equal to incremental set_paths,
 //    fhv/storage.py:294-301, SURVEY probe) from heads >= 0.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
 #include "fhv_common.cuh"
 #include "fhv_internal.h"
 #include "fhv_lookback.cuh"
@@ -307,6 +312,218 @@ __global__ void __launch_bounds__(32 * WARPS, WARPS <= 16 ? 2 : 1) k_dir_tiles(c
   }
 }
 
+// ---------------------------------------------------------------------------
+// POFA directory through TMA tensor copies (L >= 5).  The counts are viewed
+// as a 2-D tensor of 128-B rows (32 leaves); one CTA owns a tile of kDbChunks
+// x 256 rows (kDbChunks x 32 KB, whole level-(L-4) subtrees).  Thread 0 puts
+// the whole tile in flight at once -- one cp.async.bulk.tensor per 32-KB
+// chunk, each completing on its own mbarrier, 128-B swizzled so that thread
+// t's row (its 32 consecutive leaves) reads conflict-free -- and every thread
+// processes chunk j as soon as it lands: pyramid levels L-1..L-4 (L-5 too
+// for 4 chunks) from registers / shuffles / ballots, per-chunk block scans;
+// the decoupled tile look-back, then the offsets are written in place into
+// the same swizzled buffers and stored back with cp.async.bulk.tensor
+// (shared -> global).  Counts are read from HBM exactly once, 8 B per leaf of
+// traffic in 32-KB TMA transfers; the last CTA builds the levels above.
+constexpr int kDbThreads = 256;
+constexpr int kDbRows = 256;                         // 128-B rows per chunk (one per thread)
+constexpr int kDbLeaves = kDbRows * 32;              // 8192 leaves per chunk
+constexpr int kDbBytes = kDbLeaves * 4;              // 32 KB
+#ifndef FHV_DIR_CHUNKS
+#define FHV_DIR_CHUNKS 2
+#endif
+constexpr int kDbChunks = FHV_DIR_CHUNKS;            // chunks per CTA tile (1, 2 or 4)
+constexpr long long kDbTile = (long long)kDbChunks * kDbLeaves;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LAB_WAIT;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(smem)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int c0, int c1, const void* smem) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tm), "r"(c0),
+               "r"(c1), "r"(smem_u32(smem))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 16-B unit q of row t inside a 128-B-swizzled chunk (CU_TENSOR_MAP_SWIZZLE_128B)
+__device__ __forceinline__ uint4* swz(uint32_t* chunk, unsigned t, unsigned q) {
+  return reinterpret_cast<uint4*>(reinterpret_cast<char*>(chunk) + t * 128u + ((q ^ (t & 7u)) << 4));
+}
+
+static_assert(kDbTile == (1ll << kDirSumShift) || kDbChunks != 2, "tile totals match the tile");
+
+#ifndef FHV_DIR_MINB
+#define FHV_DIR_MINB 3
+#endif
+__global__ void __launch_bounds__(kDbThreads, FHV_DIR_MINB) k_dir_tma(const __grid_constant__ CUtensorMap tm_counts,
+                                                         const __grid_constant__ CUtensorMap tm_offsets,
+                                                         uint8_t* __restrict__ pyr, int levels, uint64_t* status,
+                                                         Control* ctl, unsigned n_tiles, unsigned tile0,
+                                                         uint64_t base, const uint32_t* __restrict__ tile_sums) {
+  extern __shared__ __align__(1024) unsigned char dyn[];  // kDbChunks x 32 KB, 1024-B aligned (swizzle atoms)
+  uint32_t* buf = reinterpret_cast<uint32_t*>(dyn + ((1024u - (smem_u32(dyn) & 1023u)) & 1023u));
+  __shared__ __align__(8) uint64_t bar[kDbChunks];
+  __shared__ unsigned tile_s;
+  __shared__ uint64_t prefix_s, ctot_s[kDbChunks];
+  __shared__ uint8_t l3_s[kDbChunks][kDbThreads / 16];
+  __shared__ int last_s;
+  const unsigned tid = threadIdx.x, lane = tid & 31u;
+  if (tid == 0) {
+    // with the counting pass's tile totals the tiles are independent (blockIdx);
+    // else ticket order: the look-back never waits on an unstarted tile
+    const unsigned t = tile_sums ? blockIdx.x : draw_tile(ctl, n_tiles);
+    tile_s = t;
+    for (int j = 0; j < kDbChunks; ++j) mbar_init(&bar[j], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int j = 0; j < kDbChunks; ++j) {  // the whole tile in flight at once, one barrier per 32-KB chunk
+      mbar_expect_tx(&bar[j], kDbBytes);
+      tma_load_2d(buf + j * kDbLeaves, &tm_counts, 0, (int)((long long)t * kDbChunks * kDbRows + j * kDbRows), &bar[j]);
+    }
+  }
+  __syncthreads();
+  const unsigned tile = tile_s;
+  const unsigned gtile = tile0 + tile;
+  uint64_t excl[kDbChunks];
+#pragma unroll
+  for (int j = 0; j < kDbChunks; ++j) {  // chunk j: leaves [j * 8192, (j + 1) * 8192) of the tile; my row = tid
+    mbar_wait(&bar[j], 0);
+    uint32_t* cb = buf + j * kDbLeaves;
+    uint32_t sum = 0;
+    uint32_t m1 = 0;  // my 4 level-(L-1) node masks
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 v = *swz(cb, tid, q);
+      sum += v.x + v.y + v.z + v.w;
+      m1 |= ((v.x != 0u ? 1u : 0u) | (v.y != 0u ? 2u : 0u) | (v.z != 0u ? 4u : 0u) | (v.w != 0u ? 8u : 0u)) << (4 * q);
+    }
+    const long long node1 = ((long long)gtile * kDbChunks + j) * (kDbLeaves / 8) + 4 * tid;
+    {  // (level offsets (8^k - 1) / 7 are not 4-B aligned: byte stores)
+      uint8_t* l1 = pyr + pyr_level_offset(levels - 1) + node1;
+#pragma unroll
+      for (int nd = 0; nd < 4; ++nd) l1[nd] = (uint8_t)(m1 >> (8 * nd));
+    }
+    // level L-2: node = 8 level-(L-1) nodes = 2 threads
+    const unsigned my4 = ((m1 & 0xffu) != 0 ? 1u : 0u) | ((m1 & 0xff00u) != 0 ? 2u : 0u) |
+                         ((m1 & 0xff0000u) != 0 ? 4u : 0u) | ((m1 & 0xff000000u) != 0 ? 8u : 0u);
+    const unsigned pair = my4 | (__shfl_down_sync(0xffffffffu, my4, 1) << 4);
+    if ((lane & 1u) == 0) pyr[pyr_level_offset(levels - 2) + node1 / 8] = (uint8_t)pair;
+    // level L-3: node = 8 level-(L-2) nodes = 16 threads
+    const unsigned occ = __ballot_sync(0xffffffffu, (lane & 1u) == 0 && pair != 0u);
+    if ((lane & 15u) == 0) {
+      const unsigned h = (occ >> lane) & 0xffffu;
+      unsigned m3 = 0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) m3 |= ((h >> (2 * g)) & 1u) << g;
+      pyr[pyr_level_offset(levels - 3) + node1 / 64] = (uint8_t)m3;
+      l3_s[j][tid / 16] = (uint8_t)m3;
+    }
+    excl[j] = block_excl_scan<kDbThreads>((uint64_t)sum, &ctot_s[j]);
+  }
+  uint64_t t_all = 0;
+#pragma unroll
+  for (int j = 0; j < kDbChunks; ++j) t_all += ctot_s[j];
+  uint64_t pf;
+  if (tile_sums) {  // prefix = the predecessors' totals (a block sum), no chain
+    uint64_t v = 0;
+    for (unsigned q = tid; q < tile; q += kDbThreads) v += tile_sums[q];
+    __shared__ uint64_t tsum_s;
+    uint64_t dummy = block_excl_scan<kDbThreads>(v, &tsum_s);
+    (void)dummy;
+    pf = tsum_s;
+    if (tid == 0 && tile_sums[tile] != (uint32_t)t_all) raise_status(&ctl->status, FHV_PASS_MISMATCH);
+  } else {
+    pf = lookback_block<kDbThreads>(status, tile, t_all);  // the whole block looks back
+  }
+  if (tid < 32) {
+    if (lane == 0) {
+      prefix_s = pf;
+      if (tile == n_tiles - 1) ctl->scan_total = pf + t_all;
+    }
+    if (lane < 2 * kDbChunks) {  // level L-4: two subtree roots per chunk
+      unsigned m4 = 0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) m4 |= (l3_s[lane / 2][8 * (lane & 1) + g] != 0 ? 1u : 0u) << g;
+      pyr[pyr_level_offset(levels - 4) + (long long)gtile * 2 * kDbChunks + lane] = (uint8_t)m4;
+      const unsigned m4all = __ballot_sync((1u << (2 * kDbChunks)) - 1u, m4 != 0u);
+      if (lane == 0 && kDbChunks == 4) pyr[pyr_level_offset(levels - 5) + gtile] = (uint8_t)m4all;  // tile root
+    }
+  }
+  __syncthreads();
+  uint64_t cbase = base + prefix_s;
+#pragma unroll
+  for (int j = 0; j < kDbChunks; ++j) {
+    uint64_t run = cbase + excl[j];
+    cbase += ctot_s[j];
+    uint32_t* cb = buf + j * kDbLeaves;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint4* p4 = swz(cb, tid, q);
+      const uint4 v = *p4;
+      uint4 o;
+      o.x = (uint32_t)run; run += v.x;
+      o.y = (uint32_t)run; run += v.y;
+      o.z = (uint32_t)run; run += v.z;
+      o.w = (uint32_t)run; run += v.w;
+      *p4 = o;
+    }
+  }
+  fence_proxy_async();  // my generic-proxy writes -> visible to the tensor copies
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j < kDbChunks; ++j)
+      tma_store_2d(&tm_offsets, 0, (int)((long long)tile * kDbChunks * kDbRows + j * kDbRows), buf + j * kDbLeaves);
+    bulk_commit();
+    bulk_wait_read<0>();  // the copy engine has read the buffers: shared memory may be released
+    __threadfence();
+    const unsigned done = atomicAdd(&ctl->dir_done, 1u);
+    last_s = done == n_tiles - 1;
+  }
+  __syncthreads();
+  if (!last_s) return;
+  __threadfence();
+  for (int k = levels - (kDbChunks == 4 ? 6 : 5); k >= 0; --k) {  // levels above what the tiles wrote
+    const long long nn = 1ll << (3 * k);
+    const uint8_t* below = pyr + pyr_level_offset(k + 1);
+    uint8_t* out = pyr + pyr_level_offset(k);
+    for (long long jj = tid; jj < nn; jj += blockDim.x) {
+      unsigned m = 0;
+#pragma unroll
+      for (int b2 = 0; b2 < 8; ++b2) m |= (__ldcg(&below[8 * jj + b2]) != 0 ? 1u : 0u) << b2;
+      out[jj] = (uint8_t)m;
+    }
+    __syncthreads();
+  }
+}
+
 // one pyramid level from the level below: node k at level l has children
 // 8k..8k+7 at level l+1 (one 8-byte load)
 __global__ void k_pyramid_up(const uint64_t* __restrict__ below, uint8_t* __restrict__ level, int64_t n) {
@@ -428,8 +645,76 @@ static int launch_dir_tiles(fhv_ctx* ctx, bool scan, const uint32_t* counts, uin
   return check_cuda(ctx, cudaGetLastError());
 }
 
+// the TMA tensor-copy directory (k_dir_tma); FHV_DIR_STREAM=0 selects k_dir_tiles (A/B)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// 2-D view of a u32 leaf array: rows of 32 leaves (128 B), boxes of 256 rows, 128-B swizzle
+static bool rows_tensor_map(CUtensorMap* tm, const uint32_t* base, uint64_t n_leaves) {
+  auto enc = tensor_map_encoder();
+  if (!enc || n_leaves % 32) return false;
+  const cuuint64_t dims[2] = {32, (cuuint64_t)(n_leaves / 32)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {32, (cuuint32_t)kDbRows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int launch_dir_bulk(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid, int levels,
+                           cudaStream_t s, uint64_t lo, uint64_t hi, uint64_t base,
+                           const uint32_t* tile_sums = nullptr) {
+  const unsigned tiles = (unsigned)((hi - lo) / (uint64_t)kDbTile);
+  const unsigned tile0 = (unsigned)(lo / (uint64_t)kDbTile);
+  CUtensorMap tm_c, tm_o;
+  if (!rows_tensor_map(&tm_c, counts + lo, hi - lo) || !rows_tensor_map(&tm_o, offsets + lo, hi - lo))
+    return launch_dir_tiles(ctx, true, counts, offsets, nullptr, pyramid, levels, s, lo, hi, base);
+  uint64_t* st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)tiles * sizeof(uint64_t));
+  if (!st) return FHV_NOMEM;
+  int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)tiles * sizeof(uint64_t), s));
+  if (rc) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->dir_ticket, 0, 8, s)))) return rc;  // (done counter)
+  constexpr int kSmem = kDbChunks * kDbBytes + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dir_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  {
+    LaunchScope L_(ctx, kStScanLeaves, s);
+    k_dir_tma<<<tiles, kDbThreads, kSmem, s>>>(tm_c, tm_o, pyramid, levels, st, ctx->ctl, tiles, tile0, base,
+                                                 tile_sums);
+  }
+  return check_cuda(ctx, cudaGetLastError());
+}
+
+static bool dir_stream_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("FHV_DIR_STREAM");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
                             int levels, cudaStream_t s) {
+  if (levels >= 5 && dir_stream_enabled()) {
+    // the counting pass's per-tile totals, when it left them for this directory (one use)
+    const uint32_t* sums = (ctx->dir_sums_levels == levels && kDbChunks == 2) ? (const uint32_t*)ctx->bufs[kTileSums].ptr
+                                                                             : nullptr;
+    ctx->dir_sums_levels = -1;
+    return launch_dir_bulk(ctx, counts, offsets, pyramid, levels, s, 0, 1ull << (3 * levels), 0, sums);
+  }
   if (levels >= 4) return launch_dir_tiles(ctx, true, counts, offsets, nullptr, pyramid, levels, s);
   constexpr int B = 256;
   const int64_t n_nodes = 1ll << (3 * (levels - 1));
