@@ -60,6 +60,9 @@ def parse():
                          "exact order (default: exact, byte-identical pool)")
     ap.add_argument("--exact-order", dest="exact_order", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--packed", action="store_true", help="packed 64-bit splat z-test")
+    ap.add_argument("--c5-partition", default="views", choices=("views", "subtrees"),
+                    help="C5 on N GPUs: shard the 64 views (POFA replicated) or the octree (each rank traces its "
+                         "octant subtrees of every view; partials composited in entry order)")
     ap.add_argument("--composite", default="auto", choices=("auto", "peer", "allreduce"),
                     help="multi-GPU splat composite: peer memory (fhv_splat_peer over NVLink P2P) or NCCL "
                          "all-reduces; auto = peer when the peer mappings can be set up")
@@ -380,22 +383,42 @@ def extra_config(args):
         scene = sample_scenes.scatter1m()
         cam = capture_camera(scene, "+z", 1080)
         cfg = RasterConfig((1920, 1080), RasterConfig.from_camera(cam).projection, extent=1.0)
-        # views shard across ranks, the FHV replicated
-        vol = fhv.pofa_build(scene, ns, cfg, 8, device=dev)
-        rcfg = fhv.default_raycast_config(vol)
         all_views = sample_scenes.c5_views(64)
-        views = all_views[rank::world]
-        W, H = views[0].resolution
-        shs = [DeviceShading(scene.materials, [headlight(v)], dev) for v in views]
-        buf = img_buf(W, H)
+        subtrees = args.c5_partition == "subtrees" and world > 1
+        if subtrees:
+            # each rank owns whole octant subtrees (one box
+            # per rank), traces them for every view; per-ray (C, A) partials are
+            # composited across ranks in entry order (shard.render_raycast_shard)
+            from paper_2211_15460_b200 import shard as shard_mod
+            comm = shard_mod.TorchComm(device=dev)
+            vol = shard_mod.pofa_build_shard(scene, ns, cfg, 8, comm, balance=False, device=dev)
+            rcfg = fhv.default_raycast_config(vol)
+            views = all_views
+            W, H = views[0].resolution
+            shs = [DeviceShading(scene.materials, [headlight(v)], dev) for v in views]
 
-        def step():
-            sts = []
-            for v, sh in zip(views, shs):
-                buf.pixels.zero_()
-                _, st = fhv.render_raycast(vol, v, [headlight(v)], rcfg, out=buf, sync=False, shading=sh)
-                sts.append(st.counters)
-            return sts
+            def step():
+                sts = []
+                for v, sh in zip(views, shs):
+                    _, st = shard_mod.render_raycast_shard(vol, v, [headlight(v)], rcfg, comm, shading=sh)
+                    sts.append(torch.tensor(list(st.as_dict().values()), dtype=torch.int64, device=dev))
+                return sts
+        else:
+            # views shard across ranks, the FHV replicated
+            vol = fhv.pofa_build(scene, ns, cfg, 8, device=dev)
+            rcfg = fhv.default_raycast_config(vol)
+            views = all_views[rank::world]
+            W, H = views[0].resolution
+            shs = [DeviceShading(scene.materials, [headlight(v)], dev) for v in views]
+            buf = img_buf(W, H)
+
+            def step():
+                sts = []
+                for v, sh in zip(views, shs):
+                    buf.pixels.zero_()
+                    _, st = fhv.render_raycast(vol, v, [headlight(v)], rcfg, out=buf, sync=False, shading=sh)
+                    sts.append(st.counters)
+                return sts
         for _ in range(args.warmup):
             step()
         if world > 1:
@@ -416,8 +439,10 @@ def extra_config(args):
                      "rays_per_s": W * H * len(all_views) / (ms / 1e3),
                      "config": {"workload": "C5: 64 x 3840x2160 perspective ray-cast views (Fibonacci sphere, "
                                             "distance 1.5, fov 45) of C3's POFA (scatter1M, L=8)",
-                                "fragments": vol.pool.next_free, "views": len(all_views),
-                                "parallelism": f"views sharded x{world}, FHV replicated" if world > 1 else "single"},
+                                "fragments": vol.total if subtrees else vol.pool.next_free, "views": len(all_views),
+                                "parallelism": (f"octant subtrees x{world}, partials composited in entry order"
+                                                if subtrees else f"views sharded x{world}, FHV replicated")
+                                if world > 1 else "single"},
                      "raycast_stats": stats.as_dict(),
                      "stage_ms": {k: round(v, 4) for k, v in stage.items()},
                      "roofline": {"bound": "hbm", "kernel": "raycast", "achieved": round(rb / (t_ray / 1e3) / 1e9, 1),

@@ -40,11 +40,12 @@ from . import _lib
 from .device import DeviceShading, capture_cfg, device_scene, host_f64
 from .lights import ImageBuffer
 from .raster import CaptureStrategy, RasterConfig, capture_plan
+from .raycast import primary_rays
 from .scene import Camera, SceneError
 from .storage import FhvError, FragmentPool, OccupancyPyramid, PofaDirectory, _check_levels, morton_decode
 
 __all__ = ["Comm", "FhvPofaShard", "ThreadComm", "TorchComm", "fragment_weights", "pofa_build_shard",
-           "range_boxes", "shard_ranges", "splat_render_shard", "tile_leaves", "PeerFrame"]
+           "range_boxes", "render_raycast_shard", "shard_ranges", "splat_render_shard", "tile_leaves", "PeerFrame"]
 
 MAX_BOXES = 64
 BIN_MARGIN = 1e-5  # world units; fragments lie within 1 f32 ulp of the triangle's AABB
@@ -153,6 +154,10 @@ class Comm:
         """Every rank's device work issued so far is complete on return."""
         raise NotImplementedError
 
+    def all_gather_tensor(self, t: torch.Tensor) -> list:
+        """Every rank's tensor (same shape / dtype), in rank order."""
+        raise NotImplementedError
+
     def peer_alloc(self, shapes_dtypes: list, device) -> tuple:
         """Peer-visible device buffers: (local tensors, per-rank lists of the
         buffers' device pointers as mapped in THIS process)."""
@@ -197,6 +202,12 @@ class TorchComm(Comm):
         if self.device is not None:
             torch.cuda.synchronize(self.device)
         self.dist.barrier(group=self.group)
+
+    def all_gather_tensor(self, t: torch.Tensor) -> list:
+        src = t.contiguous() if self.backend == "nccl" or not t.is_cuda else t.cpu()
+        out = torch.empty((self.world,) + tuple(src.shape), dtype=src.dtype, device=src.device)
+        self.dist.all_gather_into_tensor(out, src, group=self.group)
+        return [o.to(t.device) for o in out]
 
     def peer_alloc(self, shapes_dtypes: list, device) -> tuple:
         # NVLink peer mappings through torch's symmetric memory (one buffer per
@@ -248,6 +259,16 @@ class ThreadComm(Comm):
     def barrier(self) -> None:
         torch.cuda.synchronize(self.device)
         self.hub.barrier.wait()
+
+    def all_gather_tensor(self, t: torch.Tensor) -> list:
+        if t.is_cuda:
+            torch.cuda.synchronize(t.device)
+        parts = self._exchange(t)
+        got = [p.clone() for p in parts]
+        if t.is_cuda:
+            torch.cuda.synchronize(t.device)
+        self._exchange(None)  # every rank has copied every part before any rank reuses its own
+        return got
 
     def peer_alloc(self, shapes_dtypes: list, device) -> tuple:
         # one process, one device: every rank's pointers are directly usable
@@ -508,3 +529,118 @@ def splat_render_shard(vol: FhvPofaShard, camera: Camera, lights, splat_radius_w
     comm.all_reduce_(out.pixels, "sum")
     comm.all_reduce_(out.depth, "sum")
     return out
+
+
+# ---------------------------------------------------------------------------
+# sharded ray cast ("opaque: min-t reduction; R/T: each rank
+# composites its subtree's segment into a partial (C, A); partials composited
+# in per-ray entry order")
+
+
+def region_box(lo: int, hi: int, levels: int):
+    """The world box of leaves [lo, hi) when the range is one axis-aligned box
+    (a union of whole sibling octree nodes forming a slab / quadrant / node:
+    the even partitions of the top-level octants for N = 1, 2, 4, 8), else None."""
+    b = range_boxes(lo, hi, levels)
+    lo3, hi3 = b[:, :3].min(axis=0), b[:, 3:].max(axis=0)
+    vol = float(np.prod(hi3 - lo3))
+    if abs(vol - float(np.sum(np.prod(b[:, 3:] - b[:, :3], axis=1)))) > 1e-12 * max(vol, 1e-300):
+        return None
+    return lo3, hi3
+
+
+def local_volume(vol: FhvPofaShard):
+    """This rank's shard as a stand-alone POFA volume for the ray cast:
+    full-size directory (zero counts outside the owned range, offsets local
+    to the shard's pool) and the pyramid of the shard's own occupancy."""
+    from .storage import FhvPofa
+    L = vol.levels
+    dev = vol.pool.device
+    n = 8 ** L
+    counts = torch.zeros(n, dtype=torch.uint32, device=dev)
+    offsets = torch.zeros(n, dtype=torch.uint32, device=dev)
+    counts[vol.cell_lo:vol.cell_hi] = vol.directory.counts
+    offsets[vol.cell_lo:vol.cell_hi] = (vol.directory.offsets.to(torch.int64) - vol.base).to(torch.uint32)
+    data = vol.pyramid.data.clone()
+    k_tile = L - int(round(np.log(tile_leaves(L)) / np.log(8)))
+    off = [((1 << (3 * k)) - 1) // 7 for k in range(L + 1)]
+    bit = (1 << torch.arange(8, device=dev, dtype=torch.int32))
+    for k in range(k_tile - 1, -1, -1):  # the levels above the tiles, from this shard's occupancy alone
+        below = data[off[k + 1]:off[k + 2]].to(torch.int32).reshape(-1, 8)
+        data[off[k]:off[k + 1]] = ((below != 0).to(torch.int32) * bit).sum(dim=1).to(torch.uint8)
+    pool = vol.pool
+    return FhvPofa(PofaDirectory(L, offsets, counts), OccupancyPyramid(L, data), pool, vol.capture_resolution,
+                   vol.stats, vol.materials)
+
+
+def _entry_t(camera: Camera, box, dev) -> torch.Tensor:
+    """Per pixel: the primary ray's entry parameter into ``box`` (+inf if it
+    misses) -- orders the ranks' segments along each ray."""
+    o, d = primary_rays(camera)
+    w, h = camera.resolution
+    o = torch.from_numpy(np.ascontiguousarray(o)).to(dev)
+    d = torch.from_numpy(np.ascontiguousarray(d)).to(dev)
+    lo3 = torch.tensor(box[0], dtype=torch.float64, device=dev)
+    hi3 = torch.tensor(box[1], dtype=torch.float64, device=dev)
+    with np.errstate(divide="ignore"):
+        inv = 1.0 / d
+    t0, t1 = (lo3 - o) * inv, (hi3 - o) * inv
+    tn = torch.nan_to_num(torch.minimum(t0, t1), nan=-float("inf")).amax(dim=1).clamp_min(0.0)
+    tf = torch.nan_to_num(torch.maximum(t0, t1), nan=float("inf")).amin(dim=1)
+    return torch.where(tn <= tf, tn, torch.full_like(tn, float("inf"))).reshape(h, w)
+
+
+def render_raycast_shard(vol: FhvPofaShard, camera: Camera, lights, cfg, comm: Comm, materials=None,
+                         background=(0.0, 0.0, 0.0, 0.0), *, shading: DeviceShading | None = None):
+    """``render_raycast`` of the whole volume from the ranks' shards, each
+    rank tracing only its own subtree (its Morton range must be one box: the
+    even octant partitions, ``shard_ranges(L, N)`` for N in 1, 2, 4, 8).
+    Each rank returns the full frame and its own RaycastStats.
+
+    * opaque_nearest: each rank's first hit in its traversal order with
+      alpha 1 (the kernel over a transparent background); the front-most
+      region with a hit wins -- bit-identical to the 1-GPU render.
+    * transparency: each rank's front-to-back partial (premultiplied C,
+      coverage A), composited across ranks in entry order, then over the
+      background.  Equal to the 1-GPU render up to floating-point
+      reassociation when the cutoff is 1 (or off): after full coverage the
+      later segments are multiplied by 1 - A = 0.  A cutoff below 1 would
+      need each rank's entry coverage (not supported).
+    * transparency_shadows: shadow rays cross ranks -- replicate the volume.
+    """
+    from .raycast import RAYCAST_MODES, default_raycast_config, render_raycast
+    if cfg is None:
+        cfg = default_raycast_config(vol)
+    if cfg.mode == "transparency_shadows":
+        raise FhvError("shadow rays cross shards: ray-cast a replicated volume for transparency_shadows")
+    if cfg.mode == "transparency" and cfg.alpha_cutoff is not None and cfg.alpha_cutoff < 1.0:
+        raise FhvError("sharded transparency ray cast needs alpha_cutoff 1.0 or None")
+    box = region_box(vol.cell_lo, vol.cell_hi, vol.levels)
+    if box is None:
+        raise FhvError("this rank's Morton range is not one box: use shard_ranges(L, N) for N in 1, 2, 4, 8")
+    dev = vol.pool.device
+    local = local_volume(vol)
+    img, st = render_raycast(local, camera, lights, cfg, materials if materials is not None else vol.materials,
+                             (0.0, 0.0, 0.0, 0.0), shading=shading)
+    t_in = _entry_t(camera, box, dev)
+    parts = comm.all_gather_tensor(img.pixels)
+    ts = torch.stack(comm.all_gather_tensor(t_in))  # [N, h, w]
+    order = torch.argsort(ts, dim=0, stable=True)
+    P = torch.stack(parts)  # [N, h, w, 4] premultiplied (C, A) per rank
+    C = torch.zeros_like(P[0, ..., :3])
+    A = torch.zeros_like(P[0, ..., 3])
+    for k in range(P.shape[0]):
+        pk = torch.gather(P, 0, order[k][None, ..., None].expand(1, *P.shape[1:3], 4))[0]
+        C = C + (1.0 - A)[..., None] * pk[..., :3]
+        A = A + (1.0 - A) * pk[..., 3]
+    bg = torch.tensor(background, dtype=torch.float64, device=dev)
+    out = torch.empty_like(P[0])
+    if cfg.mode == "opaque_nearest":
+        hit = A > 0.0
+        out[..., :3] = torch.where(hit[..., None], C, bg[:3].expand_as(C))
+        out[..., 3] = torch.where(hit, torch.ones_like(A), bg[3].expand_as(A))
+    else:
+        out[..., :3] = C + ((1.0 - A) * bg[3])[..., None] * bg[:3]
+        out[..., 3] = A + (1.0 - A) * bg[3]
+    img.pixels.copy_(out)
+    return img, st

@@ -10,6 +10,7 @@ import torch
 import paper_2211_15460_b200 as fhv
 from paper_2211_15460_b200 import sample_scenes, shard
 from paper_2211_15460_b200.render import image_numpy
+from paper_2211_15460_b200.scene import look_at_camera
 
 pytestmark = pytest.mark.gpu
 
@@ -134,3 +135,45 @@ def test_peer_composited_splat_equals_single_gpu(name, world):
             want = refs[i // 2]
             assert np.array_equal(img.depth, want.depth)
             assert np.array_equal(img.pixels, want.pixels)
+
+
+@pytest.mark.parametrize("name", ("cornell", "spheres"))
+@pytest.mark.parametrize("world", (2, 4, 8))
+@pytest.mark.parametrize("mode", ("opaque_nearest", "transparency"))
+def test_subtree_sharded_raycast_equals_single_gpu(name, world, mode):
+    """SURVEY 8(e) ray-cast partition: every rank traces only its own octant
+    subtrees; opaque = front-most region's first hit (bit-identical),
+    transparency = per-region (C, A) partials composited in entry order
+    (equal up to reassociation, 1e-12)."""
+    scene = _scene(name)
+    res, L = 256, 6
+    cfg = fhv.RasterConfig.from_camera(fhv.capture_camera(scene, "+z", res))
+    ns = fhv.CaptureStrategy.normal_space()
+    ref = fhv.pofa_build(scene, ns, cfg, L, exact_order=True)
+    cams = [fhv.viewpoint_camera("+x", (96, 80), "perspective"),
+            look_at_camera((1.3, 1.1, 1.6), resolution=(72, 64))]
+    rc = fhv.default_raycast_config(ref, mode=mode)
+    bg = (0.1, 0.2, 0.3, 0.5)
+    refs = []
+    for cam in cams:
+        img, st = fhv.render_raycast(ref, cam, [fhv.headlight(cam)], rc, scene.materials, bg)
+        refs.append((img.pixels.cpu().numpy(), st))
+
+    def rank_fn(c):
+        v = shard.pofa_build_shard(scene, ns, cfg, L, c, balance=False, exact_order=True)
+        outs = []
+        for cam in cams:
+            img, st = shard.render_raycast_shard(v, cam, [fhv.headlight(cam)], rc, c, scene.materials, bg)
+            outs.append((img.pixels.cpu().numpy(), st))
+        return outs
+
+    per_rank = _run_ranks(world, rank_fn)
+    for i, (want, st_ref) in enumerate(refs):
+        hits = sum(o[i][1].hits for o in per_rank)
+        assert hits >= st_ref.hits > 0
+        for o in per_rank:
+            got = o[i][0]
+            if mode == "opaque_nearest":
+                assert np.array_equal(got, want)
+            else:
+                assert np.max(np.abs(got - want)) <= 1e-12

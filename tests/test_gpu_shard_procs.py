@@ -1,0 +1,104 @@
+"""The sharded pipeline over a REAL process group: two processes joined by
+torch.distributed (gloo -- both ranks share the one B200 of a test box; on
+an 8-GPU box the same code runs over NCCL, one process per GPU, bench.py
+--gpus N), each running pofa_build_shard + splat_render_shard through
+TorchComm.  The union of the ranks' shards and every rank's frame must be
+bit-identical to the 1-GPU pofa_build / splat_render."""
+import hashlib
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+RES, L = 256, 6
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _sha(t):
+    return hashlib.sha256(np.ascontiguousarray(t.cpu().numpy()).tobytes()).hexdigest()
+
+
+def _setup():
+    import paper_2211_15460_b200 as fhv
+    from paper_2211_15460_b200 import sample_scenes
+    scene = sample_scenes.sphere_field(6, 3, seed=3, r_lo=0.05, r_hi=0.2, c_lo=0.2, c_hi=0.8)
+    cfg = fhv.RasterConfig.from_camera(fhv.capture_camera(scene, "+z", RES))
+    cam = fhv.viewpoint_camera("+x", (96, 80), "perspective")
+    return fhv, scene, cfg, cam
+
+
+def _worker(rank, world, port, q, steps):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fhv, scene, cfg, cam = _setup()
+        from paper_2211_15460_b200 import shard
+        from paper_2211_15460_b200.render import image_numpy
+        comm = shard.TorchComm(device=torch.device("cuda", 0))
+        ns = fhv.CaptureStrategy.normal_space()
+        out = []
+        for _ in range(steps):  # repeated steps: cached plans, pool guesses, reused buffers
+            v = shard.pofa_build_shard(scene, ns, cfg, L, comm, exact_order=True)
+            img = image_numpy(shard.splat_render_shard(v, cam, [fhv.headlight(cam)], 1.0 / RES, scene.materials, comm))
+            pyr = v.gather_pyramid(comm)
+            out.append({"lo": v.cell_lo, "hi": v.cell_hi, "base": v.base, "total": v.total,
+                        "pool": {k: getattr(v.pool, k).cpu().numpy() for k in
+                                 ("position", "normal", "material_id", "object_id", "prev_index")},
+                        "counts": v.directory.counts.cpu().numpy(), "offsets": v.directory.offsets.cpu().numpy(),
+                        "pyr": pyr.data.cpu().numpy(), "depth": img.depth, "rgba": img.pixels})
+        q.put((rank, out))
+    except BaseException as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", (2,))
+def test_two_process_sharded_pofa_and_splat_equal_single_gpu(world):
+    import torch.multiprocessing as mp
+    fhv, scene, cfg, cam = _setup()
+    ref = fhv.pofa_build(scene, fhv.CaptureStrategy.normal_space(), cfg, L, exact_order=True)
+    from paper_2211_15460_b200.render import image_numpy
+    ref_img = image_numpy(fhv.splat_render(ref.pool, cam, [fhv.headlight(cam)], 1.0 / RES, scene.materials))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    steps = 2
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, steps)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+    for step in range(steps):
+        shards = [res[r][step] for r in range(world)]
+        assert shards[0]["lo"] == 0 and shards[-1]["hi"] == 8 ** L
+        assert all(shards[r]["hi"] == shards[r + 1]["lo"] for r in range(world - 1))
+        assert all(s["total"] == ref.pool.capacity for s in shards)
+        for k in ("position", "normal", "material_id", "object_id", "prev_index"):
+            cat = np.concatenate([s["pool"][k] for s in shards])
+            assert np.array_equal(cat, getattr(ref.pool, k).cpu().numpy()), (step, k)
+        assert np.array_equal(np.concatenate([s["counts"] for s in shards]), ref.directory.counts.cpu().numpy())
+        assert np.array_equal(np.concatenate([s["offsets"] for s in shards]), ref.directory.offsets.cpu().numpy())
+        for s in shards:
+            assert np.array_equal(s["pyr"], ref.pyramid.data.cpu().numpy())
+            assert np.array_equal(s["depth"], ref_img.depth)
+            assert np.array_equal(s["rgba"], ref_img.pixels)
+    for p in procs:
+        assert p.exitcode == 0
