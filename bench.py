@@ -70,6 +70,9 @@ def parse():
                     help="time the Python-enqueued steps instead of CUDA-graph replays of one captured step")
     ap.add_argument("--sync-steps", action="store_true",
                     help="wait for each pofa_build on the host (default: asynchronous steps, tickets checked)")
+    ap.add_argument("--upload", default="indexed", choices=("indexed", "soup"),
+                    help="e2e: the scene crosses PCIe as an indexed mesh expanded on the device (default) or as the "
+                         "triangle arrays")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="few steps, no clocks/e2e/cpu (for ncu)")
     return ap.parse_args()
@@ -776,14 +779,35 @@ def main():
     # buffered, so step k+1's upload and step k-1's read-back overlap step
     # k's kernels (a two-deep pipeline, as a serving loop would run it).
     if not args.profile_only:
-        # face normals are a pure function of the positions (make_triangle,
-        # fhv/scene.py:137-139): they are re-derived on the device, bit-identical
-        # (tests/test_gpu_fullsize.py::test_device_face_normals_bit_exact), not uploaded
+        # The scene crosses PCIe every step.  --upload indexed (default): as an
+        # IndexedMesh (shared vertex rows + u32 faces, 43 MB for C3 instead of
+        # the 149-MB triangle soup) that the device expands into the soup
+        # arrays, byte for byte (checked below), face normals re-derived with
+        # make_triangle's arithmetic.  --upload soup: the triangle arrays as such.
+        from paper_2211_15460_b200.device import IndexedMesh, IndexedUpload
         probe = DeviceScene(scene, dev)
         derive_fn = bool(torch.equal(probe.fnrm.clone(), probe.derive_face_normals()))
+        indexed = args.upload == "indexed" and derive_fn
+        if indexed:
+            mesh = IndexedMesh.from_scene(scene)
+            arrays = mesh.arrays()
+            stage = [IndexedUpload(mesh, dev) for _ in range(2)]
+            for d_, src in zip(stage[0].tensors(), arrays):
+                d_.copy_(torch.from_numpy(np.ascontiguousarray(src)))
+            ref_soup = DeviceScene(scene, dev)
+            probe.pos.zero_(); probe.vnrm.zero_(); probe.fnrm.zero_()
+            probe.load_indexed(stage[0])
+            idx_ok = all(torch.equal(getattr(probe, f).view(torch.int64) if getattr(probe, f).dtype == torch.float64
+                                     else getattr(probe, f), getattr(ref_soup, f).view(torch.int64)
+                                     if getattr(ref_soup, f).dtype == torch.float64 else getattr(ref_soup, f))
+                         for f in ("pos", "vnrm", "fnrm", "mat", "obj"))
+            if not idx_ok:
+                raise RuntimeError("indexed expansion differs from the triangle arrays")
+            del ref_soup
+        else:
+            arrays = (scene.positions, scene.normals) + (() if derive_fn else (scene.face_normals,)) + \
+                (scene.material_id.view(np.int32), scene.object_id.view(np.int32))
         del probe
-        arrays = (scene.positions, scene.normals) + (() if derive_fn else (scene.face_normals,)) + \
-            (scene.material_id.view(np.int32), scene.object_id.view(np.int32))
         pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays]
         bufs_in = [ds, DeviceScene(scene, dev)]
         bufs_out = [img, ImageBuffer(W, H, torch.empty((H, W, 4), dtype=torch.float64, device=dev),
@@ -791,13 +815,18 @@ def main():
         out_px = [torch.empty((H, W, 4), dtype=torch.float64).pin_memory() for _ in range(2)]
         out_dp = [torch.empty((H, W), dtype=torch.float64).pin_memory() for _ in range(2)]
         h2d = sum(p.numel() * p.element_size() for p in pin)
+
+        def dst_of(k):
+            if indexed:
+                return stage[k % 2].tensors()
+            b = bufs_in[k % 2]
+            return (b.pos, b.vnrm) + (() if derive_fn else (b.fnrm,)) + (b.mat.view(torch.int32), b.obj.view(torch.int32))
         # the link itself: the same pinned uploads alone (PCIe bound of the e2e line)
         torch.cuda.synchronize()
         el0, el1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         el0.record(stream)
         for _ in range(3):
-            for d_, src in zip((ds.pos, ds.vnrm) + (() if derive_fn else (ds.fnrm,)) +
-                               (ds.mat.view(torch.int32), ds.obj.view(torch.int32)), pin):
+            for d_, src in zip(dst_of(0), pin):
                 d_.copy_(src, non_blocking=True)
         el1.record(stream)
         torch.cuda.synchronize()
@@ -810,13 +839,11 @@ def main():
         e_start = ev()
 
         def upload(k):
-            b = bufs_in[k % 2]
             s_in.wait_event(e_start)
             if k >= 2:
                 s_in.wait_event(e_done[k - 2])  # buffer k%2 free again
-            dsts = (b.pos, b.vnrm) + (() if derive_fn else (b.fnrm,)) + (b.mat.view(torch.int32), b.obj.view(torch.int32))
             with torch.cuda.stream(s_in):
-                for d, src in zip(dsts, pin):
+                for d, src in zip(dst_of(k), pin):
                     d.copy_(src, non_blocking=True)
                 e_in[k].record(s_in)
 
@@ -838,7 +865,9 @@ def main():
             stream.wait_event(e_in[k])
             if k >= 2:
                 stream.wait_event(e_out[k - 2])  # image buffer k%2 read back
-            if derive_fn:
+            if indexed:
+                bufs_in[k % 2].load_indexed(stage[k % 2])  # gather + ids + face normals, on the device
+            elif derive_fn:
                 bufs_in[k % 2].derive_face_normals()
             step(bufs_in[k % 2], bufs_out[k % 2])
             e_done[k].record(stream)
@@ -859,6 +888,9 @@ def main():
         e2e = {"value": n_frags * args.steps / (ms_e2e / 1e3), "unit": "frag/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps,
                "pipeline": "2-deep: H2D(k+1) and D2H(k-1) on copy streams overlap step k",
+               "upload": ("indexed mesh: %d shared vertex rows + %d u32 faces, expanded on the device into the "
+                          "triangle arrays (checked byte-identical before timing)" % (mesh.n_vertices, mesh.n_triangles)
+                          if indexed else "triangle arrays"),
                "face_normals": "derived on device (bit-identical)" if derive_fn else "uploaded",
                "readback_matches_device": bool(ok), "h2d_link_gbs": round(h2d_gbs, 1)}
     else:

@@ -395,6 +395,16 @@ int fhv_raycast_image(fhv_ctx *ctx, int64_t start, int64_t end, const double *or
 /* make_triangle face normals for a bulk scene (fhv/scene.py:137-139). Async. */
 int fhv_face_normals(fhv_ctx *ctx, int64_t n_tri, const double *pos, double *fnrm, void *stream);
 
+/* Indexed scene upload: triangle arrays pos / vnrm [n_tri][3][3] f64 gathered
+   from shared vertex rows vpos / vn [n_vert][3] through faces [n_tri][3]
+   (u32 vertex indices) -- the triangle-soup arrays load_scene / make_triangle
+   produce (fhv/scene.py:129-146, 291-378), byte for byte, from ~1/3.5 of the
+   bytes over PCIe (meshes share each vertex among ~6 triangles).  A face
+   index >= n_vert -> FHV_BAD_ARGS (checked on the device, reported by the
+   next synchronising call).  Async. */
+int fhv_expand_indexed(fhv_ctx *ctx, int64_t n_vert, const double *vpos, const double *vn, int64_t n_tri,
+                       const uint32_t *faces, double *pos, double *vnrm, void *stream);
+
 /* ---- the reference's operator API, kernels() (fhv/_backend.py:25-29), batched ----
    coverage (fhv/_ckern.pyx:25-105) of n raster-space triangles v6[n][6] =
    (ax, ay, bx, by, cx, cy) on rasters wh[n][2] = (w, h): covered pixel

@@ -111,6 +111,7 @@ _SIGS = {
     "fhv_deferred": (ctypes.c_int, [c_vp, _P(Tris), c_vp, c_i32, c_i32, c_vp, _P(Shading), c_vp, c_vp, c_vp,
                                     _P(GBuf), _P(c_i64), c_vp]),
     "fhv_face_normals": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "fhv_expand_indexed": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "fhv_capture_list_depth": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                               c_vp, _P(c_i64), c_vp]),
     "fhv_raster_screen": (ctypes.c_int, [c_vp, _P(Tris), c_vp, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,

@@ -3053,6 +3053,42 @@ extern "C" int fhv_unit_rows(fhv_ctx* ctx, int64_t n, const double* in, double* 
   return FHV_OK;
 }
 
+namespace fhv {
+namespace {
+// indexed -> triangle-soup gather: thread per (triangle, corner, component)
+// pair of f64 rows, coalesced writes
+__global__ void __launch_bounds__(256) k_expand_indexed(long long n_vert, const double* __restrict__ vpos,
+                                                        const double* __restrict__ vn, long long n_tri,
+                                                        const uint32_t* __restrict__ faces, double* __restrict__ pos,
+                                                        double* __restrict__ vnrm, int* status) {
+  const long long n = 9 * n_tri;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long corner = i / 3;  // (triangle, vertex) slot
+    const int comp = (int)(i - 3 * corner);
+    const uint32_t v = __ldg(&faces[corner]);
+    if ((long long)v >= n_vert) {
+      raise_status(status, FHV_BAD_ARGS);
+      continue;
+    }
+    pos[i] = __ldg(&vpos[3 * (long long)v + comp]);
+    vnrm[i] = __ldg(&vn[3 * (long long)v + comp]);
+  }
+}
+}  // namespace
+}  // namespace fhv
+
+extern "C" int fhv_expand_indexed(fhv_ctx* ctx, int64_t n_vert, const double* vpos, const double* vn, int64_t n_tri,
+                                  const uint32_t* faces, double* pos, double* vnrm, void* stream) {
+  if (!ctx || n_vert < 0 || n_tri < 0 || (n_tri && (!vpos || !vn || !faces || !pos || !vnrm))) return FHV_BAD_ARGS;
+  if (n_tri == 0) return FHV_OK;
+  {
+    LaunchScope L_(ctx, kStFaceNormals, (cudaStream_t)stream);
+    k_expand_indexed<<<grid_for(9 * n_tri, 256), 256, 0, (cudaStream_t)stream>>>(n_vert, vpos, vn, n_tri, faces, pos,
+                                                                                vnrm, &ctx->ctl->status);
+  }
+  return check_cuda(ctx, cudaGetLastError());
+}
+
 extern "C" int fhv_face_normals(fhv_ctx* ctx, int64_t n_tri, const double* pos, double* fnrm, void* stream) {
   if (!ctx || n_tri < 0 || (n_tri && (!pos || !fnrm))) return FHV_BAD_ARGS;
   if (n_tri == 0) return FHV_OK;

@@ -67,6 +67,22 @@ class DeviceScene:
         _lib.check(rc, "face normals")
         return self.fnrm
 
+    def load_indexed(self, up: "IndexedUpload") -> "DeviceScene":
+        """Fill this scene's triangle arrays from indexed device buffers on the
+        current stream: the gather (fhv_expand_indexed), the ids, and the face
+        normals re-derived with make_triangle's arithmetic."""
+        if up.n_tri != self.n_tri:
+            raise ValueError("indexed upload has a different triangle count")
+        lib = _lib.load()
+        rc = lib.fhv_expand_indexed(_lib.ctx(self.device), up.n_vert, _lib.ptr(up.vpos), _lib.ptr(up.vn), up.n_tri,
+                                    _lib.ptr(up.faces), _lib.ptr(self.pos), _lib.ptr(self.vnrm),
+                                    _lib.stream_ptr(self.device))
+        _lib.check(rc, "expand indexed")
+        self.mat.view(torch.int32).copy_(up.mat)
+        self.obj.view(torch.int32).copy_(up.obj)
+        self.derive_face_normals()
+        return self
+
     def struct(self) -> _lib.Tris:
         # the C struct is cached with the pointers it was built from
         key = (self.n_tri, self.pos.data_ptr(), self.vnrm.data_ptr(), self.fnrm.data_ptr(), self.mat.data_ptr(),
@@ -81,6 +97,78 @@ class DeviceScene:
     @property
     def nbytes(self) -> int:
         return 176 * self.n_tri
+
+
+class IndexedMesh:
+    """A scene's triangle arrays in shared-vertex form, for cheap uploads:
+    (position, vertex normal) rows deduplicated by their exact bytes and the
+    faces as u32 vertex indices -- the same doubles, ~1/3.5 of the bytes for a
+    mesh (each vertex shared by ~6 triangles).  ``DeviceScene.load_indexed``
+    expands them on the device into the triangle arrays ``make_triangle`` /
+    ``load_scene`` produce (fhv/scene.py:129-146, 291-378), byte for byte;
+    face normals are re-derived there (``derive_face_normals``)."""
+
+    def __init__(self, vpos: np.ndarray, vn: np.ndarray, faces: np.ndarray, mat: np.ndarray, obj: np.ndarray):
+        self.vpos = np.ascontiguousarray(vpos, dtype=np.float64)
+        self.vn = np.ascontiguousarray(vn, dtype=np.float64)
+        self.faces = np.ascontiguousarray(faces, dtype=np.uint32)
+        self.mat = np.ascontiguousarray(mat, dtype=np.uint32)
+        self.obj = np.ascontiguousarray(obj, dtype=np.uint32)
+        if self.vpos.shape != self.vn.shape or self.vpos.ndim != 2 or self.vpos.shape[1] != 3:
+            raise ValueError("vertex rows must be [n_vert, 3] positions and normals")
+        if self.faces.ndim != 2 or self.faces.shape[1] != 3 or len(self.mat) != len(self.faces) \
+                or len(self.obj) != len(self.faces):
+            raise ValueError("faces must be [n_tri, 3] with one material / object id per face")
+        if len(self.faces) and int(self.faces.max()) >= len(self.vpos):
+            raise ValueError("face vertex index out of range")
+
+    @staticmethod
+    def from_scene(scene) -> "IndexedMesh":
+        """Deduplicate a scene's corners (cached on the scene)."""
+        hit = scene.__dict__.get("_indexed_mesh")
+        if hit is not None:
+            return hit
+        T = scene.n_triangles
+        rows = np.ascontiguousarray(np.concatenate((scene.positions.reshape(3 * T, 3),
+                                                    scene.normals.reshape(3 * T, 3)), axis=1))
+        keys = rows.view(np.dtype((np.void, 48))).reshape(-1)
+        _, first, inv = np.unique(keys, return_index=True, return_inverse=True)
+        uniq = rows[first]
+        mesh = IndexedMesh(uniq[:, :3], uniq[:, 3:], inv.reshape(T, 3).astype(np.uint32),
+                           scene.material_id, scene.object_id)
+        scene.__dict__["_indexed_mesh"] = mesh
+        return mesh
+
+    @property
+    def n_vertices(self) -> int:
+        return len(self.vpos)
+
+    @property
+    def n_triangles(self) -> int:
+        return len(self.faces)
+
+    @property
+    def nbytes(self) -> int:
+        return self.vpos.nbytes + self.vn.nbytes + self.faces.nbytes + self.mat.nbytes + self.obj.nbytes
+
+    def arrays(self) -> tuple:
+        return self.vpos, self.vn, self.faces.view(np.int32), self.mat.view(np.int32), self.obj.view(np.int32)
+
+
+class IndexedUpload:
+    """Device staging buffers of one IndexedMesh (vertex rows, faces, ids),
+    refilled by each upload (e.g. from pinned host copies on a copy stream)."""
+
+    def __init__(self, mesh: IndexedMesh, device: torch.device):
+        self.n_vert, self.n_tri = mesh.n_vertices, mesh.n_triangles
+        self.vpos = torch.empty((self.n_vert, 3), dtype=torch.float64, device=device)
+        self.vn = torch.empty((self.n_vert, 3), dtype=torch.float64, device=device)
+        self.faces = torch.empty((self.n_tri, 3), dtype=torch.int32, device=device)
+        self.mat = torch.empty(self.n_tri, dtype=torch.int32, device=device)
+        self.obj = torch.empty(self.n_tri, dtype=torch.int32, device=device)
+
+    def tensors(self) -> tuple:
+        return self.vpos, self.vn, self.faces, self.mat, self.obj
 
 
 def device_scene(scene, device=None) -> DeviceScene:

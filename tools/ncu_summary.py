@@ -22,6 +22,14 @@ COLS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps %"),
     ("launch__registers_per_thread", "regs"),
 ]
+ATOM = [
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", "RED req L1"),
+    ("lts__t_requests_srcunit_tex_op_red.sum", "RED req L2"),
+    ("l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_red.sum.pct_of_peak_sustained_elapsed", "RED L1 pipe %"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum", "ATOM req L1"),
+    ("lts__t_requests_srcunit_tex_op_atom_dot_alu.sum", "ATOM req L2"),
+    ("l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_atom.sum.pct_of_peak_sustained_elapsed", "ATOM L1 pipe %"),
+]
 SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
 
 
@@ -47,6 +55,20 @@ def main(path):
         gbs = (vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) * 1e6 / (t_us * 1e-6) / 1e9
         name = d[kn].split("(")[0].replace("void ", "")
         print(f"| `{name}` | " + " | ".join(f"{vals[k]:.1f}" for k, _ in COLS) + f" | {gbs:.0f} |")
+    atom_cols = [c for c in ATOM if c[0] in hdr]
+    if not atom_cols:
+        return
+    print("\n## Atomic / reduction traffic per launch (RED = no return value, ATOM = returning)\n")
+    print("| kernel | us | " + " | ".join(h for _, h in atom_cols) + " |")
+    print("|---" * (len(atom_cols) + 2) + "|")
+    for d in data:
+        red = [float(d[hdr.index(k)].replace(",", "")) for k, _ in atom_cols]
+        if not any(red):
+            continue
+        t_us = float(d[ix["gpu__time_duration.sum"]]) * SCALE.get(units[ix["gpu__time_duration.sum"]], 1.0)
+        name = d[kn].split("(")[0].replace("void ", "")
+        print(f"| `{name}` | {t_us:.1f} | " + " | ".join(
+            f"{v:.2f}" if "pct" in k else f"{v:,.0f}" for v, (k, _) in zip(red, atom_cols)) + " |")
 
 
 if __name__ == "__main__":
