@@ -162,7 +162,10 @@ int64_t fhv_ctx_launches(const fhv_ctx *ctx);
 /* diagnostics of the last SYNCHRONISED call on this context: out[0] = leaves
    the EXACT_ORDER POFA tile fix-up re-sorted, out[1] = fragments the raster
    passes sent through the exact (uncertified) path, out[2] = long leaves
-   handed to the per-leaf pass; returns the words written (3) */
+   handed to the per-leaf pass; with n >= 4 (synchronises the device) the
+   last packet ray cast (fhv_raycast): out[3] = rays handed to its per-ray
+   kernel, out[4] = (ray, node) pairs that took their own child order (tied
+   entry distances); returns the words written (3, 4 or 5) */
 int fhv_ctx_counters(const fhv_ctx *ctx, int64_t *out, int n);
 
 /* per-kernel CUDA-event timing on the launching stream (off by default).

@@ -254,6 +254,18 @@ def counters(device: torch.device) -> tuple:
     return tuple(int(v) for v in out)
 
 
+def raycast_diag(device: torch.device) -> tuple:
+    """(rays handed to the per-ray kernel, (ray, node) pairs that took their
+    own child order) of the last packet ray cast on the calling thread's
+    context (fhv_ctx_counters words 3-4; synchronises the device)."""
+    import numpy as np
+    out = np.zeros(5, dtype=np.int64)
+    rc = load().fhv_ctx_counters(ctx(device), out.ctypes.data, 5)
+    if rc < 0:
+        check(-rc, "raycast_diag")
+    return int(out[3]), int(out[4])
+
+
 def prof_enable(device: torch.device, on: bool = True) -> None:
     idx = device.index if device.index is not None else torch.cuda.current_device()
     _prof_on[idx] = on

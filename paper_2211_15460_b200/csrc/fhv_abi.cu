@@ -81,7 +81,7 @@ LaunchScope::~LaunchScope() {
 static const char* kStageNames[kNumStages] = {
     "job_setup", "scan", "item_expand", "count", "count_leaves", "emit_list", "emit_ppfl", "emit_pofl",
     "emit_pofa", "chain_order", "leaf_order", "scan_leaves", "pyramid", "splat_depth", "splat_index",
-    "splat_resolve", "raycast", "face_normals", "deferred", "ops", "scalar", "leaf_sort"};
+    "splat_resolve", "raycast", "face_normals", "deferred", "ops", "scalar", "leaf_sort", "raycast_handoff"};
 
 }  // namespace fhv
 
@@ -155,7 +155,23 @@ extern "C" int64_t fhv_ctx_launches(const fhv_ctx* ctx) { return ctx ? ctx->laun
 extern "C" int fhv_ctx_counters(const fhv_ctx* ctx, int64_t* out, int n) {
   if (!ctx || !out || n < 3) return -FHV_BAD_ARGS;
   for (int k = 0; k < 3; ++k) out[k] = (int64_t)ctx->ctl_host->leaf_n[k];
-  return 3;
+  if (n < 4) return 3;
+  // the last packet ray cast: out[3] = rays handed to the per-ray kernel,
+  // out[4] = (lane, node) pairs that took their own child order (synchronises)
+  out[3] = 0;
+  if (n > 4) out[4] = 0;
+  const DevBuf& b = ctx->bufs[kRays];
+  if (b.ptr) {
+    unsigned long long v[3] = {0, 0, 0};
+    cudaDeviceSynchronize();
+    if (cudaMemcpy(v, b.ptr, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaGetLastError();
+      return -FHV_CUDA_ERROR;
+    }
+    out[3] = (int64_t)v[0];
+    if (n > 4) out[4] = (int64_t)v[2];
+  }
+  return n > 4 ? 5 : 4;
 }
 
 // self-test of the shared-divisor division (fhv_common.cuh div_rn) against

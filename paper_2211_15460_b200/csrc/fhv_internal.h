@@ -48,7 +48,8 @@ namespace fhv {
 enum Stage {
   kStJobSetup = 0, kStScan, kStItemExpand, kStCount, kStCountLeaves, kStEmitList, kStEmitPpfl, kStEmitPofl,
   kStEmitPofa, kStChainOrder, kStLeafOrder, kStScanLeaves, kStPyramid, kStSplatDepth, kStSplatIndex,
-  kStSplatResolve, kStRaycast, kStFaceNormals, kStDeferred, kStOps, kStScalar, kStLeafSort, kNumStages
+  kStSplatResolve, kStRaycast, kStFaceNormals, kStDeferred, kStOps, kStScalar, kStLeafSort, kStRaycastHandoff,
+  kNumStages
 };
 struct PendingEvent {
   int stage;

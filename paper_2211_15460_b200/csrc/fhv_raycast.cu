@@ -46,6 +46,11 @@ struct RayParams {
   int32_t* out_ids;
   long long* counters;
   unsigned long long* tile_ticket;  // dynamic 32-ray work fetching (zeroed before the launch)
+  // packet kernel -> per-ray kernel hand-off: pixel indices of the rays whose
+  // own (t_enter, child) order left the packet's shared child order
+  long long* ray_list;
+  unsigned long long* ray_list_n;
+  unsigned long long* own_order_n;  // (lane, node) pairs that took their own child order
 };
 
 struct Stats {
@@ -412,16 +417,19 @@ __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
   const long long tiles_per_row = x.W / 8;
   // warps fetch 32-ray tiles from a global ticket (ray costs vary by orders
   // of magnitude: dynamic fetching instead of a static stride evens the tail)
-  const long long n_rays = x.end - x.start;
+  // list mode: the rays the packet kernel handed off (count on the device)
+  const long long n_rays = x.ray_list ? (long long)*x.ray_list_n : x.end - x.start;
   while (true) {
     unsigned long long t = 0;
     if (lane_id() == 0) t = atomicAdd(x.tile_ticket, 1ull);
     t = __shfl_sync(0xffffffffu, t, 0);
     if ((long long)t * 32 >= n_rays) break;
     const long long kk = x.start + (long long)t * 32 + lane_id();
-    if (kk >= x.end) continue;
+    if (kk >= x.start + n_rays) continue;
     long long k = kk;
-    if (tiled) {
+    if (x.ray_list) {
+      k = x.ray_list[kk - x.start];
+    } else if (tiled) {
       const long long i = kk - x.start, tile = i >> 5, l = i & 31;
       const long long ty = tile / tiles_per_row, tx = tile - ty * tiles_per_row;
       k = x.start + (ty * 4 + (l >> 3)) * x.W + tx * 8 + (l & 7);
@@ -492,6 +500,458 @@ __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
     for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
   }
   if (lane_id() == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (v[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&x.counters[q]), v[q]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Packet ray cast (camera rays, modes 0 / 1): one warp walks the octree ONCE
+// for its 8x4 pixel tile.
+//
+// The DFS stack lives in shared memory and each entry carries the mask of the
+// lanes whose ray reached that node, so every node is expanded by the whole
+// warp in lock-step (the per-lane slab arithmetic is exactly expand_node's)
+// and every leaf's fragment list is walked once, its loads broadcast to the
+// lanes that test it.  The warp pushes the children in ONE shared order: for
+// rays leaving a common eye (perspective) or along a common direction
+// (orthographic) the children a ray meets form a chain across the node's
+// three centre planes, and ordering them by (child XOR s) -- s = the eye's /
+// the ray's entry side of each plane -- is a front-to-back order for every
+// ray of the tile.  Each lane checks at every node that the shared order of
+// the children IT meets is its own (t_enter, child) order (the reference's
+// insertion sort, fhv/_ckern.pyx:580-632); a lane where it is not (ties of
+// rounded entry distances) leaves the packet and its ray is re-run, from
+// scratch, by the per-ray kernel (k_raycast in list mode), so every ray's
+// visit sequence -- and with it the image and RaycastStats -- is the
+// reference's.
+//
+// Hits are shaded warp-wide: the hits all lanes deliver from a leaf are laid
+// out lane-major in shared memory, each lane shades one of every 32, and each
+// lane then composites its own hits in (t, index) order.
+#ifndef FHV_PKT_HITS
+#define FHV_PKT_HITS 4  // per-lane buffered hits per leaf (more: exact rescans)
+#endif
+#ifndef FHV_PKT_MINB
+#define FHV_PKT_MINB 4
+#endif
+constexpr int kPktHits = FHV_PKT_HITS;
+constexpr int kPktWarps = 4;  // 128-thread CTAs
+
+// shared stack: 7 per level for the shared order plus room for the lanes
+// that take their own order at a node (ties); a push that would not fit hands
+// those lanes to the per-ray kernel instead
+constexpr int kPktStack = 16 * kRayMaxLevels + 8;
+template <class E>
+struct PktShared {
+  E node[kPktStack];
+  unsigned lanes[kPktStack];
+  int slot_idx[32 * kPktHits];
+  double col[32][3];
+};
+
+// sorted insertion into the register buffer (compile-time indices only: the
+// candidate walks up, swapping with every larger entry; the largest falls off)
+__device__ __forceinline__ void pkt_insert(double t, int k, double bt[kPktHits], int bi[kPktHits], int& nb) {
+  if (nb == kPktHits && !hit_less(t, k, bt[kPktHits - 1], bi[kPktHits - 1])) return;
+#pragma unroll
+  for (int q = 0; q < kPktHits; ++q) {
+    if (q < nb) {
+      if (hit_less(t, k, bt[q], bi[q])) {
+        const double ut = bt[q];
+        const int uk = bi[q];
+        bt[q] = t;
+        bi[q] = k;
+        t = ut;
+        k = uk;
+      }
+    } else if (q == nb) {
+      bt[q] = t;
+      bi[q] = k;
+    }
+  }
+  if (nb < kPktHits) ++nb;
+}
+
+// the kPktHits smallest (t, k) of the leaf above (lt, li) for lanes with `on`;
+// returns how many hits lie above the bound.  The fragment walk is warp-uniform.
+template <bool kBound>
+__device__ __forceinline__ int pkt_collect(const RayParams& x, long long code, bool on, const double o[3],
+                                           const double d[3], double lt, int li, double bt[kPktHits],
+                                           int bi[kPktHits], int& nb, unsigned& tested) {
+  int nh = 0;
+  nb = 0;
+  if (x.v.layout == 0) {
+    const long long beg = __ldg(&x.v.offsets[code]);
+    const long long cnt = __ldg(&x.v.counts[code]);
+    for (long long kk = beg; kk < beg + cnt; ++kk) {
+      if (!on) continue;
+      const int k = (int)kk;
+      ++tested;
+      double t;
+      if (!hit_test(x, k, o, d, 0.0, __longlong_as_double(0x7ff0000000000000ll), &t)) continue;
+      if (kBound && !hit_less(lt, li, t, k)) continue;
+      ++nh;
+      pkt_insert(t, k, bt, bi, nb);
+    }
+  } else {
+    for (int k = __ldg(&x.v.heads[code]); k >= 0; k = __ldg(&x.v.prev[k])) {
+      if (!on) continue;
+      ++tested;
+      double t;
+      if (!hit_test(x, k, o, d, 0.0, __longlong_as_double(0x7ff0000000000000ll), &t)) continue;
+      if (kBound && !hit_less(lt, li, t, k)) continue;
+      ++nh;
+      pkt_insert(t, k, bt, bi, nb);
+    }
+  }
+  return nh;
+}
+
+#ifndef FHV_PKT_SHADE_NOINLINE
+#define FHV_PKT_SHADE_NOINLINE 0
+#endif
+#if FHV_PKT_SHADE_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void pkt_shade(const RayParams& x, int i, long long leaf, double col[3]) {
+  Stats dummy = {0, 0, 0, 0};
+  shade_hit<1, uint32_t>(x, i, leaf, dummy, col);  // modes 0 / 1: no shadow traversal
+}
+
+template <int kMode, class E>
+__global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet(RayParams x) {
+  using SC = StackCodec<E>;
+  __shared__ PktShared<E> shm[kPktWarps];
+  PktShared<E>& S = shm[threadIdx.x >> 5];
+  const unsigned lane = lane_id();
+  const unsigned full = 0xffffffffu;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const int L = x.v.levels;
+  const long long tiles_per_row = x.W / 8;
+  const long long n_tiles = (x.end - x.start) / 32;
+  // totals of the rays this thread finished inside the packet
+  unsigned long long tv = 0, tt = 0, th = 0, te = 0;
+  while (true) {
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(x.tile_ticket, 1ull);
+    tk = __shfl_sync(full, tk, 0);
+    if ((long long)tk >= n_tiles) break;
+    const long long ty = (long long)tk / tiles_per_row, tx = (long long)tk - ty * tiles_per_row;
+    const long long k = x.start + (ty * 4 + (lane >> 3)) * x.W + tx * 8 + (lane & 7);
+    double o[3], d[3];
+    camera_ray(x, k, o, d);
+    Recip rd[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) rd[a] = recip_of(d[a]);
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, acc = 0.0;
+    bool any_hit = false;
+    int first_obj = -1;
+    unsigned rv = 0, rt = 0, rh = 0, re = 0;  // this ray's RaycastStats
+    // root slab (slab_box over [0,1]^3)
+    bool in_root;
+    {
+      const double zero3[3] = {0.0, 0.0, 0.0}, one3[3] = {1.0, 1.0, 1.0};
+      double t_e;
+      in_root = slab_box(o, d, zero3, one3, 0.0, inf, &t_e);
+    }
+    unsigned active = __ballot_sync(full, in_root);
+    unsigned irregular = 0;
+    int sp = 0;
+    if (active) {
+      if (lane == 0) {
+        S.node[0] = (E)0;
+        S.lanes[0] = active;
+      }
+      sp = 1;
+    }
+    __syncwarp();
+    while (sp > 0 && active) {
+      --sp;
+      const E e = S.node[sp];
+      const unsigned M = S.lanes[sp] & active;
+      __syncwarp();
+      if (!M) continue;
+      const bool on = (M >> lane) & 1u;
+      const int level = (int)(e >> SC::kShift);
+      const unsigned long long code = (unsigned long long)(e & SC::kMask);
+      if (level == L) {
+        // ---- leaf: hits in (t, index) order, shaded warp-wide
+        if (on) ++rv;
+        double bt[kPktHits];
+        int bi[kPktHits];
+        int nb = 0;
+        int left = pkt_collect<false>(x, (long long)code, on, o, d, -inf, -1, bt, bi, nb, rt);
+        if (kMode == 0 && left > 1) left = 1;
+        bool stop = false;
+        while (__any_sync(full, left > 0)) {
+          const int take = left < nb ? left : nb;
+          // lane-major slots: exclusive scan of `take`
+          int base = take;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(full, base, off);
+            if ((int)lane >= off) base += v;
+          }
+          const int total = __shfl_sync(full, base, 31);
+          base -= take;
+#pragma unroll
+          for (int q = 0; q < kPktHits; ++q)
+            if (q < take) S.slot_idx[base + q] = bi[q];
+          __syncwarp();
+          for (int r0 = 0; r0 < total; r0 += 32) {
+            const int j = r0 + (int)lane;
+            if (j < total) {
+              double col[3];
+              pkt_shade(x, S.slot_idx[j], (long long)code, col);
+              S.col[lane][0] = col[0];
+              S.col[lane][1] = col[1];
+              S.col[lane][2] = col[2];
+            }
+            __syncwarp();
+            const int q0 = base > r0 ? base : r0;
+            const int q1 = (base + take) < (r0 + 32) ? (base + take) : (r0 + 32);
+            for (int q = q0; q < q1; ++q) {
+              const int i = S.slot_idx[q];
+              ++rh;
+              if (first_obj < 0) first_obj = (int)__ldg(&x.v.obj[i]);
+              const double* col = S.col[q - r0];
+              if (kMode == 0) {
+                c0 = col[0];
+                c1 = col[1];
+                c2 = col[2];
+                acc = 1.0;
+                any_hit = true;
+                stop = true;
+              } else {
+                const double a = x.s.alpha[__ldg(&x.v.mat[i])];
+                const double tc = __dmul_rn(__dsub_rn(1.0, acc), a);
+                c0 = __dadd_rn(c0, __dmul_rn(tc, col[0]));
+                c1 = __dadd_rn(c1, __dmul_rn(tc, col[1]));
+                c2 = __dadd_rn(c2, __dmul_rn(tc, col[2]));
+                acc = __dadd_rn(acc, tc);
+                any_hit = true;
+              }
+            }
+            __syncwarp();
+          }
+          left -= take;
+          if (__any_sync(full, left > 0)) {
+            // more hits than the buffer held: the next ones above the last delivered
+            double lt2 = -inf;
+            int li2 = -1;
+#pragma unroll
+            for (int q = 0; q < kPktHits; ++q)
+              if (q == take - 1) {
+                lt2 = bt[q];
+                li2 = bi[q];
+              }
+            unsigned dummy_tested = 0;
+            const bool more = left > 0;
+            pkt_collect<true>(x, (long long)code, more, o, d, lt2, li2, bt, bi, nb, dummy_tested);
+            if (!more) nb = 0;
+          }
+        }
+        bool done = false;
+        if (on) {
+          if (stop) {
+            done = true;
+          } else if (x.cutoff >= 0.0 && acc >= x.cutoff) {
+            ++re;
+            done = true;
+          }
+        }
+        active &= ~__ballot_sync(full, done);
+        continue;
+      }
+      // ---- inner node: expand_node for every lane in M, one shared child order
+      const unsigned mask = __ldg(&x.v.pyramid[pyr_level_offset(level) + (long long)code]);
+      if (mask == 0) continue;
+      const double half = __longlong_as_double((1022LL - level) << 52);  // 0.5 / 2^level, exact
+      const double size = __dmul_rn(2.0, half);
+      double pl[3][3];
+      pl[0][0] = __dmul_rn((double)compact3(code), size);
+      pl[1][0] = __dmul_rn((double)compact3(code >> 1), size);
+      pl[2][0] = __dmul_rn((double)compact3(code >> 2), size);
+      unsigned s = 0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        pl[a][1] = __dadd_rn(pl[a][0], half);
+        pl[a][2] = __dadd_rn(pl[a][1], half);
+        const bool hi_first = x.persp ? (x.eye[a] > pl[a][1]) : (x.ff[a] < 0.0);
+        s |= (hi_first ? 1u : 0u) << a;
+      }
+      const unsigned side_lo[3] = {mask & 0x55u, mask & 0x33u, mask & 0x0Fu};
+      const unsigned side_hi[3] = {mask & 0xAAu, mask & 0xCCu, mask & 0xF0u};
+      // per axis: the child slab's entry / exit parameter for each half, in
+      // the shared order's bit (bit ^ s_a).  slab_axis's per-axis test is
+      // t0 = max(t0, entry), t1 = min(t1, exit) with entry / exit the ordered
+      // pair of the two plane parameters (d > 0: lo first); a d == 0 axis is
+      // (-inf, +inf) inside the half and (+inf, -inf) outside it (a miss).
+      double en[3][2], ex[3][2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double e0, x0, e1, x1;
+        if (d[a] == 0.0) {
+          const bool in0 = !(o[a] < pl[a][0] || o[a] > pl[a][1]);
+          const bool in1 = !(o[a] < pl[a][1] || o[a] > pl[a][2]);
+          e0 = in0 ? -inf : inf;
+          x0 = -e0;
+          e1 = in1 ? -inf : inf;
+          x1 = -e1;
+        } else {
+          const double t0 = (on && side_lo[a]) ? div_rn(__dsub_rn(pl[a][0], o[a]), rd[a]) : 0.0;
+          const double t1 = on ? div_rn(__dsub_rn(pl[a][1], o[a]), rd[a]) : 0.0;
+          const double t2 = (on && side_hi[a]) ? div_rn(__dsub_rn(pl[a][2], o[a]), rd[a]) : 0.0;
+          const bool pos = d[a] > 0.0;
+          e0 = pos ? t0 : t1;
+          x0 = pos ? t1 : t0;
+          e1 = pos ? t1 : t2;
+          x1 = pos ? t2 : t1;
+        }
+        const bool sa = (s >> a) & 1u;
+        en[a][0] = sa ? e1 : e0;
+        ex[a][0] = sa ? x1 : x0;
+        en[a][1] = sa ? e0 : e1;
+        ex[a][1] = sa ? x0 : x1;
+      }
+      // children in reverse shared order: pushed far-first, so the shared
+      // order pops next; each lane checks its own (t_enter, child) order
+      bool have_next = false, irr = false;
+      double nt = 0.0;
+      int ncc = 0;
+      const E lvl = (E)((E)(level + 1) << SC::kShift);
+      const int sp0 = sp;
+#pragma unroll
+      for (int jj = 7; jj >= 0; --jj) {
+        const int c = jj ^ (int)s;
+        if (!((mask >> c) & 1u)) continue;
+        const int jx = jj & 1, jy = (jj >> 1) & 1, jz = jj >> 2;
+        double t0 = en[0][jx] > 0.0 ? en[0][jx] : 0.0;
+        t0 = en[1][jy] > t0 ? en[1][jy] : t0;
+        t0 = en[2][jz] > t0 ? en[2][jz] : t0;
+        double t1 = ex[0][jx];
+        t1 = ex[1][jy] < t1 ? ex[1][jy] : t1;
+        t1 = ex[2][jz] < t1 ? ex[2][jz] : t1;
+        const bool hit = on && !(t0 > t1);
+        if (hit) {
+          if (have_next && !hit_less(t0, c, nt, ncc)) irr = true;
+          have_next = true;
+          nt = t0;
+          ncc = c;
+        }
+        const unsigned b = __ballot_sync(full, hit);
+        if (b) {
+          if (lane == 0) {
+            S.node[sp] = lvl | (E)(code * 8ull + (unsigned long long)c);
+            S.lanes[sp] = b;
+          }
+          ++sp;
+        }
+      }
+      const unsigned bad = __ballot_sync(full, irr);
+      if (bad) {
+        // lanes whose own (t_enter, child) order differs from the shared one
+        // (rounded entry distances tie): drop them from this node's shared
+        // pushes and push their children in their own order, one push set per
+        // group of lanes with the same order -- above the shared entries, so
+        // each group's subtrees pop first and every lane still sees exactly
+        // its own preorder (expand_node's insertion sort)
+        unsigned key = 0;
+        int nk = 0;
+        if (irr) {
+          double cte[8];
+          int cc[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int c = jj ^ (int)s;
+            if (!((mask >> c) & 1u)) continue;
+            const int jx = jj & 1, jy = (jj >> 1) & 1, jz = jj >> 2;
+            double t0 = en[0][jx] > 0.0 ? en[0][jx] : 0.0;
+            t0 = en[1][jy] > t0 ? en[1][jy] : t0;
+            t0 = en[2][jz] > t0 ? en[2][jz] : t0;
+            double t1 = ex[0][jx];
+            t1 = ex[1][jy] < t1 ? ex[1][jy] : t1;
+            t1 = ex[2][jz] < t1 ? ex[2][jz] : t1;
+            if (t0 > t1) continue;
+            int m = nk - 1;
+            while (m >= 0 && (cte[m] > t0 || (cte[m] == t0 && cc[m] > c))) {
+              cte[m + 1] = cte[m];
+              cc[m + 1] = cc[m];
+              --m;
+            }
+            cte[m + 1] = t0;
+            cc[m + 1] = c;
+            ++nk;
+          }
+          for (int q = 0; q < nk; ++q) key |= (unsigned)cc[q] << (3 * q);
+        }
+        if (lane == 0)
+          for (int q = sp0; q < sp; ++q) S.lanes[q] &= ~bad;
+        if (lane == 0) atomicAdd(x.own_order_n, (unsigned long long)__popc(bad));
+        unsigned pend = bad;
+        while (pend) {
+          const int leader = __ffs(pend) - 1;
+          const unsigned kl = __shfl_sync(full, key, leader);
+          const int nl = __shfl_sync(full, nk, leader);
+          const unsigned grp = __ballot_sync(full, ((pend >> lane) & 1u) && key == kl && nk == nl);
+          pend &= ~grp;
+          if (sp + nl > kPktStack) {  // no room: the per-ray kernel takes these rays
+            irregular |= grp;
+            active &= ~grp;
+            continue;
+          }
+          for (int q = nl - 1; q >= 0; --q) {
+            if (lane == 0) {
+              S.node[sp] = lvl | (E)(code * 8ull + (unsigned long long)((kl >> (3 * q)) & 7u));
+              S.lanes[sp] = grp;
+            }
+            ++sp;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+    const bool irr_ray = (irregular >> lane) & 1u;
+    if (irr_ray) {
+      // hand the ray to the per-ray kernel (warp-aggregated append)
+      const unsigned n_irr = __popc(irregular);
+      const int leader = __ffs(irregular) - 1;
+      unsigned long long base = 0;
+      if ((int)lane == leader) base = atomicAdd(x.ray_list_n, (unsigned long long)n_irr);
+      base = __shfl_sync(irregular, base, leader);
+      x.ray_list[base + __popc(irregular & ((1u << lane) - 1u))] = k;
+    } else {
+      tv += rv;
+      tt += rt;
+      th += rh;
+      te += re;
+      double4 px;
+      if (kMode == 0) {
+        px = any_hit ? make_double4(c0, c1, c2, 1.0) : make_double4(x.bg[0], x.bg[1], x.bg[2], x.bg[3]);
+      } else {
+        const double ra = __dsub_rn(1.0, acc);
+        px.x = __dadd_rn(c0, __dmul_rn(__dmul_rn(ra, x.bg[3]), x.bg[0]));
+        px.y = __dadd_rn(c1, __dmul_rn(__dmul_rn(ra, x.bg[3]), x.bg[1]));
+        px.z = __dadd_rn(c2, __dmul_rn(__dmul_rn(ra, x.bg[3]), x.bg[2]));
+        px.w = __dadd_rn(acc, __dmul_rn(ra, x.bg[3]));
+      }
+      reinterpret_cast<double4*>(x.out_rgba)[k] = px;
+      if (x.out_ids && first_obj >= 0) x.out_ids[k] = (int32_t)first_obj;
+    }
+    __syncwarp();
+  }
+  unsigned long long v[4] = {tv, tt, th, te};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_xor_sync(full, v[q], off);
+  }
+  if (lane == 0) {
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (v[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&x.counters[q]), v[q]);
@@ -681,11 +1141,55 @@ inline int grid_for(long long n, int block, int per_sm = 16) {
   return (int)g;
 }
 
+#ifndef FHV_RAY_PACKET
+#define FHV_RAY_PACKET 1  // 0: per-ray kernel only (experiment switch)
+#endif
+
+// camera rays of modes 0 / 1 over whole 4-row strips of a width divisible by
+// 8: packet kernel, then the per-ray kernel over the rays it handed off
+template <class E>
+int launch_packet(fhv_ctx* ctx, RayParams& x, cudaStream_t st) {
+  const long long n = x.end - x.start;
+  // [0] rays handed off, [1] hand-off kernel ticket, [2] own-order (lane, node) pairs, [3..] the list
+  auto* buf = (unsigned long long*)scratch(ctx, kRays, (size_t)(3 + n) * 8);
+  if (!buf) return FHV_NOMEM;
+  x.ray_list_n = buf;
+  x.own_order_n = buf + 2;
+  x.ray_list = (long long*)(buf + 3);
+  int rc = check_cuda(ctx, cudaMemsetAsync(buf, 0, 3 * sizeof(unsigned long long), st));
+  if (rc) return rc;
+  {
+    LaunchScope L_(ctx, kStRaycast, st);
+    const int g = grid_for(n / 32, kPktWarps, 16);
+    if (x.mode == 0)
+      k_raycast_packet<0, E><<<g, 32 * kPktWarps, 0, st>>>(x);
+    else
+      k_raycast_packet<1, E><<<g, 32 * kPktWarps, 0, st>>>(x);
+  }
+  if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  RayParams y = x;
+  y.tile_ticket = buf + 1;
+  {
+    LaunchScope L_(ctx, kStRaycastHandoff, st);
+    if (x.mode == 0)
+      k_raycast<0, E><<<148, 128, 0, st>>>(y);
+    else
+      k_raycast<1, E><<<148, 128, 0, st>>>(y);
+  }
+  return check_cuda(ctx, cudaGetLastError());
+}
+
 int launch(fhv_ctx* ctx, RayParams& x, void* stream) {
   if (x.end <= x.start) return FHV_OK;
   x.tile_ticket = &ctx->ctl->spare[3];
   int rc = check_cuda(ctx, cudaMemsetAsync(x.tile_ticket, 0, sizeof(unsigned long long), (cudaStream_t)stream));
   if (rc) return rc;
+  const bool packet = FHV_RAY_PACKET && x.from_camera && x.mode < 2 && x.W % 8 == 0 && x.start % (4 * x.W) == 0 &&
+                      x.end % (4 * x.W) == 0;
+  if (packet) {
+    if (x.v.levels <= 9) return launch_packet<uint32_t>(ctx, x, (cudaStream_t)stream);
+    return launch_packet<unsigned long long>(ctx, x, (cudaStream_t)stream);
+  }
   {
     LaunchScope L_(ctx, kStRaycast, (cudaStream_t)stream);
     const int g = grid_for(x.end - x.start, 128);

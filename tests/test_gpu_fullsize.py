@@ -119,6 +119,38 @@ def test_c2_full_size_pofl_and_raycast_band():
     assert np.max(np.abs(got - want)) <= 1e-12
 
 
+@pytest.mark.parametrize("mode", ("transparency", "opaque_nearest"))
+def test_c2_packet_raycast_tie_rays(mode):
+    """The C2 view's image-diagonal rays (eye at y = z = 0.5: d_y == -d_z
+    exactly) cross two centre planes at the same rounded t, so their own
+    (t_enter, child) order differs from the packet's shared child order at
+    those nodes: the packet kernel must push their children in their own order
+    (fhv/_ckern.pyx:580-632) -- image, ids and RaycastStats equal the oracle's,
+    and no ray is handed to the per-ray kernel."""
+    import dataclasses
+    s = _scene("spheres100k")
+    cfg = _cfg1080(s)
+    ns = fhv.CaptureStrategy.normal_space()
+    gpu = fhv.build_pofl(s, ns, cfg, 8, exact_order=True)
+    ref = orc.build_pofl(s, ns, cfg, 8)
+    view = viewpoint_camera("+x", (1920, 1080), "perspective")
+    lights = [headlight(view)]
+    rc = dataclasses.replace(fhv.default_raycast_config(gpu), mode=mode)
+    band = (220, 272)  # holds image-diagonal tie rays (rows 221-270 at columns 710-770)
+    img, st, ids = fhv.render_raycast(gpu, view, lights, rc, rows=band, collect_ids=True)
+    handed, own = _lib.raycast_diag(gpu.pool.device)
+    orgba, ost, oids = orc.raycast(ref, view, lights, rc.splat_radius_world, mode=mode, materials=s.materials,
+                                   rows=band, collect_ids=True)
+    got = img.pixels.cpu().numpy().reshape(-1, 4)[band[0] * 1920:band[1] * 1920]
+    want = orgba.reshape(-1, 4)[band[0] * 1920:band[1] * 1920]
+    assert st.as_dict() == ost
+    assert np.max(np.abs(got - want)) <= 1e-12
+    gi = ids.cpu().numpy().reshape(-1)[band[0] * 1920:band[1] * 1920]
+    assert np.array_equal(gi, np.asarray(oids).reshape(-1)[band[0] * 1920:band[1] * 1920])
+    assert own > 0, "the band's tie rays never took their own child order"
+    assert handed == 0
+
+
 def test_c4_depth_complex_ppfl_vs_pofa():
     s = _scene("layers80")
     res = 1080
