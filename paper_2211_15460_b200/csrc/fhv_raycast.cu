@@ -331,8 +331,11 @@ __device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats
   const double shin = x.s.shininess[m];
   double v[3] = {__dsub_rn(x.eye[0], p[0]), __dsub_rn(x.eye[1], p[1]), __dsub_rn(x.eye[2], p[2])};
   const double vl = __dsqrt_rn(plain3(v[0], v[1], v[2]));
+  // one reciprocal per normalised vector, each quotient still __ddiv_rn's
+  // (fhv_common.cuh div_rn)
+  const Recip rvl = recip_of(vl);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) v[k] = vl > 0.0 ? ddiv_z(v[k], vl) : 0.0;
+  for (int k = 0; k < 3; ++k) v[k] = vl > 0.0 ? div_rn(v[k], rvl) : 0.0;
   double r = 0.0, g = 0.0, b = 0.0;
   for (int li = 0; li < x.s.n_lights; ++li) {
     double l[3];
@@ -343,13 +346,15 @@ __device__ void shade_hit(const RayParams& x, long long i, long long leaf, Stats
 #pragma unroll
       for (int k = 0; k < 3; ++k) l[k] = __dsub_rn(x.s.light_vec[3 * li + k], p[k]);
       const double ll = __dsqrt_rn(plain3(l[0], l[1], l[2]));
+      const Recip rll = recip_of(ll);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) l[k] = ll > 0.0 ? ddiv_z(l[k], ll) : 0.0;
+      for (int k = 0; k < 3; ++k) l[k] = ll > 0.0 ? div_rn(l[k], rll) : 0.0;
     }
     double h[3] = {__dadd_rn(l[0], v[0]), __dadd_rn(l[1], v[1]), __dadd_rn(l[2], v[2])};
     const double hl = __dsqrt_rn(plain3(h[0], h[1], h[2]));
+    const Recip rhl = recip_of(hl);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) h[k] = hl > 0.0 ? ddiv_z(h[k], hl) : 0.0;
+    for (int k = 0; k < 3; ++k) h[k] = hl > 0.0 ? div_rn(h[k], rhl) : 0.0;
     double ndl = __dadd_rn(__dadd_rn(__dmul_rn(n[0], l[0]), __dmul_rn(n[1], l[1])), __dmul_rn(n[2], l[2]));
     if (ndl < 0.0) ndl = 0.0;
     double ndh = __dadd_rn(__dadd_rn(__dmul_rn(n[0], h[0]), __dmul_rn(n[1], h[1])), __dmul_rn(n[2], h[2]));
@@ -537,6 +542,10 @@ __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
 #define FHV_PKT_MINB 4
 #endif
 constexpr int kPktHits = FHV_PKT_HITS;
+#ifndef FHV_PKT_BUF
+#define FHV_PKT_BUF 12  // deferred (pool index, weight) records per lane before a shading flush
+#endif
+constexpr int kPktBuf = FHV_PKT_BUF;
 constexpr int kPktWarps = 4;  // 128-thread CTAs
 
 // shared stack: 7 per level for the shared order plus room for the lanes
@@ -547,9 +556,24 @@ template <class E>
 struct PktShared {
   E node[kPktStack];
   unsigned lanes[kPktStack];
-  int slot_idx[32 * kPktHits];
+  int slot_idx[32 * kPktBuf];
   double col[32][3];
+  int ri[kPktBuf][32];     // each lane's delivered hits in order: pool index ...
+  double rw[kPktBuf][32];  // ... and compositing weight (1 - acc) * alpha
 };
+
+// a leaf's fragments in pool order (POFA range) or chain order (POFL);
+// warp-uniform walk
+template <class F>
+__device__ __forceinline__ void pkt_for_leaf(const RayParams& x, long long code, F&& f) {
+  if (x.v.layout == 0) {
+    const int beg = (int)__ldg(&x.v.offsets[code]);
+    const int cnt = (int)__ldg(&x.v.counts[code]);
+    for (int k = beg; k < beg + cnt; ++k) f(k);
+  } else {
+    for (int k = __ldg(&x.v.heads[code]); k >= 0; k = __ldg(&x.v.prev[k])) f(k);
+  }
+}
 
 // sorted insertion into the register buffer (compile-time indices only: the
 // candidate walks up, swapping with every larger entry; the largest falls off)
@@ -622,6 +646,51 @@ void pkt_shade(const RayParams& x, int i, long long leaf, double col[3]) {
   shade_hit<1, uint32_t>(x, i, leaf, dummy, col);  // modes 0 / 1: no shadow traversal
 }
 
+// shade every lane's queued records warp-wide (lane-major slots, one slot
+// per lane per round) and composite each lane's in queue order
+template <int kMode, class Sh>
+__device__ __forceinline__ void pkt_flush(const RayParams& x, Sh& S, int& nbuf, double& c0, double& c1, double& c2) {
+  const unsigned full = 0xffffffffu, lane = lane_id();
+  int base = nbuf;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(full, base, off);
+    if ((int)lane >= off) base += v;
+  }
+  const int total = __shfl_sync(full, base, 31);
+  base -= nbuf;
+  for (int q = 0; q < nbuf; ++q) S.slot_idx[base + q] = S.ri[q][lane];
+  __syncwarp();
+  for (int r0 = 0; r0 < total; r0 += 32) {
+    const int j = r0 + (int)lane;
+    if (j < total) {
+      double col[3];
+      pkt_shade(x, S.slot_idx[j], -1, col);
+      S.col[lane][0] = col[0];
+      S.col[lane][1] = col[1];
+      S.col[lane][2] = col[2];
+    }
+    __syncwarp();
+    const int q0 = base > r0 ? base : r0;
+    const int q1 = (base + nbuf) < (r0 + 32) ? (base + nbuf) : (r0 + 32);
+    for (int q = q0; q < q1; ++q) {
+      const double* col = S.col[q - r0];
+      if (kMode == 0) {
+        c0 = col[0];
+        c1 = col[1];
+        c2 = col[2];
+      } else {
+        const double tc = S.rw[q - base][lane];
+        c0 = __dadd_rn(c0, __dmul_rn(tc, col[0]));
+        c1 = __dadd_rn(c1, __dmul_rn(tc, col[1]));
+        c2 = __dadd_rn(c2, __dmul_rn(tc, col[2]));
+      }
+    }
+    __syncwarp();
+  }
+  nbuf = 0;
+}
+
 template <int kMode, class E>
 __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet(RayParams x) {
   using SC = StackCodec<E>;
@@ -651,6 +720,7 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
     bool any_hit = false;
     int first_obj = -1;
     unsigned rv = 0, rt = 0, rh = 0, re = 0;  // this ray's RaycastStats
+    int nbuf = 0;                             // queued (index, weight) records
     // root slab (slab_box over [0,1]^3)
     bool in_root;
     {
@@ -669,7 +739,9 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
       sp = 1;
     }
     __syncwarp();
-    while (sp > 0 && active) {
+    bool need_flush = false;
+    while (true) {
+    while (sp > 0 && active && !need_flush) {
       --sp;
       const E e = S.node[sp];
       const unsigned M = S.lanes[sp] & active;
@@ -683,77 +755,71 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
         if (on) ++rv;
         double bt[kPktHits];
         int bi[kPktHits];
-        int nb = 0;
-        int left = pkt_collect<false>(x, (long long)code, on, o, d, -inf, -1, bt, bi, nb, rt);
-        if (kMode == 0 && left > 1) left = 1;
-        bool stop = false;
-        while (__any_sync(full, left > 0)) {
-          const int take = left < nb ? left : nb;
-          // lane-major slots: exclusive scan of `take`
-          int base = take;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const int v = __shfl_up_sync(full, base, off);
-            if ((int)lane >= off) base += v;
-          }
-          const int total = __shfl_sync(full, base, 31);
-          base -= take;
-#pragma unroll
-          for (int q = 0; q < kPktHits; ++q)
-            if (q < take) S.slot_idx[base + q] = bi[q];
-          __syncwarp();
-          for (int r0 = 0; r0 < total; r0 += 32) {
-            const int j = r0 + (int)lane;
-            if (j < total) {
-              double col[3];
-              pkt_shade(x, S.slot_idx[j], (long long)code, col);
-              S.col[lane][0] = col[0];
-              S.col[lane][1] = col[1];
-              S.col[lane][2] = col[2];
+        int nb = 0, left;
+        if (kMode == 0) {
+          // the nearest hit only
+          int nh = 0;
+          pkt_for_leaf(x, (long long)code, [&](int k) {
+            if (!on) return;
+            ++rt;
+            double t;
+            if (!hit_test(x, k, o, d, 0.0, inf, &t)) return;
+            if (nh++ == 0 || hit_less(t, k, bt[0], bi[0])) {
+              bt[0] = t;
+              bi[0] = k;
             }
-            __syncwarp();
-            const int q0 = base > r0 ? base : r0;
-            const int q1 = (base + take) < (r0 + 32) ? (base + take) : (r0 + 32);
-            for (int q = q0; q < q1; ++q) {
-              const int i = S.slot_idx[q];
+          });
+          left = nb = nh > 0 ? 1 : 0;
+        } else {
+          left = pkt_collect<false>(x, (long long)code, on, o, d, -inf, -1, bt, bi, nb, rt);
+        }
+        // deliver in (t, index) order: the weight (1 - acc) * alpha and acc
+        // need only the materials' alphas, so shading is deferred -- the
+        // (index, weight) records queue per lane and are shaded warp-wide
+        // at flushes (pkt_flush), composited in the same order
+        bool stop = false;
+        while (true) {
+          const int take = left < nb ? left : nb;
+#pragma unroll
+          for (int q = 0; q < kPktHits; ++q) {
+            if (q < take) {
+              const int i = bi[q];
               ++rh;
               if (first_obj < 0) first_obj = (int)__ldg(&x.v.obj[i]);
-              const double* col = S.col[q - r0];
+              any_hit = true;
+              S.ri[nbuf][lane] = i;
               if (kMode == 0) {
-                c0 = col[0];
-                c1 = col[1];
-                c2 = col[2];
                 acc = 1.0;
-                any_hit = true;
                 stop = true;
               } else {
                 const double a = x.s.alpha[__ldg(&x.v.mat[i])];
                 const double tc = __dmul_rn(__dsub_rn(1.0, acc), a);
-                c0 = __dadd_rn(c0, __dmul_rn(tc, col[0]));
-                c1 = __dadd_rn(c1, __dmul_rn(tc, col[1]));
-                c2 = __dadd_rn(c2, __dmul_rn(tc, col[2]));
                 acc = __dadd_rn(acc, tc);
-                any_hit = true;
+                S.rw[nbuf][lane] = tc;
               }
+              ++nbuf;
             }
-            __syncwarp();
           }
           left -= take;
-          if (__any_sync(full, left > 0)) {
-            // more hits than the buffer held: the next ones above the last delivered
-            double lt2 = -inf;
-            int li2 = -1;
-#pragma unroll
-            for (int q = 0; q < kPktHits; ++q)
-              if (q == take - 1) {
-                lt2 = bt[q];
-                li2 = bi[q];
-              }
-            unsigned dummy_tested = 0;
-            const bool more = left > 0;
-            pkt_collect<true>(x, (long long)code, more, o, d, lt2, li2, bt, bi, nb, dummy_tested);
-            if (!more) nb = 0;
+          if (__any_sync(full, nbuf > kPktBuf - kPktHits)) {
+            if (kMode == 0 || !__any_sync(full, left > 0)) {
+              need_flush = true;  // flushed by the traversal loop's single flush site
+              break;
+            }
+            pkt_flush<kMode>(x, S, nbuf, c0, c1, c2);  // mid-leaf (a ray with more hits than the buffer)
           }
+          if (kMode == 0 || !__any_sync(full, left > 0)) break;
+          // more hits than the buffer held: the next ones above the last delivered
+          double lt = -inf;
+          int li = -1;
+#pragma unroll
+          for (int q = 0; q < kPktHits; ++q)
+            if (q == take - 1) {
+              lt = bt[q];
+              li = bi[q];
+            }
+          unsigned dummy_tested = 0;
+          pkt_collect<true>(x, (long long)code, left > 0, o, d, lt, li, bt, bi, nb, dummy_tested);
         }
         bool done = false;
         if (on) {
@@ -916,6 +982,10 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
       __syncwarp();
     }
     __syncwarp();
+    if (__any_sync(full, nbuf > 0)) pkt_flush<kMode>(x, S, nbuf, c0, c1, c2);
+    if (!need_flush) break;
+    need_flush = false;
+    }
     const bool irr_ray = (irregular >> lane) & 1u;
     if (irr_ray) {
       // hand the ray to the per-ray kernel (warp-aggregated append)
