@@ -691,6 +691,59 @@ __device__ __forceinline__ void pkt_flush(const RayParams& x, Sh& S, int& nbuf, 
   nbuf = 0;
 }
 
+// one inner node for one ray, exactly as expand_node (fhv/_ckern.pyx:580-632):
+// bits 0-7 the children hit, bit 8 set when their (t_enter, child) order is
+// not the shared order s, bits 9-12 their count, bits 13.. the children in
+// that order (3 bits each).  Out of line: the packet kernel's rare path.
+__device__ __noinline__ unsigned long long exact_node(double o0, double o1, double o2, double d0, double d1,
+                                                      double d2, int level, unsigned long long code, unsigned mask,
+                                                      unsigned s) {
+  const double o[3] = {o0, o1, o2}, d[3] = {d0, d1, d2};
+  const double half = __longlong_as_double((1022LL - level) << 52);
+  const double size = __dmul_rn(2.0, half);
+  double pl[3][3], tp[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    pl[a][0] = __dmul_rn((double)compact3(code >> a), size);
+    pl[a][1] = __dadd_rn(pl[a][0], half);
+    pl[a][2] = __dadd_rn(pl[a][1], half);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) tp[a][k] = d[a] != 0.0 ? ddiv_z(__dsub_rn(pl[a][k], o[a]), d[a]) : 0.0;
+  }
+  double cte[8];
+  int cc[8];
+  int nc = 0;
+  unsigned hits = 0;
+  for (int c = 0; c < 8; ++c) {
+    if (!((mask >> c) & 1u)) continue;
+    double t0 = 0.0, t1 = __longlong_as_double(0x7ff0000000000000ll);
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int bit = (c >> a) & 1;
+      if (ok) ok = slab_axis(o[a], d[a], pl[a][bit], pl[a][bit + 1], tp[a][bit], tp[a][bit + 1], t0, t1);
+    }
+    if (!ok || t0 > t1) continue;
+    hits |= 1u << c;
+    int m = nc - 1;
+    while (m >= 0 && (cte[m] > t0 || (cte[m] == t0 && cc[m] > c))) {
+      cte[m + 1] = cte[m];
+      cc[m + 1] = cc[m];
+      --m;
+    }
+    cte[m + 1] = t0;
+    cc[m + 1] = c;
+    ++nc;
+  }
+  unsigned long long seq = 0;
+  bool irr = false;
+  for (int q = 0; q < nc; ++q) {
+    seq |= (unsigned long long)cc[q] << (3 * q);
+    if (q > 0 && ((unsigned)cc[q] ^ s) < ((unsigned)cc[q - 1] ^ s)) irr = true;
+  }
+  return (unsigned long long)hits | ((unsigned long long)irr << 8) | ((unsigned long long)nc << 9) | (seq << 13);
+}
+
 template <int kMode, class E>
 __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet(RayParams x) {
   using SC = StackCodec<E>;
@@ -713,9 +766,20 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
     const long long k = x.start + (ty * 4 + (lane >> 3)) * x.W + tx * 8 + (lane & 7);
     double o[3], d[3];
     camera_ray(x, k, o, d);
-    Recip rd[3];
+    // certified f32 slab parameters: t(pl) ~ fma(pl, inv32, c32) with
+    // inv32 = 1/d (two f32 roundings), c32 = -o * inv32 (one): for pl in
+    // [0, 1], |t - t_exact| <= 2^-23 |t| + 2^-24 (|t| + |c32|) <= e32; a
+    // lane with a zero direction component takes exact_node at every node
+    float inv32[3], c32[3], e32 = 0.0f;
+    bool lane_exact = false;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) rd[a] = recip_of(d[a]);
+    for (int a = 0; a < 3; ++a) {
+      lane_exact = lane_exact || d[a] == 0.0;
+      inv32[a] = __frcp_rn((float)d[a]);
+      c32[a] = (float)__dmul_rn(-o[a], (double)inv32[a]);
+      e32 = fmaxf(e32, 0x1.0p-22f * (fabsf(inv32[a]) + fabsf(c32[a])));
+    }
+    lane_exact = lane_exact || !(e32 < 0x1.0p-8f);  // huge / non-finite parameters
     double c0 = 0.0, c1 = 0.0, c2 = 0.0, acc = 0.0;
     bool any_hit = false;
     int first_obj = -1;
@@ -836,80 +900,87 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
       // ---- inner node: expand_node for every lane in M, one shared child order
       const unsigned mask = __ldg(&x.v.pyramid[pyr_level_offset(level) + (long long)code]);
       if (mask == 0) continue;
-      const double half = __longlong_as_double((1022LL - level) << 52);  // 0.5 / 2^level, exact
-      const double size = __dmul_rn(2.0, half);
-      double pl[3][3];
-      pl[0][0] = __dmul_rn((double)compact3(code), size);
-      pl[1][0] = __dmul_rn((double)compact3(code >> 1), size);
-      pl[2][0] = __dmul_rn((double)compact3(code >> 2), size);
+      // shared order: the eye's (perspective) / the rays' entry (orthographic)
+      // side of each centre plane; any choice is exact (each lane checks it)
+      const float half32 = __int_as_float((126 - level) << 23);  // 0.5 / 2^level, exact
+      const float size32 = 2.0f * half32;
+      float pl[3][3];
       unsigned s = 0;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        pl[a][1] = __dadd_rn(pl[a][0], half);
-        pl[a][2] = __dadd_rn(pl[a][1], half);
-        const bool hi_first = x.persp ? (x.eye[a] > pl[a][1]) : (x.ff[a] < 0.0);
+        pl[a][0] = (float)compact3(code >> a) * size32;  // exact: dyadic, < 2^24 units of 2^-level
+        pl[a][1] = pl[a][0] + half32;
+        pl[a][2] = pl[a][1] + half32;
+        const bool hi_first = x.persp ? ((float)x.eye[a] > pl[a][1]) : (x.ff[a] < 0.0);
         s |= (hi_first ? 1u : 0u) << a;
       }
-      const unsigned side_lo[3] = {mask & 0x55u, mask & 0x33u, mask & 0x0Fu};
-      const unsigned side_hi[3] = {mask & 0xAAu, mask & 0xCCu, mask & 0xF0u};
-      // per axis: the child slab's entry / exit parameter for each half, in
-      // the shared order's bit (bit ^ s_a).  slab_axis's per-axis test is
-      // t0 = max(t0, entry), t1 = min(t1, exit) with entry / exit the ordered
-      // pair of the two plane parameters (d > 0: lo first); a d == 0 axis is
-      // (-inf, +inf) inside the half and (+inf, -inf) outside it (a miss).
-      double en[3][2], ex[3][2];
+      // this lane's children from the certified f32 slab parameters (within
+      // e32 of expand_node's f64 values); decisions closer than the margin --
+      // and lanes with a d == 0 axis -- take exact_node
+      unsigned hits = 0, seq = 0;
+      int nk = 0;
+      bool irr = false;
+      if (on) {
+        bool unsure = lane_exact;
+        if (!unsure) {
+          float en[3][2], ex[3][2];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        double e0, x0, e1, x1;
-        if (d[a] == 0.0) {
-          const bool in0 = !(o[a] < pl[a][0] || o[a] > pl[a][1]);
-          const bool in1 = !(o[a] < pl[a][1] || o[a] > pl[a][2]);
-          e0 = in0 ? -inf : inf;
-          x0 = -e0;
-          e1 = in1 ? -inf : inf;
-          x1 = -e1;
-        } else {
-          const double t0 = (on && side_lo[a]) ? div_rn(__dsub_rn(pl[a][0], o[a]), rd[a]) : 0.0;
-          const double t1 = on ? div_rn(__dsub_rn(pl[a][1], o[a]), rd[a]) : 0.0;
-          const double t2 = (on && side_hi[a]) ? div_rn(__dsub_rn(pl[a][2], o[a]), rd[a]) : 0.0;
-          const bool pos = d[a] > 0.0;
-          e0 = pos ? t0 : t1;
-          x0 = pos ? t1 : t0;
-          e1 = pos ? t1 : t2;
-          x1 = pos ? t2 : t1;
+          for (int a = 0; a < 3; ++a) {
+            const float t0 = __fmaf_rn(pl[a][0], inv32[a], c32[a]);
+            const float t1 = __fmaf_rn(pl[a][1], inv32[a], c32[a]);
+            const float t2 = __fmaf_rn(pl[a][2], inv32[a], c32[a]);
+            const bool pos = inv32[a] > 0.0f;
+            const float e0 = pos ? t0 : t1, x0 = pos ? t1 : t0, e1 = pos ? t1 : t2, x1 = pos ? t2 : t1;
+            const bool sa = (s >> a) & 1u;
+            en[a][0] = sa ? e1 : e0;
+            ex[a][0] = sa ? x1 : x0;
+            en[a][1] = sa ? e0 : e1;
+            ex[a][1] = sa ? x0 : x1;
+          }
+          const float m2 = 2.5f * e32;  // two approximations, each within e32
+          bool have_next = false;
+          float nt = 0.0f;
+#pragma unroll
+          for (int jj = 7; jj >= 0; --jj) {
+            const int c = jj ^ (int)s;
+            if (!((mask >> c) & 1u)) continue;
+            const int jx = jj & 1, jy = (jj >> 1) & 1, jz = jj >> 2;
+            const float t0 = fmaxf(fmaxf(fmaxf(0.0f, en[0][jx]), en[1][jy]), en[2][jz]);
+            const float t1 = fminf(fminf(ex[0][jx], ex[1][jy]), ex[2][jz]);
+            const float gap = t1 - t0;
+            if (gap > m2) {
+              hits |= 1u << c;
+              if (have_next) {
+                const float dn = nt - t0;
+                if (!(dn > m2)) {
+                  if (dn < -m2) irr = true;
+                  else unsure = true;
+                }
+              }
+              have_next = true;
+              nt = t0;
+            } else if (!(gap < -m2)) {
+              unsure = true;  // NaN / inf included
+            }
+          }
         }
-        const bool sa = (s >> a) & 1u;
-        en[a][0] = sa ? e1 : e0;
-        ex[a][0] = sa ? x1 : x0;
-        en[a][1] = sa ? e0 : e1;
-        ex[a][1] = sa ? x0 : x1;
+        if (unsure || irr) {
+          const unsigned long long r = exact_node(o[0], o[1], o[2], d[0], d[1], d[2], level, code, mask, s);
+          hits = (unsigned)(r & 0xffu);
+          irr = (r >> 8) & 1u;
+          nk = (int)((r >> 9) & 0xfu);
+          seq = (unsigned)(r >> 13);
+        }
       }
       // children in reverse shared order: pushed far-first, so the shared
-      // order pops next; each lane checks its own (t_enter, child) order
-      bool have_next = false, irr = false;
-      double nt = 0.0;
-      int ncc = 0;
+      // order pops next
       const E lvl = (E)((E)(level + 1) << SC::kShift);
       const int sp0 = sp;
 #pragma unroll
       for (int jj = 7; jj >= 0; --jj) {
         const int c = jj ^ (int)s;
         if (!((mask >> c) & 1u)) continue;
-        const int jx = jj & 1, jy = (jj >> 1) & 1, jz = jj >> 2;
-        double t0 = en[0][jx] > 0.0 ? en[0][jx] : 0.0;
-        t0 = en[1][jy] > t0 ? en[1][jy] : t0;
-        t0 = en[2][jz] > t0 ? en[2][jz] : t0;
-        double t1 = ex[0][jx];
-        t1 = ex[1][jy] < t1 ? ex[1][jy] : t1;
-        t1 = ex[2][jz] < t1 ? ex[2][jz] : t1;
-        const bool hit = on && !(t0 > t1);
-        if (hit) {
-          if (have_next && !hit_less(t0, c, nt, ncc)) irr = true;
-          have_next = true;
-          nt = t0;
-          ncc = c;
-        }
-        const unsigned b = __ballot_sync(full, hit);
+        const unsigned b = __ballot_sync(full, (hits >> c) & 1u);
         if (b) {
           if (lane == 0) {
             S.node[sp] = lvl | (E)(code * 8ull + (unsigned long long)c);
@@ -922,39 +993,11 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
       if (bad) {
         // lanes whose own (t_enter, child) order differs from the shared one
         // (rounded entry distances tie): drop them from this node's shared
-        // pushes and push their children in their own order, one push set per
-        // group of lanes with the same order -- above the shared entries, so
-        // each group's subtrees pop first and every lane still sees exactly
-        // its own preorder (expand_node's insertion sort)
-        unsigned key = 0;
-        int nk = 0;
-        if (irr) {
-          double cte[8];
-          int cc[8];
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const int c = jj ^ (int)s;
-            if (!((mask >> c) & 1u)) continue;
-            const int jx = jj & 1, jy = (jj >> 1) & 1, jz = jj >> 2;
-            double t0 = en[0][jx] > 0.0 ? en[0][jx] : 0.0;
-            t0 = en[1][jy] > t0 ? en[1][jy] : t0;
-            t0 = en[2][jz] > t0 ? en[2][jz] : t0;
-            double t1 = ex[0][jx];
-            t1 = ex[1][jy] < t1 ? ex[1][jy] : t1;
-            t1 = ex[2][jz] < t1 ? ex[2][jz] : t1;
-            if (t0 > t1) continue;
-            int m = nk - 1;
-            while (m >= 0 && (cte[m] > t0 || (cte[m] == t0 && cc[m] > c))) {
-              cte[m + 1] = cte[m];
-              cc[m + 1] = cc[m];
-              --m;
-            }
-            cte[m + 1] = t0;
-            cc[m + 1] = c;
-            ++nk;
-          }
-          for (int q = 0; q < nk; ++q) key |= (unsigned)cc[q] << (3 * q);
-        }
+        // pushes and push their children in their own order (exact_node's
+        // insertion sort), one push set per group of lanes with the same
+        // order -- above the shared entries, so each group's subtrees pop
+        // first and every lane still sees exactly its own preorder
+        const unsigned key = seq;
         if (lane == 0)
           for (int q = sp0; q < sp; ++q) S.lanes[q] &= ~bad;
         if (lane == 0) atomicAdd(x.own_order_n, (unsigned long long)__popc(bad));
