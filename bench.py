@@ -303,19 +303,49 @@ def extra_config(args):
         vol0 = fhv.build_pofl(scene, ns, cfg, 8, device=dev)
         rcfg = fhv.default_raycast_config(vol0)
 
+        n0 = vol0.pool.next_free
+        acc2 = torch.zeros(2, dtype=torch.int64, device=dev)
+        tk2 = torch.zeros(4, dtype=torch.int64).pin_memory()
+
         def step():
-            vol = fhv.build_pofl(scene, ns, cfg, 8, device=dev)
+            # asynchronous POFL build (no host wait; its ticket checked on the
+            # device) and the ray cast of the same stream
+            vol = fhv.build_pofl(scene, ns, cfg, 8, device=dev, sync=False, ticket=tk2)
+            _lib.check(_lib.load().fhv_ticket_accumulate(_lib.ctx(dev), int(n0), _lib.ptr(acc2),
+                                                         _lib.stream_ptr(dev)), "ticket")
             buf.pixels.zero_()
             img, st = fhv.render_raycast(vol, view, lights, rcfg, out=buf, sync=False, shading=sh)
             return vol, st
         for _ in range(args.warmup):
             step()
+        torch.cuda.synchronize()
+        g2 = None
+        if not args.no_graph:  # the step captured once in a CUDA graph and replayed
+            gs2 = torch.cuda.Stream(dev)
+            with torch.cuda.stream(gs2):
+                for _ in range(2):
+                    step()
+            torch.cuda.synchronize()
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2, stream=gs2):
+                g_out = step()
+            torch.cuda.synchronize()
+            g2.replay()
+            torch.cuda.synchronize()
+        acc2.zero_()
         with ClockSampler(0) as clk:
-            ms, (vol, st) = _timed(step, args.steps, stream)
+            if g2 is not None:
+                ms, _ = _timed(g2.replay, args.steps, stream)
+                vol, st = g_out
+            else:
+                ms, (vol, st) = _timed(step, args.steps, stream)
+        bad2, checked2 = (int(v) for v in acc2.cpu().tolist())
+        if bad2 or checked2 != args.steps:
+            raise RuntimeError(f"C2 steps: build ticket status {bad2}, {checked2}/{args.steps} checked")
         stats = fhv.RaycastStats(*st.counters.cpu().tolist())
-        n = vol.pool.next_free
+        n = n0
         stage, prof = _stage_profile(step, args.steps, dev)
-        t_ray = stage.get("raycast", 0.0)
+        t_ray = stage.get("raycast", 0.0) + stage.get("raycast_handoff", 0.0)  # packet + per-ray hand-off kernels
         P = 1920 * 1080
         rb = ray_bytes(stats, P)
         line.update({"value": n / (ms / 1e3), "unit": "frag/s", "ms_per_step": ms,
@@ -327,7 +357,11 @@ def extra_config(args):
                      "roofline": {"bound": "hbm", "kernel": "raycast", "achieved": round(rb / (t_ray / 1e3) / 1e9, 1),
                                   "peak": peak, "unit": "GB/s", "frac": round(rb / (t_ray / 1e3) / 1e9 / peak, 4),
                                   "traffic": None, "algorithmic_bytes": rb, "peak_kind": peak_kind,
-                                  "note": "latency/divergence bound (f64 slab DFS), see profiles/"},
+                                  "note": "packet traversal, latency bound (register-limited occupancy), see "
+                                          "profiles/"},
+                     "host": ("CUDA-graph replays of one captured step (asynchronous POFL build + ray cast), every "
+                              "build ticket checked on the device" if g2 is not None else
+                              "Python-enqueued asynchronous steps, build tickets checked on the device"),
                      "clocks": clk.summary()})
         if not args.no_cpu_baseline:
             from oracle import oracle as orc
@@ -358,8 +392,41 @@ def extra_config(args):
         for _ in range(args.warmup):
             step_pofa()
             step_ppfl()
+        # the POFA step as C3 times it: the asynchronous build (pool sized by
+        # the last exact total, no host wait) captured once in a CUDA graph
+        # and replayed; every replay's build ticket is checked on the device
+        ds4 = device_scene(scene, dev)
+        acc4 = torch.zeros(2, dtype=torch.int64, device=dev)
+        tk4 = torch.zeros(4, dtype=torch.int64).pin_memory()
+        gs4 = torch.cuda.Stream(dev)
+
+        def step_pofa_async():
+            v = fhv.pofa_build(scene, one, cfg, 8, device=dev, tris=ds4, sync=False, ticket=tk4)
+            _lib.check(_lib.load().fhv_ticket_accumulate(_lib.ctx(dev), int(n), _lib.ptr(acc4),
+                                                         _lib.stream_ptr(dev)), "ticket")
+            return v
+        g4 = None
+        if not args.no_graph:
+            with torch.cuda.stream(gs4):
+                for _ in range(2):
+                    step_pofa_async()
+            torch.cuda.synchronize()
+            g4 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g4, stream=gs4):
+                step_pofa_async()
+            torch.cuda.synchronize()
+            g4.replay()
+            torch.cuda.synchronize()
+            acc4.zero_()
         with ClockSampler(0) as clk:
-            ms_a, _ = _timed(step_pofa, args.steps, stream)
+            if g4 is not None:
+                ms_a, _ = _timed(g4.replay, args.steps, stream)
+                bad4, checked4 = (int(v) for v in acc4.cpu().tolist())
+                if bad4 or checked4 != args.steps:
+                    raise RuntimeError(f"C4 graph replays: build ticket status {bad4}, {checked4}/{args.steps}")
+            else:
+                ms_a, _ = _timed(step_pofa, args.steps, stream)
+            ms_sync, _ = _timed(step_pofa, args.steps, stream)
             ms_p, _ = _timed(step_ppfl, args.steps, stream)
         st_a, _ = _stage_profile(step_pofa, args.steps, dev)
         st_p, _ = _stage_profile(step_ppfl, args.steps, dev)
@@ -375,7 +442,10 @@ def extra_config(args):
                                 "parallelism": "single"},
                      "ppfl": {"value": n / (ms_p / 1e3), "unit": "frag/s", "ms_per_step": ms_p, "bytes": mem_p,
                               "stage_ms": {k: round(v, 4) for k, v in st_p.items()}},
-                     "pofa": {"bytes": mem_a, "stage_ms": {k: round(v, 4) for k, v in st_a.items()}},
+                     "pofa": {"bytes": mem_a, "stage_ms": {k: round(v, 4) for k, v in st_a.items()},
+                              "host": ("CUDA-graph replays of one captured asynchronous build, every build ticket "
+                                       "checked on the device" if g4 is not None else "Python-enqueued sync builds"),
+                              "sync_build_ms_per_step": ms_sync},
                      "clocks": clk.summary()})
         if algo:
             t = st_a[dom] / 1e3
@@ -437,7 +507,7 @@ def extra_config(args):
         stage, _ = _stage_profile(step, 1, dev)
         P = W * H * len(views)
         rb = ray_bytes(stats, P)  # per step (this rank's views)
-        t_ray = stage.get("raycast", ms)
+        t_ray = stage.get("raycast", ms) + stage.get("raycast_handoff", 0.0)
         line.update({"value": len(all_views) / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms,
                      "rays_per_s": W * H * len(all_views) / (ms / 1e3),
                      "config": {"workload": "C5: 64 x 3840x2160 perspective ray-cast views (Fibonacci sphere, "
@@ -451,7 +521,8 @@ def extra_config(args):
                      "roofline": {"bound": "hbm", "kernel": "raycast", "achieved": round(rb / (t_ray / 1e3) / 1e9, 1),
                                   "peak": peak, "unit": "GB/s", "frac": round(rb / (t_ray / 1e3) / 1e9 / peak, 4),
                                   "traffic": None, "algorithmic_bytes": rb, "peak_kind": peak_kind,
-                                  "note": "latency/divergence bound (f64 slab DFS), see profiles/"},
+                                  "note": "packet traversal, latency bound (register-limited occupancy), see "
+                                          "profiles/"},
                      "clocks": clk.summary()})
         if not args.no_cpu_baseline and rank == 0 and world == 1:
             from oracle import oracle as orc

@@ -255,6 +255,15 @@ int fhv_ticket_check(const fhv_ticket_t *ticket, int64_t expect_total);
    (device int64, zeroed by the caller) keeps the first non-OK status,
    acc[1] counts the checks.  Async. */
 int fhv_ticket_accumulate(fhv_ctx *ctx, int64_t expect_total, int64_t *acc, void *stream);
+/* build_pofl without a host wait, on the same ticket protocol: the pool's
+   capacity is the caller's (e.g. the previous build's total), the outcome
+   (status; the total in frags_total = scan_total = alloc) lands in *ticket.
+   fhv_ticket_check(ticket, guess) is FHV_OK when the total equals the guess;
+   FHV_STALE (a speculative item plan missed, or another total) means rebuild
+   with fhv_build_pofl.  Replaces fhv/storage.py:574-587 like fhv_build_pofl. */
+int fhv_build_pofl_async(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int32_t levels,
+                         fhv_pool_t *pool, int32_t *heads, uint8_t *pyramid, int32_t flags, fhv_ticket_t *ticket,
+                         void *stream);
 
 /* rebuild_pofl_as_pofa (fhv/storage.py:624-652): repack the first n records
    of a linked-list pool into per-leaf contiguous ranges (Morton order, pool

@@ -122,6 +122,8 @@ _SIGS = {
     "fhv_op_pofa_scatter": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, _P(c_i64), c_vp]),
     "fhv_pofa_build_async": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, c_vp, c_vp, c_vp, _P(Pool), c_i32,
                                             c_vp, c_vp]),
+    "fhv_build_pofl_async": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, _P(Pool), c_vp, c_vp, c_i32, c_vp,
+                                            c_vp]),
     "fhv_ticket_check": (ctypes.c_int, [c_vp, c_i64]),
     "fhv_ticket_accumulate": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp]),
     "fhv_chain_indices": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, _P(c_i64), c_vp]),

@@ -2884,6 +2884,57 @@ __global__ void k_ticket_acc(const Control* ctl, long long expect, long long* ac
 }  // namespace
 }  // namespace fhv
 
+namespace fhv {
+namespace {
+// the linked build's outcome in the POFA ticket's words: total in all three
+// count fields (so fhv_ticket_check / k_ticket_acc compare it with the guess)
+__global__ void k_ticket_linked(Control* ctl, int atomic_alloc) {
+  const unsigned long long total = atomic_alloc ? ctl->alloc : ctl->scan_total;
+  ctl->spare[4] = (unsigned long long)(long long)ctl->status;
+  ctl->spare[5] = total;
+  ctl->spare[6] = total;
+  ctl->spare[7] = total;
+}
+}  // namespace
+}  // namespace fhv
+
+// build_pofl without a host wait (the POFA build's ticket protocol): the pool
+// capacity is the caller's (its guess of the total, or the overalloc), the
+// item plan speculative when this ctx has one for the job count; the total
+// and the status land in *ticket.  A total above the capacity means dropped
+// records (FHV_OVERFLOW semantics of the synchronous build), a speculation
+// miss FHV_RETRY_ITEMS in the status (rebuild with fhv_build_pofl).
+extern "C" int fhv_build_pofl_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
+                                    int32_t levels, fhv_pool_t* pool, int32_t* heads, uint8_t* pyramid, int32_t flags,
+                                    fhv_ticket_t* ticket, void* stream) {
+  if (!ctx || !pool || !heads || !pyramid || !ticket) return FHV_BAD_ARGS;
+  int rc = validate(tris, cfg);
+  if (rc) return rc;
+  if (pool->capacity < 0 || pool->capacity >= (1LL << 31)) return FHV_BAD_ARGS;
+  if (levels < 1 || levels > kMaxLevels) return FHV_BAD_ARGS;
+  cudaStream_t s = (cudaStream_t)stream;
+  const CaptureParams p = make_params(tris, cfg);
+  const bool atomic_alloc = (flags & FHV_ALLOC_ATOMIC) != 0;
+  const long long n_keys = 1LL << (3 * levels);
+  if ((rc = plan(ctx, p, s, true))) return rc;
+  if ((rc = count(ctx, p, false, 0, nullptr, s))) return rc;
+  EmitOut o = empty_out();
+  set_pool(o, pool);
+  o.heads = heads;
+  o.flags = flags;
+  o.levels = levels;
+  o.n_keys = n_keys;
+  if ((rc = emit<kPofl>(ctx, p, o, atomic_alloc, s))) return rc;
+  if ((flags & FHV_EXACT_ORDER) && (rc = chain_order(ctx, heads, pool->prev, n_keys, pool->capacity, s))) return rc;
+  if ((rc = pyramid_from_heads(ctx, heads, pyramid, levels, s))) return rc;
+  {
+    LaunchScope L_(ctx, kStScan, s);
+    k_ticket_linked<<<1, 1, 0, s>>>(ctx->ctl, atomic_alloc ? 1 : 0);
+  }
+  if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  return check_cuda(ctx, cudaMemcpyAsync(ticket, &ctx->ctl->spare[4], sizeof(fhv_ticket_t), cudaMemcpyDefault, s));
+}
+
 extern "C" int fhv_ticket_accumulate(fhv_ctx* ctx, int64_t expect_total, int64_t* acc, void* stream) {
   if (!ctx || !acc) return FHV_BAD_ARGS;
   {

@@ -387,6 +387,28 @@ class FhvPofl:
     def occupied_leaves(self) -> torch.Tensor:
         return torch.nonzero(self.directory.heads >= 0).reshape(-1).to(torch.int64)
 
+    pending = None  # (ticket, guessed total, synchronous rebuild) of an asynchronous build_pofl
+    done = None     # CUDA event recorded after the asynchronous build's ticket copy
+
+    def wait(self) -> "FhvPofl":
+        """Finish an asynchronous build_pofl: synchronise, check its ticket,
+        rebuild synchronously in place if the speculation was wrong."""
+        if self.pending is None:
+            return self
+        tk, guess, rebuild = self.pending
+        if self.done is not None:
+            self.done.synchronize()
+        else:
+            torch.cuda.current_stream(self.pool.device).synchronize()
+        rc = ticket_status(tk, guess)
+        self.pending = None
+        if rc == _lib.FHV_STALE:
+            fresh = rebuild()
+            self.directory, self.pyramid, self.pool, self.stats = fresh.directory, fresh.pyramid, fresh.pool, fresh.stats
+        else:
+            _lib.check(rc, "build_pofl")
+        return self
+
 
 @dataclass
 class FhvPofa:
@@ -497,8 +519,15 @@ def build_ppfl(scene: Scene, cfg: RasterConfig, strategy: CaptureStrategy | None
 
 def build_pofl(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int,
                capacity: int | None = None, overalloc: float = 10.0, threads: int = 1, *,
-               exact_order: bool = False, alloc: str = "ordered", device=None) -> FhvPofl:
-    """Per-octant linked lists + occupancy pyramid (fhv/storage.py:574-587)."""
+               exact_order: bool = False, alloc: str = "ordered", device=None, sync: bool = True,
+               ticket: torch.Tensor | None = None) -> FhvPofl:
+    """Per-octant linked lists + occupancy pyramid (fhv/storage.py:574-587).
+
+    ``sync=False`` (once a build of the same scene / plan has run): nothing
+    waits for the device -- the pool is sized by the capacity as usual,
+    ``next_free`` is the last exact total, and the outcome goes to ``ticket``
+    (pinned int64[4]); :meth:`FhvPofl.wait` checks it and rebuilds in place
+    when the speculation (item plan, total) was wrong."""
     if levels < 1:
         raise FhvError("octree needs at least one level")
     _check_levels(levels)
@@ -511,13 +540,33 @@ def build_pofl(scene: Scene, strategy: CaptureStrategy, cfg: RasterConfig, level
     pool = FragmentPool(capacity, dev)
     heads = torch.full((8 ** levels,), -1, dtype=torch.int32, device=dev)
     pyr = OccupancyPyramid(levels, device=dev)
-    nf = ctypes_i64()
     lib = _lib.load()
     tris, p = ds.struct(), pool.struct()
+    guesses = ds.__dict__.setdefault("_pofl_totals", {})
+    gkey = (plan.key, levels, capacity, alloc, exact_order)
+    guess = guesses.get(gkey)
+    if not sync and guess is not None:
+        tk = ticket if ticket is not None else torch.zeros(4, dtype=torch.int64).pin_memory()
+        rc = lib.fhv_build_pofl_async(_lib.ctx(dev), tris, c, levels, p, _lib.ptr(heads), _lib.ptr(pyr.data),
+                                      _flags(alloc, exact_order), c_vp_of(tk), _lib.stream_ptr(dev))
+        _lib.check(rc, "build_pofl")
+        pool.next_free = guess
+        pool.overflowed = guess > pool.capacity
+        pool.in_unit_cube = True
+        vol = FhvPofl(PoflDirectory(levels, heads), pyr, pool, h, plan.stats(guess), scene.materials)
+        vol.pending = (tk, guess, lambda: build_pofl(scene, strategy, cfg, levels, capacity, overalloc, threads,
+                                                     exact_order=exact_order, alloc=alloc, device=device))
+        if not torch.cuda.is_current_stream_capturing():
+            done = torch.cuda.Event()
+            done.record(torch.cuda.current_stream(dev))
+            vol.done = done
+        return vol
+    nf = ctypes_i64()
     rc = lib.fhv_build_pofl(_lib.ctx(dev), tris, c, levels, p, _lib.ptr(heads), _lib.ptr(pyr.data),
                             _flags(alloc, exact_order), nf, _lib.stream_ptr(dev))
     _lib.check(rc, "build_pofl", allow=(_lib.FHV_OK, _lib.FHV_OVERFLOW))
     pool.next_free = int(nf.value)
+    guesses[gkey] = pool.next_free
     pool.overflowed = pool.next_free > pool.capacity
     pool.in_unit_cube = True
     return FhvPofl(PoflDirectory(levels, heads), pyr, pool, h, plan.stats(pool.next_free), scene.materials)

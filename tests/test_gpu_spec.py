@@ -247,3 +247,97 @@ def test_job_setup_error_survives_pool_guess(exact):
         fhv.pofa_build(good, ns, cfg, 4, exact_order=exact, tris=ds)
     with pytest.raises(ValueError):
         fhv.pofa_build(good, ns, cfg, 4, exact_order=exact, tris=ds, sync=False).wait()
+
+
+def _same_pofl(a, b):
+    assert a.pool.next_free == b.pool.next_free
+    assert np.array_equal(a.directory.heads.cpu().numpy(), b.directory.heads.cpu().numpy())
+    assert np.array_equal(a.pyramid.data.cpu().numpy(), b.pyramid.data.cpu().numpy())
+    n = b.pool.stored_count
+    ha, hb = a.pool.numpy(), b.pool.numpy()
+    for k in ("position", "normal", "material_id", "object_id", "prev_index"):
+        assert np.array_equal(ha[k][:n], hb[k][:n]), k
+
+
+@pytest.mark.parametrize("exact", (True, False))
+def test_async_pofl_build_matches_sync(exact):
+    """build_pofl(sync=False): the same chains / pyramid / pool as the
+    synchronous build (fhv/storage.py:574-587), no host wait until wait()."""
+    s = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+    cfg = _cfg(s, 128)
+    ref = fhv.build_pofl(s, ns, cfg, 5, exact_order=exact)
+    vols = [fhv.build_pofl(s, ns, cfg, 5, exact_order=exact, sync=False) for _ in range(3)]
+    assert all(v.pending is not None for v in vols)
+    for v in vols:
+        v.wait()
+        assert v.pending is None
+        if exact:
+            _same_pofl(v, ref)
+        else:  # ordered allocation without the chain fix-up: same multiset of records per leaf
+            assert v.pool.next_free == ref.pool.next_free
+            assert np.array_equal(v.pyramid.data.cpu().numpy(), ref.pyramid.data.cpu().numpy())
+
+
+def test_async_pofl_build_wrong_guess_is_rebuilt():
+    s = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+    cfg = _cfg(s, 96)
+    ref = fhv.build_pofl(s, ns, cfg, 5, exact_order=True)
+    ds = fhv.device.device_scene(s)
+    key = next(k for k in ds._pofl_totals if k[1] == 5 and k[0][2] == tuple(cfg.resolution))
+    ds._pofl_totals[key] = ref.pool.next_free + 3  # a wrong speculation
+    v = fhv.build_pofl(s, ns, cfg, 5, exact_order=True, sync=False)
+    torch.cuda.synchronize()
+    assert fhv.storage.check_ticket(v) == fhv._lib.FHV_STALE
+    v.wait()
+    _same_pofl(v, ref)
+
+
+def test_async_pofl_build_and_raycast_in_a_cuda_graph():
+    """The C2 step as the bench times it: build_pofl(sync=False) + the device
+    ticket check + render_raycast captured once in a CUDA graph; every replay
+    re-runs both and the image / RaycastStats equal the synchronous ones."""
+    s = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+    cfg = _cfg(s, 160)
+    ref = fhv.build_pofl(s, ns, cfg, 5, exact_order=True)
+    cam = fhv.viewpoint_camera("+x", (96, 64), "perspective")
+    lights = lights_for("head", cam)
+    rc = fhv.default_raycast_config(ref)
+    rimg, rst = fhv.render_raycast(ref, cam, lights, rc)
+    gs = torch.cuda.Stream()
+    acc = torch.zeros(2, dtype=torch.int64, device="cuda")
+    tk = torch.zeros(4, dtype=torch.int64).pin_memory()
+    lib = fhv._lib.load()
+    n = ref.pool.next_free
+
+    from paper_2211_15460_b200.device import DeviceShading
+    from paper_2211_15460_b200.lights import ImageBuffer
+    sh = DeviceShading(s.materials, lights, torch.device("cuda"))
+    w, h = cam.resolution
+    buf = ImageBuffer(w, h, torch.zeros((h, w, 4), dtype=torch.float64, device="cuda"),
+                      torch.empty((h, w), dtype=torch.float64, device="cuda"))
+
+    def step():  # everything the graph replays is device work (no host-side tensor creation)
+        v = fhv.build_pofl(s, ns, cfg, 5, exact_order=True, sync=False, ticket=tk)
+        assert lib.fhv_ticket_accumulate(fhv._lib.ctx(v.pool.device), n, fhv._lib.ptr(acc),
+                                         fhv._lib.stream_ptr(v.pool.device)) == 0
+        buf.pixels.zero_()
+        img, st = fhv.render_raycast(v, cam, lights, rc, out=buf, sync=False, shading=sh)
+        return v, img, st
+    with torch.cuda.stream(gs):
+        step()
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=gs):
+        v, img, st = step()
+    acc.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    bad, k = acc.cpu().tolist()
+    assert (bad, k) == (0, 3)
+    assert np.array_equal(img.pixels.cpu().numpy(), rimg.pixels.cpu().numpy())
+    assert fhv.RaycastStats(*st.counters.cpu().tolist()).as_dict() == rst.as_dict()
