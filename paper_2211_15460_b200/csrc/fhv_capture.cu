@@ -1724,8 +1724,10 @@ __global__ void k_leaf_order(const uint32_t* __restrict__ offsets, const uint32_
 //                in the tile that do not end inside the look-ahead are listed
 //                for k_leaf_fix_big.
 //   k_leaf_fix_big  a CTA per listed segment: end by a flag search, sorted
-//                check, bitonic sort of (rank, index) keys in shared memory
-//                (<= 4096) or scratch, records gathered through scratch.
+//                check; segments of <= 256 slots ranked by counting (a
+//                thread per record, one barrier), longer ones by a bitonic
+//                sort of (rank, index) keys in shared memory (<= 4096) or
+//                scratch, records gathered through scratch.
 //   prev := -1   one memset (fhv/storage.py:439).
 // No directory access at all; when nothing is out of order the cost is one
 // coalesced read of the ranks.  Result: records of each leaf in ascending
@@ -1908,7 +1910,7 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_leaf_fix(PoolRefs pl, const 
 }
 
 // long segments (did not end inside a tile's look-ahead): a CTA per segment
-__global__ void __launch_bounds__(1024) k_leaf_fix_big(PoolRefs pl, const unsigned long long* __restrict__ n_dev,
+__global__ void __launch_bounds__(256) k_leaf_fix_big(PoolRefs pl, const unsigned long long* __restrict__ n_dev,
                                                        long long cap, const unsigned long long* __restrict__ big_list,
                                                        const unsigned long long* __restrict__ n_big,
                                                        unsigned long long big_cap,
@@ -1941,6 +1943,29 @@ __global__ void __launch_bounds__(1024) k_leaf_fix_big(PoolRefs pl, const unsign
       if ((pl.rank[i] & ~kSegBit) < (pl.rank[i - 1] & ~kSegBit)) s_dis = 1;
     __syncthreads();
     if (!s_dis) continue;
+    if (cnt <= (long long)blockDim.x) {
+      // short segment (the common big one, ~65-100 slots): an element's
+      // destination = how many ranks of the segment are smaller (ranks are
+      // distinct); records held in registers across one barrier, then
+      // written in place
+      uint32_t* rk = reinterpret_cast<uint32_t*>(sk);
+      const long long i = threadIdx.x;
+      uint32_t R[9];
+      uint32_t mine = 0;
+      if (i < cnt) {
+        stage_record(pl, R, off + i);
+        mine = R[8] & ~kSegBit;
+        rk[i] = mine;
+      }
+      __syncthreads();
+      if (i < cnt) {
+        int dst = 0;
+        for (int j = 0; j < (int)cnt; ++j) dst += rk[j] < mine ? 1 : 0;
+        unstage_record(pl, R, off + dst, dst == 0 ? kSegBit : 0u);
+      }
+      __syncthreads();
+      continue;
+    }
     long long np2 = 1;
     while (np2 < cnt) np2 <<= 1;
     unsigned long long* K = np2 <= kSortSmem ? sk : kscr + 2 * off;
@@ -2722,7 +2747,7 @@ static int pofa_scatter_async(fhv_ctx* ctx, const CaptureParams& p, int32_t leve
     }
     {
       LaunchScope L_(ctx, kStLeafSort, s);
-      k_leaf_fix_big<<<148, 1024, 0, s>>>(pl, n_frags_dev, cap, big, &ctx->ctl->leaf_n[2], big_cap, keys, recs);
+      k_leaf_fix_big<<<148, 256, 0, s>>>(pl, n_frags_dev, cap, big, &ctx->ctl->leaf_n[2], big_cap, keys, recs);
     }
     if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
     if ((rc = check_cuda(ctx, cudaMemsetAsync(pool->prev, 0xff, (size_t)cap * 4, s)))) return rc;
