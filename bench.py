@@ -606,10 +606,20 @@ def main():
                     raise
                 composite = f"allreduce (peer mapping unavailable: {type(e).__name__})"
         mode = "peer" if peer is not None else "allreduce"
+        # after the first (synchronous) build every step's build is
+        # speculative: no host wait and no collective (every rank's total,
+        # base and binning from that build); the tickets of all ranks are
+        # checked after the timed loop -- a wrong speculation fails the run
+        sh_tickets = torch.zeros((4 * (args.steps + 4), 4), dtype=torch.int64).pin_memory()
+        sh_used: list = []
 
         def step(tris=ds, out=img):
+            asynchronous = not args.sync_steps and len(sh_used) < len(sh_tickets)
+            tk = sh_tickets[len(sh_used)] if asynchronous else None
             vol = shard.pofa_build_shard(scene, strat, cfg, L, comm, ranges=ranges, exact_order=args.exact_order,
-                                         device=dev, tris=tris)
+                                         device=dev, tris=tris, sync=not asynchronous, ticket=tk)
+            if vol.pending is not None:
+                sh_used.append(vol.pending[:2])
             shard.splat_render_shard(vol, view, w["lights"], w["radius"], scene.materials, comm, out=out,
                                      shading=shading, buffers=bufs, composite=mode, peer=peer)
             return vol
@@ -645,7 +655,17 @@ def main():
 
     if world > 1:
         def check_tickets():
-            return 0
+            torch.cuda.synchronize()
+            worst = 0
+            for tk, guess in sh_used:
+                rc = fhv.storage.ticket_status(tk, guess)
+                worst = worst or rc
+            n = len(sh_used)
+            sh_used.clear()
+            codes = comm.all_gather_int(worst)  # every rank's tickets (a lower rank's miss moves the bases)
+            if any(codes):
+                raise RuntimeError(f"speculative sharded build failed its ticket check (statuses {codes})")
+            return n
     for _ in range(args.warmup):
         vol = step()
     torch.cuda.synchronize()

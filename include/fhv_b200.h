@@ -354,6 +354,19 @@ int fhv_pofa_shard_scatter(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_captu
                            const fhv_shard_t *shard, const uint32_t *counts_local,
                            const uint32_t *offsets_local, uint64_t base, fhv_pool_t *pool, int32_t flags,
                            void *stream);
+/* The three steps above in one call with no host wait and no collective
+   (speculative, the fhv_pofa_build_async ticket protocol): the caller passes
+   base and a pool sized by THIS rank's total, both taken from the previous
+   build of the same scene and ranges on every rank; that build's triangle
+   binning is reused when this ctx made it for the same triangle arrays and
+   shard (their contents must not have changed).  *ticket receives this
+   rank's status and total; the build is valid when fhv_ticket_check(ticket,
+   pool capacity) is FHV_OK on EVERY rank (then every rank's base was right).
+   Replaces fhv/storage.py:590-621 per rank like the three-step form. */
+int fhv_pofa_shard_build_async(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t *cfg, int32_t levels,
+                               const fhv_shard_t *shard, uint32_t *counts_local, uint32_t *offsets_local,
+                               uint8_t *pyramid, uint64_t base, fhv_pool_t *pool, int32_t flags,
+                               fhv_ticket_t *ticket, void *stream);
 
 /* splat_render over pool[0:n): out_rgba [H][W][4] f64, out_depth [H][W] f64,
    out_winner [H][W] int32 (pool index or -1, may be NULL), gbuffer may be

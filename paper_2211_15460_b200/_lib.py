@@ -91,6 +91,8 @@ _SIGS = {
     "fhv_pofa_shard_directory": (ctypes.c_int, [c_vp, c_i32, _P(Shard), c_vp, c_vp, c_vp, ctypes.c_uint64, c_vp]),
     "fhv_pofa_shard_scatter": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, _P(Shard), c_vp, c_vp,
                                               ctypes.c_uint64, _P(Pool), c_i32, c_vp]),
+    "fhv_pofa_shard_build_async": (ctypes.c_int, [c_vp, _P(Tris), _P(CaptureCfg), c_i32, _P(Shard), c_vp, c_vp, c_vp,
+                                                  ctypes.c_uint64, _P(Pool), c_i32, c_vp, c_vp]),
     "fhv_splat": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_f64, c_vp, _P(Shading), c_vp, c_vp,
                                  c_vp, _P(GBuf), c_i32, c_vp]),
     "fhv_splat_shard_keys": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_f64, c_vp, c_vp, c_vp]),

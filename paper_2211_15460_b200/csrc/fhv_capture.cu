@@ -2560,10 +2560,28 @@ bool shard_ok(const fhv_shard_t* sh, int levels) {
          sh->cell_hi % tl == 0 && sh->n_boxes >= 0 && sh->n_boxes <= FHV_SHARD_MAX_BOXES && sh->margin >= 0.0;
 }
 
+// FNV-1a over the shard description (range, margin, boxes)
+uint64_t shard_sig(const fhv_shard_t* sh) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* d, size_t n) {
+    const unsigned char* b = (const unsigned char*)d;
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  mix(&sh->cell_lo, 8);
+  mix(&sh->cell_hi, 8);
+  mix(&sh->n_boxes, 4);
+  mix(&sh->margin, 8);
+  mix(sh->boxes, (size_t)sh->n_boxes * 6 * sizeof(double));
+  return h;
+}
+
 // params for one shard: binned triangle list (computed once by the count call
-// and kept in ctx for the scatter call) and the owned leaf range
+// and kept in ctx for the scatter call) and the owned leaf range.  reuse_bin:
+// keep the ctx's binning (no kernels, no sync) when it was made for the same
+// triangle arrays and shard -- the caller's promise that their contents did
+// not change (the speculative sharded build)
 int shard_params(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int levels,
-                 const fhv_shard_t* sh, bool do_bin, CaptureParams& p, cudaStream_t s) {
+                 const fhv_shard_t* sh, bool do_bin, CaptureParams& p, cudaStream_t s, bool reuse_bin = false) {
   p = make_params(tris, cfg);
   const unsigned long long n_leaves = 1ull << (3 * levels);
   p.cell_lo = sh ? sh->cell_lo : 0ull;
@@ -2573,7 +2591,13 @@ int shard_params(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* 
     return FHV_OK;
   }
   const long long T = tris->n_tri;
+  if (do_bin && reuse_bin && ctx->n_binned >= 0 && ctx->bin_pos == (const void*)tris->pos && ctx->bin_n_tri == T &&
+      ctx->bin_sig == shard_sig(sh))
+    do_bin = false;
   if (do_bin) {
+    ctx->bin_pos = tris->pos;
+    ctx->bin_n_tri = T;
+    ctx->bin_sig = shard_sig(sh);
     ctx->n_binned = 0;
     if (T > 0) {
       auto* flag = (uint32_t*)scratch(ctx, kTriFlag, (size_t)T * 4);
@@ -2614,12 +2638,12 @@ namespace {
 // item scan's total is parked in ctl->frags_total for the caller's next sync
 int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
                      const fhv_shard_t* shard, uint32_t* counts_local, cudaStream_t s, CaptureParams& p,
-                     bool spec = false, bool ranks = true) {
+                     bool spec = false, bool ranks = true, bool reuse_bin = false) {
   ctx->pass1_levels = -1;
   ctx->pass1_ranks = ranks;
   int rc;
   if ((rc = reset_control(ctx, s))) return rc;
-  if ((rc = shard_params(ctx, tris, cfg, levels, shard, true, p, s))) return rc;
+  if ((rc = shard_params(ctx, tris, cfg, levels, shard, true, p, s, reuse_bin))) return rc;
   const unsigned long long n_local = p.cell_hi - p.cell_lo;
   if ((rc = plan(ctx, p, s, spec))) return rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(counts_local, 0, (size_t)n_local * 4, s)))) return rc;
@@ -2885,6 +2909,49 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   // pass-1 bookkeeping for a follow-up fhv_pofa_scatter is not kept: the
   // ticket is the only result
   ctx->pass1_levels = -1;
+  return check_cuda(ctx, cudaMemcpyAsync(ticket, &ctx->ctl->spare[4], sizeof(fhv_ticket_t), cudaMemcpyDefault, s));
+}
+
+// One rank's share of pofa_build with no host wait and no collective: the
+// caller speculates every rank's fragment total from the previous build of
+// the same scene / ranges (base = the lower ranks' totals, the pool sized by
+// this rank's), reuses that build's triangle binning, and enqueues pass 1,
+// the directory (global offsets from `base`) and pass 2.  The ticket holds
+// this rank's status and total: the build is valid when EVERY rank's ticket
+// checks against its guess (then every base was right too).
+extern "C" int fhv_pofa_shard_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
+                                          int32_t levels, const fhv_shard_t* shard, uint32_t* counts_local,
+                                          uint32_t* offsets_local, uint8_t* pyramid, uint64_t base, fhv_pool_t* pool,
+                                          int32_t flags, fhv_ticket_t* ticket, void* stream) {
+  if (!ctx || !counts_local || !offsets_local || !pyramid || !ticket || levels < 1 || levels > 10 ||
+      !shard_ok(shard, levels))
+    return FHV_BAD_ARGS;
+  int rc = validate(tris, cfg);
+  if (rc) return rc;
+  if (!pool || pool->capacity < 0 || (pool->capacity > 0 && (!pool->pos || !pool->nrm || !pool->mat || !pool->obj ||
+                                                              !pool->prev)))
+    return FHV_BAD_ARGS;
+  if (base + (uint64_t)pool->capacity > 0xffffffffull) return FHV_TOO_MANY;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned long long n_leaves = 1ull << (3 * levels);
+  const unsigned long long lo = shard ? shard->cell_lo : 0ull, hi = shard ? shard->cell_hi : n_leaves;
+  CaptureParams p;
+  if ((rc = pofa_count_async(ctx, tris, cfg, levels, shard, counts_local, s, p, true, true, true))) return rc;
+  if (lo == 0 && hi == n_leaves && base == 0) {
+    if ((rc = scan_leaves_and_pyramid(ctx, counts_local, offsets_local, pyramid, levels, s))) return rc;
+  } else if ((rc = scan_leaf_range_and_pyramid(ctx, counts_local, offsets_local, pyramid, levels, lo, hi, base, s))) {
+    return rc;
+  }
+  if (pool->capacity > 0 &&
+      (rc = pofa_scatter_async(ctx, p, levels, lo, hi, counts_local, offsets_local, base, pool, flags, s, false,
+                               &ctx->ctl->frags_total, 0)))
+    return rc;
+  {
+    LaunchScope L_(ctx, kStScan, s);
+    k_ticket<<<1, 1, 0, s>>>(ctx->ctl);
+  }
+  if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  ctx->pass1_levels = -1;  // the ticket is the only result
   return check_cuda(ctx, cudaMemcpyAsync(ticket, &ctx->ctl->spare[4], sizeof(fhv_ticket_t), cudaMemcpyDefault, s));
 }
 

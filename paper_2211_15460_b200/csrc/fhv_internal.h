@@ -75,6 +75,11 @@ struct fhv_ctx {
   int64_t pass1_tris = -1;
   uint64_t pass1_lo = 0, pass1_hi = 0;
   int64_t n_binned = -1;  // triangles kept by the last shard binning (-1: no binning)
+  // what that binning ran on (the speculative sharded build reuses it without
+  // a sync when the triangle arrays and the shard are the same)
+  const void* bin_pos = nullptr;
+  int64_t bin_n_tri = -1;
+  uint64_t bin_sig = 0;
   // speculative capture planning (fhv_capture.cu plan()): item buffers sized by
   // the last exact plan with the same job count; spec = current plan is one
   int64_t item_cap = 0, last_n_jobs = -1;

@@ -313,9 +313,39 @@ class FhvPofaShard:
     materials: list | None = None
     layout = "POFA"
 
+    pending = None  # (ticket, guessed local total, collective synchronous rebuild) of a sync=False build
+    done = None     # CUDA event after the asynchronous build's ticket copy
+
     @property
     def levels(self) -> int:
         return self.directory.levels
+
+    def wait(self, comm: Comm) -> "FhvPofaShard":
+        """Finish a speculative ``pofa_build_shard(sync=False)`` on EVERY
+        rank (collective): each rank checks its ticket, the statuses are
+        gathered, and if any rank's total missed its guess all ranks rebuild
+        synchronously (the bases of the ranks above it were wrong too); any
+        other error is raised."""
+        if self.pending is None:
+            comm.all_gather_int(_lib.FHV_OK)  # stay collective with ranks that do wait
+            return self
+        tk, guess, rebuild = self.pending
+        if self.done is not None:
+            self.done.synchronize()
+        else:
+            torch.cuda.current_stream(self.pool.device).synchronize()
+        from .storage import ticket_status
+        rc = ticket_status(tk, guess)
+        self.pending = None
+        codes = comm.all_gather_int(rc)
+        bad = [c for c in codes if c not in (_lib.FHV_OK, _lib.FHV_STALE)]
+        if bad:
+            _lib.check(rc if rc != _lib.FHV_OK and rc != _lib.FHV_STALE else bad[0], "pofa_build_shard")
+        if any(c == _lib.FHV_STALE for c in codes):
+            fresh = rebuild()
+            for f in ("directory", "pyramid", "pool", "base", "total", "stats"):
+                setattr(self, f, getattr(fresh, f))
+        return self
 
     def gather_pyramid(self, comm: Comm) -> OccupancyPyramid:
         """The global occupancy pyramid: MAX over ranks is exact at and below
@@ -348,8 +378,14 @@ def _shard_struct(lo: int, hi: int, levels: int) -> _lib.Shard:
 
 def pofa_build_shard(scene, strategy: CaptureStrategy, cfg: RasterConfig, levels: int, comm: Comm,
                      ranges: list | None = None, balance: bool = True, exact_order: bool = True,
-                     device=None, tris=None) -> FhvPofaShard:
-    """This rank's share of ``pofa_build(scene, strategy, cfg, levels)``."""
+                     device=None, tris=None, sync: bool = True, ticket: torch.Tensor | None = None) -> FhvPofaShard:
+    """This rank's share of ``pofa_build(scene, strategy, cfg, levels)``.
+
+    ``sync=False`` (after a synchronous build of the same scene, ranges and
+    rank layout): no host wait and no collective -- every rank's total is
+    taken from that build (base, pool size), the triangle binning is reused
+    and the outcome goes to ``ticket``; :meth:`FhvPofaShard.wait` (collective)
+    checks all ranks' tickets and rebuilds if any speculation missed."""
     if levels < 4:
         raise FhvError("sharded capture needs levels >= 4")
     if levels > 11:
@@ -369,10 +405,35 @@ def pofa_build_shard(scene, strategy: CaptureStrategy, cfg: RasterConfig, levels
     tris, c = ds.struct(), capture_cfg(plan)
     sh = _shard_struct(lo, hi, levels)
     cx, st = _lib.ctx(dev), _lib.stream_ptr(dev)
+    cache = ds.__dict__.setdefault("_shard_totals", {})
+    ckey = (tuple(cfg.resolution), np.asarray(cfg.projection).tobytes(), strategy.kind,
+            getattr(strategy, "axis", None), levels, tuple(tuple(r) for r in ranges), comm.rank, comm.world,
+            bool(exact_order))
+    totals = cache.get(ckey)
+    if not sync and totals is not None:
+        base, total, guess = sum(totals[:comm.rank]), sum(totals), totals[comm.rank]
+        pool = FragmentPool(guess, dev, fill_prev=False)
+        tk = ticket if ticket is not None else torch.zeros(4, dtype=torch.int64).pin_memory()
+        rc = lib.fhv_pofa_shard_build_async(cx, tris, c, levels, sh, _lib.ptr(counts), _lib.ptr(offsets),
+                                            _lib.ptr(pyr.data), base, pool.struct(),
+                                            _lib.FHV_EXACT_ORDER if exact_order else 0, ctypes.c_void_p(tk.data_ptr()),
+                                            st)
+        _lib.check(rc, "pofa_build_shard")
+        pool.next_free = guess
+        vol = FhvPofaShard(PofaDirectory(levels, offsets, counts), pyr, pool, int(cfg.resolution[1]), lo, hi, base,
+                           total, comm.rank, comm.world, plan.stats(total), scene.materials)
+        vol.pending = (tk, guess, lambda: pofa_build_shard(scene, strategy, cfg, levels, comm, ranges, balance,
+                                                           exact_order, device, ds))
+        if not torch.cuda.is_current_stream_capturing():
+            done = torch.cuda.Event()
+            done.record(torch.cuda.current_stream(dev))
+            vol.done = done
+        return vol
     local = ctypes.c_int64(0)
     rc = lib.fhv_pofa_shard_count(cx, tris, c, levels, sh, _lib.ptr(counts), local, st)
     _lib.check(rc, "pofa_build_shard pass 1")
     totals = comm.all_gather_int(local.value)
+    cache[ckey] = list(totals)
     base, total = sum(totals[:comm.rank]), sum(totals)
     if total >= 1 << 32:
         raise FhvError("fragment count exceeds the 32-bit offset range")

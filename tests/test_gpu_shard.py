@@ -177,3 +177,43 @@ def test_subtree_sharded_raycast_equals_single_gpu(name, world, mode):
                 assert np.array_equal(got, want)
             else:
                 assert np.max(np.abs(got - want)) <= 1e-12
+
+
+@pytest.mark.parametrize("world", (2, 3))
+def test_speculative_sharded_build_no_sync(world):
+    """pofa_build_shard(sync=False): no host wait and no collective inside the
+    build (every rank's total, base and the triangle binning from the first
+    synchronous build); wait(comm) checks all tickets -- the union equals the
+    1-GPU pofa_build bit for bit, and a rank whose guess is wrong makes EVERY
+    rank rebuild (the bases above it were wrong too)."""
+    scene = _scene("spheres")
+    res, L = 256, 6
+    cfg = fhv.RasterConfig.from_camera(fhv.capture_camera(scene, "+z", res))
+    ns = fhv.CaptureStrategy.normal_space()
+    ref = fhv.pofa_build(scene, ns, cfg, L, exact_order=True)
+
+    def rank_fn(c):
+        shard.pofa_build_shard(scene, ns, cfg, L, c, balance=True, exact_order=True)  # fills the guesses
+        vols = [shard.pofa_build_shard(scene, ns, cfg, L, c, balance=True, exact_order=True, sync=False)
+                for _ in range(2)]
+        assert all(v.pending is not None for v in vols)
+        for v in vols:
+            v.wait(c)
+        # a wrong guess on rank 0 shifts every higher rank's base
+        ds = fhv.device.device_scene(scene)
+        key = next(k for k in ds._shard_totals if k[6] == c.rank and k[7] == c.world)
+        good = list(ds._shard_totals[key])
+        ds._shard_totals[key] = [good[0] + 5] + good[1:]  # every rank holds the same (wrong) vector
+        bad = shard.pofa_build_shard(scene, ns, cfg, L, c, balance=True, exact_order=True, sync=False)
+        bad.wait(c)
+        return vols[-1], bad
+
+    out = _run_ranks(world, rank_fn)
+    for idx in (0, 1):
+        vols = [o[idx] for o in out]
+        assert sum(v.pool.capacity for v in vols) == ref.pool.capacity
+        cat = lambda f: torch.cat([f(v) for v in vols]).cpu()  # noqa: E731
+        assert torch.equal(cat(lambda v: v.directory.counts), ref.directory.counts.cpu())
+        assert torch.equal(cat(lambda v: v.directory.offsets), ref.directory.offsets.cpu())
+        for k in ("position", "normal", "material_id", "object_id", "prev_index"):
+            assert torch.equal(cat(lambda v: getattr(v.pool, k)), getattr(ref.pool, k).cpu()), (idx, k)

@@ -50,9 +50,12 @@ def _worker(rank, world, port, q, steps):
         comm = shard.TorchComm(device=torch.device("cuda", 0))
         ns = fhv.CaptureStrategy.normal_space()
         out = []
-        for _ in range(steps):  # repeated steps: cached plans, pool guesses, reused buffers
-            v = shard.pofa_build_shard(scene, ns, cfg, L, comm, exact_order=True)
+        for i in range(steps):  # repeated steps: cached plans, pool guesses, reused buffers
+            # step 0 synchronous; later steps speculative (no host wait, no
+            # collective in the build), checked collectively by wait()
+            v = shard.pofa_build_shard(scene, ns, cfg, L, comm, exact_order=True, sync=(i == 0))
             img = image_numpy(shard.splat_render_shard(v, cam, [fhv.headlight(cam)], 1.0 / RES, scene.materials, comm))
+            v.wait(comm)
             pyr = v.gather_pyramid(comm)
             out.append({"lo": v.cell_lo, "hi": v.cell_hi, "base": v.base, "total": v.total,
                         "pool": {k: getattr(v.pool, k).cpu().numpy() for k in
@@ -77,7 +80,7 @@ def test_two_process_sharded_pofa_and_splat_equal_single_gpu(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    steps = 2
+    steps = 3
     procs = [ctx.Process(target=_worker, args=(r, world, port, q, steps)) for r in range(world)]
     for p in procs:
         p.start()
