@@ -1026,14 +1026,18 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded icosphere field, no dataset)",
                 "config": CONFIG,  # the workload; identical to the reference arm's
                 "run": dict(fragments=n_frags,
-                               parallelism=f"morton-range shards x{world} (NCCL)" if world > 1 else "single",
+                               parallelism=(f"morton-range shards x{world} ({os.environ.get('FHV_BENCH_BACKEND', 'nccl')})"
+                                            if world > 1 else "single"),
                                composite=composite if world > 1 else None,
                                exact_order=bool(args.exact_order), splat="packed" if args.packed else "exact",
                                host=("CUDA-graph replays of one captured asynchronous step (POFA build + splat, "
                                      "every kernel / memset / copy re-executed), all %d build tickets checked on the "
                                      "device" % async_checked) if graph is not None else
-                               ("asynchronous steps: pofa_build(sync=False), all %d tickets verified after the "
-                                "timed loop" % async_checked if async_checked else "synchronous steps")),
+                               ("asynchronous steps: %s, all %d tickets verified after the timed loop%s"
+                                % ("pofa_build_shard(sync=False) (no host wait, no collective in the build)"
+                                   if world > 1 else "pofa_build(sync=False)", async_checked,
+                                   " (every rank's)" if world > 1 else "")
+                                if async_checked else "synchronous steps")),
                 "novel_view_fps": 1e3 / recon_ms if recon_ms else None,
                 "capture_frag_per_s": n_frags / (capture_ms / 1e3) if capture_ms else None,
                 "step_gbs": step_bytes / (ms_step / 1e3) / 1e9, "step_bytes": step_bytes,
