@@ -19,15 +19,17 @@ oracle port on the same inputs.
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port, oracle/fhv_oracle.c, bit-identical to the reference's golden
 vectors) on ALL the host's threads (the port parallelises the capture and
-splat without changing their results; the shipped reference is fastest at
-threads=1 and is ~200x slower still: profiles/r02_shipped_reference.json) on
-the same workload and prints the same JSON line shape and ``config``.
+splat without changing their results; the shipped reference, fastest at
+threads=1, runs ~6.5 k frag/s -- ~575x below the port on one thread, ~1,650x
+below it on 16: profiles/r02_shipped_reference.json) on the same workload
+and prints the same JSON line shape and ``config``.
 Multi-GPU (torchrun, N>1): the same scene is partitioned by Morton range
 (paper_2211_15460_b200/shard.py): each rank bins the
-triangles of its leaf range, captures its slice of the POFA (one all_gather of
-a fragment total per rank for the global offsets) and splats its fragments;
-the frame is composited by depth (NVLink peer-memory slabs, or NCCL
-all-reduces).  Strong scaling: fixed total work; time = max over ranks;
+triangles of its leaf range, captures its slice of the POFA (after the first
+step with no host wait and no collective: every rank's total, hence its
+global base, speculated from the previous build, all ranks' tickets checked
+after the timed loop) and splats its fragments; the frame is composited by
+depth (NVLink peer-memory slabs, or NCCL all-reduces).  Strong scaling: fixed total work; time = max over ranks;
 value = all fragments / that time.
 """
 from __future__ import annotations
