@@ -948,6 +948,11 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
         const bool hi_first = x.persp ? ((float)x.eye[a] > pl[a][1]) : (x.ff[a] < 0.0);
         s |= (hi_first ? 1u : 0u) << a;
       }
+      // perm_mask bit jj = child jj ^ s occupied (the mask's bits permuted by XOR s)
+      unsigned perm_mask = mask;
+      if (s & 1u) perm_mask = ((perm_mask & 0x55u) << 1) | ((perm_mask >> 1) & 0x55u);
+      if (s & 2u) perm_mask = ((perm_mask & 0x33u) << 2) | ((perm_mask >> 2) & 0x33u);
+      if (s & 4u) perm_mask = ((perm_mask & 0x0Fu) << 4) | ((perm_mask >> 4) & 0x0Fu);
       // this lane's children from the certified f32 slab parameters (within
       // e32 of expand_node's f64 values); decisions closer than the margin --
       // and lanes with a d == 0 axis -- take exact_node
@@ -974,13 +979,16 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
           const float m2 = 2.5f * e32;  // two approximations, each within e32
           bool have_next = false;
           float nt = 0.0f;
-#pragma unroll
-          for (int jj = 7; jj >= 0; --jj) {
+          // occupied children, far-first in the shared order (a warp-uniform
+          // loop over set bits; the planes selected per bit)
+          for (unsigned pm = perm_mask; pm; ) {
+            const int jj = 31 - __clz(pm);
+            pm &= ~(1u << jj);
             const int c = jj ^ (int)s;
-            if (!((mask >> c) & 1u)) continue;
-            const int jx = jj & 1, jy = (jj >> 1) & 1, jz = jj >> 2;
-            const float t0 = fmaxf(fmaxf(fmaxf(0.0f, en[0][jx]), en[1][jy]), en[2][jz]);
-            const float t1 = fminf(fminf(ex[0][jx], ex[1][jy]), ex[2][jz]);
+            const bool jx = jj & 1, jy = (jj >> 1) & 1, jz = (jj >> 2) & 1;
+            const float t0 = fmaxf(fmaxf(fmaxf(0.0f, jx ? en[0][1] : en[0][0]), jy ? en[1][1] : en[1][0]),
+                                   jz ? en[2][1] : en[2][0]);
+            const float t1 = fminf(fminf(jx ? ex[0][1] : ex[0][0], jy ? ex[1][1] : ex[1][0]), jz ? ex[2][1] : ex[2][0]);
             const float gap = t1 - t0;
             if (gap > m2) {
               hits |= 1u << c;
@@ -1010,10 +1018,10 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
       // order pops next
       const E lvl = (E)((E)(level + 1) << SC::kShift);
       const int sp0 = sp;
-#pragma unroll
-      for (int jj = 7; jj >= 0; --jj) {
+      for (unsigned pm = perm_mask; pm; ) {
+        const int jj = 31 - __clz(pm);
+        pm &= ~(1u << jj);
         const int c = jj ^ (int)s;
-        if (!((mask >> c) & 1u)) continue;
         const unsigned b = __ballot_sync(full, (hits >> c) & 1u);
         if (b) {
           if (lane == 0) {
