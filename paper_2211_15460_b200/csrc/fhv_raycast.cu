@@ -553,7 +553,10 @@ constexpr int kPktWarps = 4;  // 128-thread CTAs
 // shared stack: 7 per level for the shared order plus room for the lanes
 // that take their own order at a node (ties); a push that would not fit hands
 // those lanes to the per-ray kernel instead
-constexpr int kPktStack = 16 * kRayMaxLevels + 8;
+#ifndef FHV_PKT_STACK
+#define FHV_PKT_STACK (16 * kRayMaxLevels + 8)  // tests build a tiny one to force the hand-off path
+#endif
+constexpr int kPktStack = FHV_PKT_STACK;
 template <class E>
 struct PktShared {
   E node[kPktStack];
@@ -1015,9 +1018,16 @@ __global__ void __launch_bounds__(32 * kPktWarps, FHV_PKT_MINB) k_raycast_packet
         }
       }
       // children in reverse shared order: pushed far-first, so the shared
-      // order pops next
+      // order pops next.  The shared pushes alone stay below 7 L + 1 entries;
+      // own-order push sets (ties) can fill the stack: a push that would not
+      // fit hands every lane of this node to the per-ray kernel instead
       const E lvl = (E)((E)(level + 1) << SC::kShift);
       const int sp0 = sp;
+      if (sp + __popc(perm_mask) > kPktStack) {
+        irregular |= M;
+        active &= ~M;
+        continue;
+      }
       for (unsigned pm = perm_mask; pm; ) {
         const int jj = 31 - __clz(pm);
         pm &= ~(1u << jj);
