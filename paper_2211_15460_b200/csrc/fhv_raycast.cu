@@ -583,6 +583,12 @@ __device__ __forceinline__ void pkt_for_leaf(const RayParams& x, long long code,
 // sorted insertion into the register buffer (compile-time indices only: the
 // candidate walks up, swapping with every larger entry; the largest falls off)
 __device__ __forceinline__ void pkt_insert(double t, int k, double bt[kPktHits], int bi[kPktHits], int& nb) {
+  if (nb == 0) {  // a ray's first hit in the leaf (the common case): no compare-and-shift
+    bt[0] = t;
+    bi[0] = k;
+    nb = 1;
+    return;
+  }
   if (nb == kPktHits && !hit_less(t, k, bt[kPktHits - 1], bi[kPktHits - 1])) return;
 #pragma unroll
   for (int q = 0; q < kPktHits; ++q) {
