@@ -526,6 +526,26 @@ def extra_config(args):
                                   "note": "packet traversal, latency bound (register-limited occupancy), see "
                                           "profiles/"},
                      "clocks": clk.summary()})
+        if not subtrees and not args.profile_only:
+            # SURVEY.md section 8(d) C5 "(and splat)": the same views reconstructed
+            # by exact z-tested splatting (r = 1/1080, C3's capture pitch)
+            sbuf = img_buf(W, H)
+
+            def step_splat():
+                for v, sh in zip(views, shs):
+                    fhv.splat_render(vol.pool, v, [headlight(v)], 1.0 / 1080, scene.materials, out=sbuf, shading=sh)
+            for _ in range(max(1, args.warmup)):
+                step_splat()
+            ms_s, _ = _timed(step_splat, args.steps, stream)
+            if world > 1:
+                t = torch.tensor([ms_s], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms_s = float(t.item())
+            sst, _ = _stage_profile(step_splat, 1, dev)
+            line["splat"] = {"value": len(all_views) / (ms_s / 1e3), "unit": "frames/s", "ms_per_step": ms_s,
+                             "stage_ms": {k: round(v, 4) for k, v in sst.items()},
+                             "note": "64 x 3840x2160 exact splats of the same POFA (depth pass, index pass, "
+                                     "resolve per view)"}
         if not args.no_cpu_baseline and rank == 0 and world == 1:
             from oracle import oracle as orc
             ref = orc.pofa_build(scene, ns, cfg, 8)
