@@ -454,6 +454,23 @@ def extra_config(args):
             line["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": round(algo / t / 1e9, 1), "peak": peak,
                                 "unit": "GB/s", "frac": round(algo / t / 1e9 / peak, 4), "traffic": None,
                                 "algorithmic_bytes": algo, "peak_kind": peak_kind}
+        if not args.profile_only:
+            # SURVEY.md section 8(d) C4 "optional raycast R/T": one 1080p
+            # perspective view through all 80 translucent layers of the POFA
+            vol4 = fhv.pofa_build(scene, one, cfg, 8, device=dev)
+            view4 = viewpoint_camera("+z", (1920, 1080), "perspective")
+            rc4 = fhv.default_raycast_config(vol4)
+            sh4 = DeviceShading(scene.materials, [headlight(view4)], dev)
+            buf4 = img_buf(1920, 1080)
+
+            def step_ray4():
+                buf4.pixels.zero_()
+                return fhv.render_raycast(vol4, view4, [headlight(view4)], rc4, out=buf4, sync=False, shading=sh4)[1]
+            step_ray4()
+            ms_r, st4 = _timed(step_ray4, max(1, min(args.steps, 5)), stream)
+            line["raycast"] = {"value": 1e3 / ms_r, "unit": "frames/s", "ms_per_view": ms_r,
+                               "view": "viewpoint_camera('+z', 1920x1080, perspective), transparency, cutoff 1.0",
+                               "raycast_stats": fhv.RaycastStats(*st4.counters.cpu().tolist()).as_dict()}
     else:  # C5
         scene = sample_scenes.scatter1m()
         cam = capture_camera(scene, "+z", 1080)

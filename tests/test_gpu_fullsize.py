@@ -222,3 +222,26 @@ def test_c5_4k_views_from_one_pofa_band():
         want = orgba.reshape(-1, 4)[band[0] * 3840:band[1] * 3840]
         assert st.as_dict() == ost
         assert np.max(np.abs(got - want)) <= 1e-12
+
+
+def test_c4_depth_complexity_raycast_band():
+    """C4's optional ray cast: rays through up to 80 translucent
+    layers (tens of hits per ray, long leaf lists) -- a row band of the 1080p
+    view vs the oracle: RaycastStats exact, rgba within 1e-12.  Captured at
+    384^2 so the oracle's POFA stays small."""
+    s = _scene("layers80")
+    cfg = fhv.RasterConfig.from_camera(capture_camera(s, "+z", 384))
+    one = fhv.CaptureStrategy.one_view()
+    vol = fhv.pofa_build(s, one, cfg, 8, exact_order=True)
+    ref = orc.pofa_build(s, one, cfg, 8)
+    view = viewpoint_camera("+z", (1920, 1080), "perspective")
+    lights = [headlight(view)]
+    rc = fhv.default_raycast_config(vol)
+    band = (536, 544)
+    img, st = fhv.render_raycast(vol, view, lights, rc, rows=band)
+    orgba, ost, _ = orc.raycast(ref, view, lights, rc.splat_radius_world, materials=s.materials, rows=band)
+    got = img.pixels.cpu().numpy().reshape(-1, 4)[band[0] * 1920:band[1] * 1920]
+    want = orgba.reshape(-1, 4)[band[0] * 1920:band[1] * 1920]
+    assert st.as_dict() == ost
+    assert ost["hits"] > 20 * 1920 * (band[1] - band[0]) // 4  # deep: many layers per ray
+    assert np.max(np.abs(got - want)) <= 1e-12
