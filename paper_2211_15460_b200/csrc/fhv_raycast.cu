@@ -519,24 +519,28 @@ __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
 //
 // The DFS stack lives in shared memory and each entry carries the mask of the
 // lanes whose ray reached that node, so every node is expanded by the whole
-// warp in lock-step (the per-lane slab arithmetic is exactly expand_node's)
-// and every leaf's fragment list is walked once, its loads broadcast to the
-// lanes that test it.  The warp pushes the children in ONE shared order: for
-// rays leaving a common eye (perspective) or along a common direction
-// (orthographic) the children a ray meets form a chain across the node's
-// three centre planes, and ordering them by (child XOR s) -- s = the eye's /
-// the ray's entry side of each plane -- is a front-to-back order for every
-// ray of the tile.  Each lane checks at every node that the shared order of
-// the children IT meets is its own (t_enter, child) order (the reference's
-// insertion sort, fhv/_ckern.pyx:580-632); a lane where it is not (ties of
-// rounded entry distances) leaves the packet and its ray is re-run, from
-// scratch, by the per-ray kernel (k_raycast in list mode), so every ray's
-// visit sequence -- and with it the image and RaycastStats -- is the
-// reference's.
+// warp in lock-step and every leaf's fragment list is walked once, its loads
+// broadcast to the lanes that test it.  The warp pushes the children in ONE
+// shared order: for rays leaving a common eye (perspective) or along a common
+// direction (orthographic) the children a ray meets form a chain across the
+// node's three centre planes, and ordering them by (child XOR s) -- s = the
+// eye's / the rays' entry side of each plane -- is a front-to-back order for
+// every ray of the tile.  Each lane checks at every node that the shared
+// order of the children IT meets is its own (t_enter, child) order (the
+// reference's insertion sort, fhv/_ckern.pyx:580-632); where it is not (ties
+// of rounded entry distances) the lane's children are pushed in its own order
+// instead, above the shared ones (see the node code), so every ray's visit
+// sequence -- and with it the image and RaycastStats -- is the reference's.
+// The slab decisions use certified f32 plane parameters, with the exact f64
+// expansion (exact_node) wherever a decision falls inside the error margin.
+// A push that would overflow the stack hands the affected rays to the
+// per-ray kernel (k_raycast in list mode), which re-runs them from scratch.
 //
-// Hits are shaded warp-wide: the hits all lanes deliver from a leaf are laid
-// out lane-major in shared memory, each lane shades one of every 32, and each
-// lane then composites its own hits in (t, index) order.
+// Shading is deferred: a delivered hit's compositing weight (1 - acc) * alpha
+// needs only the material alphas, so each lane queues (pool index, weight)
+// records in hit order; at the tile's end (or when a queue fills) the warp
+// shades all queued hits 32 wide and each lane accumulates its colour in
+// queue order (pkt_flush).
 #ifndef FHV_PKT_HITS
 #define FHV_PKT_HITS 4  // per-lane buffered hits per leaf (more: exact rescans)
 #endif
