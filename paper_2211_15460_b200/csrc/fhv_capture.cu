@@ -491,6 +491,9 @@ enum RasterMode { kCnt = 0, kCntLeaves = 1, kList = 2, kPpfl = 3, kPofl = 4, kPo
 #ifndef FHV_RASTER_MINB
 #define FHV_RASTER_MINB 3  // resident CTAs per SM the raster kernels are register-budgeted for
 #endif
+#ifndef FHV_RASTER_PER_SM
+#define FHV_RASTER_PER_SM 16  // raster / emission grid: CTAs per SM (grid-stride over item groups)
+#endif
 #ifndef FHV_RASTER_BLOCK
 #define FHV_RASTER_BLOCK 256
 #endif
@@ -1880,13 +1883,18 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_leaf_fix(PoolRefs pl, const 
       if (q >= nmv) continue;
       const int i = S.mv_i[q], lo = S.mv_lo[q], hi = S.mv_hi[q];
       const uint32_t rr = S.rk[i];
+      // the record's loads issue before the counting loop (their latency
+      // overlaps it)
+      const long long s_ = t0 + i;
+      const float p0 = pl.pos[3 * s_], p1 = pl.pos[3 * s_ + 1], p2 = pl.pos[3 * s_ + 2];
+      const float n0 = pl.nrm[3 * s_], n1 = pl.nrm[3 * s_ + 1], n2 = pl.nrm[3 * s_ + 2];
+      const uint32_t mt = pl.mat[s_], ob = pl.obj[s_];
       int d = lo;
       for (int j = lo; j < hi; ++j) d += S.rk[j] < rr ? 1 : 0;
-      const long long s_ = t0 + i;
-      S.pos[d][0] = pl.pos[3 * s_]; S.pos[d][1] = pl.pos[3 * s_ + 1]; S.pos[d][2] = pl.pos[3 * s_ + 2];
-      S.nrm[d][0] = pl.nrm[3 * s_]; S.nrm[d][1] = pl.nrm[3 * s_ + 1]; S.nrm[d][2] = pl.nrm[3 * s_ + 2];
-      S.mat[d] = pl.mat[s_];
-      S.obj[d] = pl.obj[s_];
+      S.pos[d][0] = p0; S.pos[d][1] = p1; S.pos[d][2] = p2;
+      S.nrm[d][0] = n0; S.nrm[d][1] = n1; S.nrm[d][2] = n2;
+      S.mat[d] = mt;
+      S.obj[d] = ob;
       S.rank[d] = rr;
       S.dst_set[d] = 1;
     }
@@ -2311,7 +2319,7 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
     o.levels = levels;
     o.leaf_counts = leaf_counts;
     o.tile_sums = tile_sums;
-    const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
+    const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock, FHV_RASTER_PER_SM);
     const bool fast = leaves && use_fast_math(ctx);
     if (fast) smem_opt_in(k_raster<kCntLeaves, false, true>, kRasterDyn);
     {
@@ -2361,7 +2369,7 @@ int emit(fhv_ctx* ctx, const CaptureParams& p, const EmitOut& o, bool atomic_all
       return check_cuda(ctx, cudaGetLastError());
     }
   }
-  const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock);
+  const int grid = grid_for((n + 31) / 32 * 32, kRasterBlock, FHV_RASTER_PER_SM);
   {
     LaunchScope L_(ctx, kMode >= kDsDepth ? kStDeferred : kStEmitList + (kMode - kList), s);
     if (atomic_alloc)
