@@ -1774,7 +1774,10 @@ __device__ __forceinline__ void unstage_record(const PoolRefs& pl, const uint32_
 constexpr int kFixChunks = 6;
 constexpr int kFixWarpTile = 128;                     // segments starting here are this warp's
 constexpr int kFixWarpRegion = 32 * kFixChunks;       // 192
-constexpr int kFixWarps = 4;                          // warps per CTA
+#ifndef FHV_FIX_WARPS
+#define FHV_FIX_WARPS 2
+#endif
+constexpr int kFixWarps = FHV_FIX_WARPS;              // warps per CTA
 
 struct FixWarpSmem {
   uint32_t rk[kFixWarpRegion];
@@ -2303,7 +2306,8 @@ inline bool use_fast_math(const fhv_ctx* ctx) {
 
 // counts per item (+ leaf histogram) and their scan (fragment ranks); async
 int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_t* leaf_counts, cudaStream_t s,
-          bool ranks = true, uint32_t* tile_sums = nullptr) {
+          bool ranks = true, uint32_t* tile_sums = nullptr, bool defer_ranks = false) {
+  ctx->item_scan_n = -1;
   const long long n = ctx->n_items;
   uint32_t* item_cnt = (uint32_t*)scratch(ctx, kItemCnt, (size_t)(n > 0 ? n : 1) * 4);
   auto* item_off = (unsigned long long*)scratch(ctx, kItemOff, (size_t)(n > 0 ? n : 1) * 8);
@@ -2341,6 +2345,11 @@ int count(fhv_ctx* ctx, const CaptureParams& p, bool leaves, int levels, uint32_
   // item fragment offsets = emission ranks; a POFA build that keeps no
   // emission order (atomic in-leaf order) needs neither them nor their total
   if (!ranks) return FHV_OK;
+  if (defer_ranks) {  // the directory launch scans them (scan_leaves_and_pyramid)
+    ctx->item_scan_n = n;
+    ctx->item_scan_dev = nd;
+    return FHV_OK;
+  }
   return scan_u32_to_u64(ctx, item_cnt, item_off, n, s, nd);
 }
 
@@ -2354,6 +2363,7 @@ int emit(fhv_ctx* ctx, const CaptureParams& p, const EmitOut& o, bool atomic_all
   const auto* io = (const unsigned long long*)ctx->bufs[kItemOff].ptr;
   const auto* im = (const uint4*)ctx->bufs[kItemMask].ptr;
   const unsigned long long* nd = items_dev(ctx);
+  if (int rc = run_deferred_item_scan(ctx, s)) return rc;  // (normally already fused into the directory)
   if constexpr (kMode == kPpfl || kMode == kPofl || kMode == kPofa) {
     if (!(o.flags & kExactMath) && use_fast_math(ctx)) {
       const int gridf = grid_for((n + 31) / 32 * 32, 32 * kEmitFastWarps);
@@ -2646,7 +2656,7 @@ namespace {
 // item scan's total is parked in ctl->frags_total for the caller's next sync
 int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg, int32_t levels,
                      const fhv_shard_t* shard, uint32_t* counts_local, cudaStream_t s, CaptureParams& p,
-                     bool spec = false, bool ranks = true, bool reuse_bin = false) {
+                     bool spec = false, bool ranks = true, bool reuse_bin = false, bool defer_ranks = false) {
   ctx->pass1_levels = -1;
   ctx->pass1_ranks = ranks;
   int rc;
@@ -2666,8 +2676,9 @@ int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg
     if ((rc = check_cuda(ctx, cudaMemsetAsync(tile_sums, 0, nt * 4, s)))) return rc;
     ctx->dir_sums_levels = levels;
   }
-  if ((rc = count(ctx, p, true, levels, counts_local, s, ranks, tile_sums))) return rc;
-  if (!ranks) return FHV_OK;  // the total comes from the directory scan (caller)
+  // deferred ranks ride in the directory launch (whole-directory builds with tile totals)
+  if ((rc = count(ctx, p, true, levels, counts_local, s, ranks, tile_sums, defer_ranks && tile_sums))) return rc;
+  if (!ranks || ctx->item_scan_n >= 0) return FHV_OK;  // the total comes from the directory scan (caller)
   return check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total, sizeof(unsigned long long),
                                          cudaMemcpyDeviceToDevice, s));
 }
@@ -2901,10 +2912,13 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   const bool ranks = (flags & FHV_EXACT_ORDER) != 0;
   CaptureParams p;
   // speculative item plan when this ctx has one for the job count (else plan() syncs once)
-  if ((rc = pofa_count_async(ctx, tris, cfg, levels, nullptr, counts, s, p, true, ranks))) return rc;
+  // (the emission ranks' scan rides in the directory launch)
+  if ((rc = pofa_count_async(ctx, tris, cfg, levels, nullptr, counts, s, p, true, ranks, false, true))) return rc;
+  const bool deferred = ctx->item_scan_n >= 0;
   if ((rc = fhv_pofa_shard_directory_nocheck(ctx, levels, counts, offsets, pyramid, s))) return rc;
-  if (!ranks && (rc = check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total,
-                                                      sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s))))
+  if ((!ranks || deferred) &&
+      (rc = check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total, sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToDevice, s))))
     return rc;
   if ((rc = pofa_scatter_async(ctx, p, levels, 0, n_leaves, counts, offsets, 0, pool, flags, s, false,
                                 &ctx->ctl->frags_total, 0)))

@@ -90,6 +90,11 @@ struct fhv_ctx {
   // levels of the directory tile totals the last counting pass left in
   // bufs[kTileSums] (-1: none; consumed by scan_leaves_and_pyramid)
   int dir_sums_levels = -1;
+  // an item-rank scan (bufs[kItemCnt] -> bufs[kItemOff]) the counting pass
+  // deferred to the directory launch: item count (-1: none) and its
+  // device-side count (speculative plan) or null
+  int64_t item_scan_n = -1;
+  const unsigned long long* item_scan_dev = nullptr;
   int last_cuda_error = 0;
 };
 
@@ -121,10 +126,13 @@ int reset_control(fhv_ctx* ctx, cudaStream_t s);
 // exclusive scans (decoupled look-back, single pass); total lands in ctl->scan_total
 // n_dev: optional device-side element count (<= n) for a speculatively sized launch
 int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, int64_t n, cudaStream_t s,
-                    const unsigned long long* n_dev = nullptr);
+                    const unsigned long long* n_dev = nullptr, bool write_total = true);
 // POFA directory: offsets = excl-scan(counts), pyramid level L-1 from counts > 0, then upper levels
+// (+ a pending deferred item-rank scan, ctx->item_scan_n)
 int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
                             int levels, cudaStream_t s);
+// the deferred item-rank scan on its own (no-op when none is pending)
+int run_deferred_item_scan(fhv_ctx* ctx, cudaStream_t s);
 // leaves per directory tile (4096 for L = 4, 32768 for L >= 5, 0 below): shard ranges are multiples
 long long dir_tile_leaves(int levels);
 // shard variant: counts/offsets cover leaves [lo, hi) (multiples of dir_tile_leaves); stored offsets get

@@ -23,11 +23,12 @@ namespace fhv {
 
 namespace {
 
+// one tile of the u32 -> u64 exclusive scan (ticket order, decoupled
+// look-back); write_total: the last tile stores the total in ctl->scan_total
 template <int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restrict__ in,
-                                                       unsigned long long* __restrict__ out, int64_t n,
-                                                       uint64_t* status, Control* ctl, unsigned n_tiles,
-                                                       const unsigned long long* n_dev) {
+__device__ __forceinline__ void scan_tile_u32_u64(const uint32_t* __restrict__ in, unsigned long long* __restrict__ out,
+                                                  int64_t n, uint64_t* status, Control* ctl, unsigned n_tiles,
+                                                  const unsigned long long* n_dev, bool write_total) {
   __shared__ unsigned tile_s;
   __shared__ uint64_t prefix_s, total_s;
   if (threadIdx.x == 0) tile_s = draw_tile(ctl, n_tiles);
@@ -37,7 +38,7 @@ __global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restri
     if ((int64_t)*n_dev < n) n = (int64_t)*n_dev;
     n_tiles = (unsigned)((n + (int64_t)BLOCK * ITEMS - 1) / ((int64_t)BLOCK * ITEMS));
     if (tile >= n_tiles) {
-      if (tile == 0 && threadIdx.x == 0) ctl->scan_total = 0;
+      if (write_total && tile == 0 && threadIdx.x == 0) ctl->scan_total = 0;
       return;
     }
   }
@@ -79,7 +80,15 @@ __global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restri
       run += v[i];
     }
   }
-  if (threadIdx.x == 0 && tile == n_tiles - 1) ctl->scan_total = prefix_s + total_s;
+  if (write_total && threadIdx.x == 0 && tile == n_tiles - 1) ctl->scan_total = prefix_s + total_s;
+}
+
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restrict__ in,
+                                                       unsigned long long* __restrict__ out, int64_t n,
+                                                       uint64_t* status, Control* ctl, unsigned n_tiles,
+                                                       const unsigned long long* n_dev, int write_total) {
+  scan_tile_u32_u64<BLOCK, ITEMS>(in, out, n, status, ctl, n_tiles, n_dev, write_total != 0);
 }
 
 // POFA leaves: thread = one level-(L-1) node (8 leaves)
@@ -380,6 +389,17 @@ __device__ __forceinline__ uint4* swz(uint32_t* chunk, unsigned t, unsigned q) {
 
 static_assert(kDbTile == (1ll << kDirSumShift) || kDbChunks != 2, "tile totals match the tile");
 
+// deferred item-rank scan riding in the directory launch (k_dir_tma)
+struct ItemScan {
+  const uint32_t* cnt;
+  unsigned long long* off;
+  int64_t n;
+  const unsigned long long* n_dev;
+  uint64_t* status;
+  unsigned tiles;  // 0: none
+};
+constexpr int kItemScanItems = 32;  // 256 x 32 = 8192 items per tile
+
 #ifndef FHV_DIR_MINB
 #define FHV_DIR_MINB 3
 #endif
@@ -387,7 +407,17 @@ __global__ void __launch_bounds__(kDbThreads, FHV_DIR_MINB) k_dir_tma(const __gr
                                                          const __grid_constant__ CUtensorMap tm_offsets,
                                                          uint8_t* __restrict__ pyr, int levels, uint64_t* status,
                                                          Control* ctl, unsigned n_tiles, unsigned tile0,
-                                                         uint64_t base, const uint32_t* __restrict__ tile_sums) {
+                                                         uint64_t base, const uint32_t* __restrict__ tile_sums,
+                                                         ItemScan is) {
+  // the first is.tiles CTAs scan the items' fragment counts into emission
+  // ranks (their own tickets and look-back; the directory tiles below use
+  // blockIdx with the counting pass's tile totals): two independent scans of
+  // one counting pass in one launch, the ranks' look-back chain hidden
+  // behind the directory's streaming
+  if (blockIdx.x < is.tiles) {
+    scan_tile_u32_u64<kDbThreads, kItemScanItems>(is.cnt, is.off, is.n, is.status, ctl, is.tiles, is.n_dev, false);
+    return;
+  }
   extern __shared__ __align__(1024) unsigned char dyn[];  // kDbChunks x 32 KB, 1024-B aligned (swizzle atoms)
   uint32_t* buf = reinterpret_cast<uint32_t*>(dyn + ((1024u - (smem_u32(dyn) & 1023u)) & 1023u));
   __shared__ __align__(8) uint64_t bar[kDbChunks];
@@ -399,7 +429,7 @@ __global__ void __launch_bounds__(kDbThreads, FHV_DIR_MINB) k_dir_tma(const __gr
   if (tid == 0) {
     // with the counting pass's tile totals the tiles are independent (blockIdx);
     // else ticket order: the look-back never waits on an unstarted tile
-    const unsigned t = tile_sums ? blockIdx.x : draw_tile(ctl, n_tiles);
+    const unsigned t = tile_sums ? blockIdx.x - is.tiles : draw_tile(ctl, n_tiles);
     tile_s = t;
     for (int j = 0; j < kDbChunks; ++j) mbar_init(&bar[j], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -567,7 +597,7 @@ inline int grid_for(int64_t n, int block) {
 }  // namespace
 
 int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, int64_t n, cudaStream_t s,
-                    const unsigned long long* n_dev) {
+                    const unsigned long long* n_dev, bool write_total) {
 #ifndef FHV_SCAN_B
 #define FHV_SCAN_B 512
 #define FHV_SCAN_I 16
@@ -576,6 +606,7 @@ int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, i
   const int64_t per = (int64_t)B * I;
   const unsigned tiles = (unsigned)((n + per - 1) / per);
   if (n <= 0) {
+    if (!write_total) return FHV_OK;
     return check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->scan_total, 0, sizeof(unsigned long long), s));
   }
   uint64_t* st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)tiles * sizeof(uint64_t));
@@ -584,7 +615,7 @@ int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, i
   if (rc) return rc;
   {
     LaunchScope L_(ctx, kStScan, s);
-    k_scan_u32_u64<B, I><<<tiles, B, 0, s>>>(in, out, n, st, ctx->ctl, tiles, n_dev);
+    k_scan_u32_u64<B, I><<<tiles, B, 0, s>>>(in, out, n, st, ctx->ctl, tiles, n_dev, write_total ? 1 : 0);
   }
   return check_cuda(ctx, cudaGetLastError());
 }
@@ -673,15 +704,27 @@ static bool rows_tensor_map(CUtensorMap* tm, const uint32_t* base, uint64_t n_le
 
 static int launch_dir_bulk(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid, int levels,
                            cudaStream_t s, uint64_t lo, uint64_t hi, uint64_t base,
-                           const uint32_t* tile_sums = nullptr) {
+                           const uint32_t* tile_sums = nullptr, bool* ranks_done = nullptr) {
   const unsigned tiles = (unsigned)((hi - lo) / (uint64_t)kDbTile);
   const unsigned tile0 = (unsigned)(lo / (uint64_t)kDbTile);
   CUtensorMap tm_c, tm_o;
   if (!rows_tensor_map(&tm_c, counts + lo, hi - lo) || !rows_tensor_map(&tm_o, offsets + lo, hi - lo))
     return launch_dir_tiles(ctx, true, counts, offsets, nullptr, pyramid, levels, s, lo, hi, base);
-  uint64_t* st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)tiles * sizeof(uint64_t));
+  // a pending item-rank scan rides along (tile totals given: the directory
+  // tiles take no tickets)
+  ItemScan is{nullptr, nullptr, 0, nullptr, nullptr, 0u};
+  const int64_t pend = ctx->item_scan_n;
+  if (ranks_done && tile_sums && pend > 0) {
+    is.cnt = (const uint32_t*)ctx->bufs[kItemCnt].ptr;
+    is.off = (unsigned long long*)ctx->bufs[kItemOff].ptr;
+    is.n = pend;
+    is.n_dev = ctx->item_scan_dev;
+    is.tiles = (unsigned)((pend + (int64_t)kDbThreads * kItemScanItems - 1) / ((int64_t)kDbThreads * kItemScanItems));
+  }
+  uint64_t* st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)(tiles + is.tiles) * sizeof(uint64_t));
   if (!st) return FHV_NOMEM;
-  int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)tiles * sizeof(uint64_t), s));
+  is.status = st + tiles;
+  int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)(tiles + is.tiles) * sizeof(uint64_t), s));
   if (rc) return rc;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->dir_ticket, 0, 8, s)))) return rc;  // (done counter)
   constexpr int kSmem = kDbChunks * kDbBytes + 1024;
@@ -692,9 +735,10 @@ static int launch_dir_bulk(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offse
   }
   {
     LaunchScope L_(ctx, kStScanLeaves, s);
-    k_dir_tma<<<tiles, kDbThreads, kSmem, s>>>(tm_c, tm_o, pyramid, levels, st, ctx->ctl, tiles, tile0, base,
-                                                 tile_sums);
+    k_dir_tma<<<tiles + is.tiles, kDbThreads, kSmem, s>>>(tm_c, tm_o, pyramid, levels, st, ctx->ctl, tiles, tile0,
+                                                            base, tile_sums, is);
   }
+  if (ranks_done && is.tiles) *ranks_done = true;
   return check_cuda(ctx, cudaGetLastError());
 }
 
@@ -706,14 +750,40 @@ static bool dir_stream_enabled() {
   return v != 0;
 }
 
+static int scan_leaves_and_pyramid_impl(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
+                                        int levels, cudaStream_t s, bool* ranks_done);
+
+// + the item-rank scan a counting pass deferred to here (fhv_capture.cu
+// count()): fused into the directory launch when it streams with tile totals,
+// else its own scan first
 int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
                             int levels, cudaStream_t s) {
+  const int64_t pend = ctx->item_scan_n;
+  bool done = pend <= 0;
+  int rc = scan_leaves_and_pyramid_impl(ctx, counts, offsets, pyramid, levels, s, done ? nullptr : &done);
+  if (rc || done) {
+    ctx->item_scan_n = -1;
+    return rc;
+  }
+  return run_deferred_item_scan(ctx, s);  // not fused: its own scan (the directory's total stays)
+}
+
+int run_deferred_item_scan(fhv_ctx* ctx, cudaStream_t s) {
+  const int64_t pend = ctx->item_scan_n;
+  ctx->item_scan_n = -1;
+  if (pend <= 0) return FHV_OK;
+  return scan_u32_to_u64(ctx, (const uint32_t*)ctx->bufs[kItemCnt].ptr, (unsigned long long*)ctx->bufs[kItemOff].ptr,
+                         pend, s, ctx->item_scan_dev, false);
+}
+
+static int scan_leaves_and_pyramid_impl(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
+                                        int levels, cudaStream_t s, bool* ranks_done) {
   if (levels >= 5 && dir_stream_enabled()) {
     // the counting pass's per-tile totals, when it left them for this directory (one use)
     const uint32_t* sums = (ctx->dir_sums_levels == levels && kDbChunks == 2) ? (const uint32_t*)ctx->bufs[kTileSums].ptr
                                                                              : nullptr;
     ctx->dir_sums_levels = -1;
-    return launch_dir_bulk(ctx, counts, offsets, pyramid, levels, s, 0, 1ull << (3 * levels), 0, sums);
+    return launch_dir_bulk(ctx, counts, offsets, pyramid, levels, s, 0, 1ull << (3 * levels), 0, sums, ranks_done);
   }
   if (levels >= 4) return launch_dir_tiles(ctx, true, counts, offsets, nullptr, pyramid, levels, s);
   constexpr int B = 256;
