@@ -2216,11 +2216,21 @@ int validate(const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg) {
   return FHV_OK;
 }
 
+// FHV_FUSED_EXPAND=0: the speculative plan's separate scan + item expansion (A/B)
+inline bool fused_expand_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("FHV_FUSED_EXPAND");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 // job setup + work-item expansion.  The number of work items is data
 // dependent.  Exact path: sync once, size the item buffers.  Speculative path
 // (allow_spec, same job count as the last exact plan on this ctx): launch on
-// the grow-only buffers of that plan without waiting; every item kernel reads
-// the true count from ctl->items_total, k_item_expand raises FHV_RETRY_ITEMS
+// the grow-only buffers of that plan without waiting -- the job scan and the
+// item expansion as one pass (k_item_scan_expand); every item kernel reads
+// the true count from ctl->items_total, the expansion raises FHV_RETRY_ITEMS
 // if it does not fit, and the caller's final sync re-plans exactly.
 int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s, bool allow_spec = false) {
   int rc = reset_control(ctx, s);
@@ -2238,11 +2248,21 @@ int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s, bool allow_spec =
     k_job_setup<<<grid_for(p.n_jobs, 128), 128, 0, s>>>(p, jobs, job_items, &ctx->ctl->status);
   }
   if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
+  const bool spec = allow_spec && ctx->last_n_jobs == p.n_jobs && ctx->item_cap > 0;
+  if (spec && fused_expand_enabled()) {  // item buffers sized by the last exact plan: scan + expand in one pass
+    const long long n_items = ctx->item_cap;
+    uint32_t* item_job = (uint32_t*)scratch(ctx, kItemJob, (size_t)n_items * 4);
+    uint32_t* item_p0 = (uint32_t*)scratch(ctx, kItemP0, (size_t)n_items * 4);
+    if (!item_job || !item_p0) return FHV_NOMEM;
+    ctx->n_items = n_items;
+    ctx->spec = true;
+    return scan_expand_items(ctx, job_items, job_item_off, p.n_jobs, item_job, item_p0, (unsigned long long)n_items,
+                             kItemPix, s);
+  }
   if ((rc = scan_u32_to_u64(ctx, job_items, job_item_off, p.n_jobs, s))) return rc;
   if ((rc = check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->items_total, &ctx->ctl->scan_total, sizeof(unsigned long long),
                                             cudaMemcpyDeviceToDevice, s))))
     return rc;
-  const bool spec = allow_spec && ctx->last_n_jobs == p.n_jobs && ctx->item_cap > 0;
   long long n_items;
   if (spec) {
     n_items = ctx->item_cap;

@@ -131,6 +131,11 @@ int scan_u32_to_u64(fhv_ctx* ctx, const uint32_t* in, unsigned long long* out, i
 // (+ a pending deferred item-rank scan, ctx->item_scan_n)
 int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offsets, uint8_t* pyramid,
                             int levels, cudaStream_t s);
+// speculative capture plan: job item counts -> offsets + the item records in
+// one launch (item total -> ctl->items_total; FHV_RETRY_ITEMS past cap)
+int scan_expand_items(fhv_ctx* ctx, const uint32_t* job_items, unsigned long long* job_item_off, int64_t n_jobs,
+                      uint32_t* item_job, uint32_t* item_p0, unsigned long long cap, uint32_t item_pix,
+                      cudaStream_t s);
 // the deferred item-rank scan on its own (no-op when none is pending)
 int run_deferred_item_scan(fhv_ctx* ctx, cudaStream_t s);
 // leaves per directory tile (4096 for L = 4, 32768 for L >= 5, 0 below): shard ranges are multiples

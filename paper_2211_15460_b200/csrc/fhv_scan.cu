@@ -91,6 +91,95 @@ __global__ void __launch_bounds__(BLOCK) k_scan_u32_u64(const uint32_t* __restri
   scan_tile_u32_u64<BLOCK, ITEMS>(in, out, n, status, ctl, n_tiles, n_dev, write_total != 0);
 }
 
+// job item counts -> item offsets AND the item records in one pass (the
+// speculative capture plan, fhv_capture.cu plan()): a tile of jobs is scanned
+// (ticket order, decoupled look-back), then its jobs' items are written --
+// small jobs by their own lane, big ones by the whole warp (ballot loop).
+// The last tile stores the item total in ctl->items_total.
+#ifndef FHV_EXP_ITEMS
+#define FHV_EXP_ITEMS 4
+#endif
+constexpr int kExpBlock = 256, kExpItems = FHV_EXP_ITEMS;  // jobs per thread (tile = 256 x kExpItems jobs)
+__global__ void __launch_bounds__(kExpBlock) k_item_scan_expand(const uint32_t* __restrict__ job_items,
+                                                               unsigned long long* __restrict__ job_item_off,
+                                                               int64_t n_jobs, uint32_t* __restrict__ item_job,
+                                                               uint32_t* __restrict__ item_p0, unsigned long long cap,
+                                                               uint32_t item_pix, uint64_t* status, Control* ctl,
+                                                               unsigned n_tiles) {
+  constexpr int kT = kExpBlock * kExpItems;
+  __shared__ unsigned tile_s;
+  __shared__ uint64_t prefix_s, total_s;
+  __shared__ uint32_t cnt_s[kT];
+  __shared__ unsigned long long off_s[kT];
+  if (threadIdx.x == 0) tile_s = draw_tile(ctl, n_tiles);
+  __syncthreads();
+  const unsigned tile = tile_s;
+  const int64_t t0 = (int64_t)tile * kT;
+  // counts striped (coalesced) into shared memory, scanned blocked
+#pragma unroll
+  for (int i = 0; i < kExpItems; ++i) {
+    const int64_t j = t0 + i * kExpBlock + threadIdx.x;
+    cnt_s[i * kExpBlock + threadIdx.x] = j < n_jobs ? job_items[j] : 0u;
+  }
+  __syncthreads();
+  uint32_t v[kExpItems];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < kExpItems; ++i) {
+    v[i] = cnt_s[threadIdx.x * kExpItems + i];
+    sum += v[i];
+  }
+  const uint64_t excl = block_excl_scan<kExpBlock>(sum, &total_s);
+  if (threadIdx.x < 32) {
+    const uint64_t pf = lookback_warp(status, tile, total_s);
+    if (threadIdx.x == 0) prefix_s = pf;
+  }
+  __syncthreads();
+  {
+    uint64_t run = prefix_s + excl;
+#pragma unroll
+    for (int i = 0; i < kExpItems; ++i) {
+      off_s[threadIdx.x * kExpItems + i] = run;
+      run += v[i];
+    }
+  }
+  if (threadIdx.x == 0 && tile == n_tiles - 1) ctl->items_total = prefix_s + total_s;
+  __syncthreads();
+  // offsets and items striped: consecutive lanes, consecutive jobs, consecutive items
+  bool over = false;
+#pragma unroll 1
+  for (int i = 0; i < kExpItems; ++i) {
+    const int q = i * kExpBlock + threadIdx.x;
+    const int64_t j = t0 + q;
+    const unsigned long long base = off_s[q];
+    uint32_t n = cnt_s[q];
+    if (j < n_jobs) job_item_off[j] = base;
+    if (base + n > cap) {  // speculative item buffers too small: the host re-plans with a sync
+      over = true;
+      n = base < cap ? (uint32_t)(cap - base) : 0u;
+    }
+    if (n <= 4u) {
+      for (uint32_t k = 0; k < n; ++k) {
+        item_job[base + k] = (uint32_t)j;
+        item_p0[base + k] = k * item_pix;
+      }
+    }
+    unsigned big = __ballot_sync(0xffffffffu, n > 4u);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t bn = __shfl_sync(0xffffffffu, n, src);
+      const unsigned long long bb = __shfl_sync(0xffffffffu, base, src);
+      const uint32_t bj = (uint32_t)(j - (int64_t)(threadIdx.x & 31u) + src);
+      for (uint32_t k = threadIdx.x & 31u; k < bn; k += 32) {
+        item_job[bb + k] = bj;
+        item_p0[bb + k] = k * item_pix;
+      }
+    }
+  }
+  if (over) raise_status(&ctl->status, FHV_RETRY_ITEMS);
+}
+
 // POFA leaves: thread = one level-(L-1) node (8 leaves)
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_scan_leaves(const uint4* __restrict__ counts, uint4* __restrict__ offsets,
@@ -766,6 +855,22 @@ int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offs
     return rc;
   }
   return run_deferred_item_scan(ctx, s);  // not fused: its own scan (the directory's total stays)
+}
+
+int scan_expand_items(fhv_ctx* ctx, const uint32_t* job_items, unsigned long long* job_item_off, int64_t n_jobs,
+                      uint32_t* item_job, uint32_t* item_p0, unsigned long long cap, uint32_t item_pix,
+                      cudaStream_t s) {
+  const unsigned tiles = (unsigned)((n_jobs + (int64_t)kExpBlock * kExpItems - 1) / ((int64_t)kExpBlock * kExpItems));
+  uint64_t* st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)tiles * sizeof(uint64_t));
+  if (!st) return FHV_NOMEM;
+  int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)tiles * sizeof(uint64_t), s));
+  if (rc) return rc;
+  {
+    LaunchScope L_(ctx, kStItemExpand, s);
+    k_item_scan_expand<<<tiles, kExpBlock, 0, s>>>(job_items, job_item_off, n_jobs, item_job, item_p0, cap, item_pix,
+                                                   st, ctx->ctl, tiles);
+  }
+  return check_cuda(ctx, cudaGetLastError());
 }
 
 int run_deferred_item_scan(fhv_ctx* ctx, cudaStream_t s) {
