@@ -147,6 +147,9 @@ extern "C" void fhv_ctx_destroy(fhv_ctx* ctx) {
     cudaEventDestroy(p.e1);
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 

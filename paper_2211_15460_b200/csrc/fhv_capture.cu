@@ -2684,7 +2684,10 @@ int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg
   if ((rc = shard_params(ctx, tris, cfg, levels, shard, true, p, s, reuse_bin))) return rc;
   const unsigned long long n_local = p.cell_hi - p.cell_lo;
   if ((rc = plan(ctx, p, s, spec))) return rc;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(counts_local, 0, (size_t)n_local * 4, s)))) return rc;
+  if (ctx->counts_zeroed != counts_local &&
+      (rc = check_cuda(ctx, cudaMemsetAsync(counts_local, 0, (size_t)n_local * 4, s))))
+    return rc;
+  ctx->counts_zeroed = nullptr;
   // whole-directory builds also total the fragments per directory tile, so
   // the directory pass (scan_leaves_and_pyramid) needs no look-back chain
   uint32_t* tile_sums = nullptr;
@@ -2696,6 +2699,7 @@ int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg
     if ((rc = check_cuda(ctx, cudaMemsetAsync(tile_sums, 0, nt * 4, s)))) return rc;
     ctx->dir_sums_levels = levels;
   }
+  if ((rc = join_aux(ctx, s))) return rc;  // the side stream's clears (asynchronous build)
   // deferred ranks ride in the directory launch (whole-directory builds with tile totals)
   if ((rc = count(ctx, p, true, levels, counts_local, s, ranks, tile_sums, defer_ranks && tile_sums))) return rc;
   if (!ranks || ctx->item_scan_n >= 0) return FHV_OK;  // the total comes from the directory scan (caller)
@@ -2761,7 +2765,10 @@ static int pofa_scatter_async(fhv_ctx* ctx, const CaptureParams& p, int32_t leve
   uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_local * 4);
   if (!cursors) return FHV_NOMEM;
   int rc;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_local * 4, s)))) return rc;
+  if ((rc = join_aux(ctx, s))) return rc;
+  if (ctx->cursors_zeroed != cursors && (rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_local * 4, s))))
+    return rc;
+  ctx->cursors_zeroed = nullptr;
   if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->alloc, 0, 8, s)))) return rc;
   if (clear_status && (rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->status, 0, sizeof(int), s)))) return rc;
   EmitOut o = empty_out();
@@ -2917,6 +2924,35 @@ __global__ void k_ticket(Control* ctl) {
   ctl->spare[7] = ctl->alloc;
 }
 }  // namespace
+int join_aux(fhv_ctx* ctx, cudaStream_t s) {
+  if (!ctx->join_pending) return FHV_OK;
+  ctx->join_pending = false;
+  return check_cuda(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+}
+
+// clear the leaf counters and the cursors on the side stream (FHV_FORK_CLEARS=0: inline, A/B)
+static int fork_clears(fhv_ctx* ctx, uint32_t* counts, unsigned long long n_leaves, cudaStream_t s) {
+  static const int on = env_int("FHV_FORK_CLEARS", 1);
+  if (!on) return FHV_OK;
+  uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_leaves * 4);
+  if (!cursors) return FHV_NOMEM;
+  int rc;
+  if (!ctx->aux) {
+    if ((rc = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking)))) return rc;
+    if ((rc = check_cuda(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)))) return rc;
+    if ((rc = check_cuda(ctx, cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)))) return rc;
+  }
+  if ((rc = check_cuda(ctx, cudaEventRecord(ctx->ev_fork, s)))) return rc;
+  if ((rc = check_cuda(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0)))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(counts, 0, (size_t)n_leaves * 4, ctx->aux)))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_leaves * 4, ctx->aux)))) return rc;
+  if ((rc = check_cuda(ctx, cudaEventRecord(ctx->ev_join, ctx->aux)))) return rc;
+  ctx->join_pending = true;
+  ctx->counts_zeroed = counts;
+  ctx->cursors_zeroed = cursors;
+  return FHV_OK;
+}
+
 }  // namespace fhv
 
 extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
@@ -2931,9 +2967,17 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   const unsigned long long n_leaves = 1ull << (3 * levels);
   const bool ranks = (flags & FHV_EXACT_ORDER) != 0;
   CaptureParams p;
+  // the leaf counters and the cursors are cleared on the side stream while
+  // the job setup and the plan run (joined before the counting pass)
+  if ((rc = fork_clears(ctx, counts, n_leaves, s))) return rc;
   // speculative item plan when this ctx has one for the job count (else plan() syncs once)
   // (the emission ranks' scan rides in the directory launch)
-  if ((rc = pofa_count_async(ctx, tris, cfg, levels, nullptr, counts, s, p, true, ranks, false, true))) return rc;
+  rc = pofa_count_async(ctx, tris, cfg, levels, nullptr, counts, s, p, true, ranks, false, true);
+  if (rc) {
+    join_aux(ctx, s);
+    ctx->counts_zeroed = ctx->cursors_zeroed = nullptr;
+    return rc;
+  }
   const bool deferred = ctx->item_scan_n >= 0;
   if ((rc = fhv_pofa_shard_directory_nocheck(ctx, levels, counts, offsets, pyramid, s))) return rc;
   if ((!ranks || deferred) &&

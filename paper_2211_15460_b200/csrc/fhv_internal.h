@@ -95,6 +95,13 @@ struct fhv_ctx {
   // device-side count (speculative plan) or null
   int64_t item_scan_n = -1;
   const unsigned long long* item_scan_dev = nullptr;
+  // side stream of the asynchronous build: the leaf-counter and cursor
+  // clears run there, off the critical path, joined before their first use
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool join_pending = false;
+  const void* counts_zeroed = nullptr;   // buffers the side stream cleared for this build
+  const void* cursors_zeroed = nullptr;
   int last_cuda_error = 0;
 };
 
@@ -136,6 +143,8 @@ int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offs
 int scan_expand_items(fhv_ctx* ctx, const uint32_t* job_items, unsigned long long* job_item_off, int64_t n_jobs,
                       uint32_t* item_job, uint32_t* item_p0, unsigned long long cap, uint32_t item_pix,
                       cudaStream_t s);
+// join the side stream's clears into `s` (no-op when nothing is pending)
+int join_aux(fhv_ctx* ctx, cudaStream_t s);
 // the deferred item-rank scan on its own (no-op when none is pending)
 int run_deferred_item_scan(fhv_ctx* ctx, cudaStream_t s);
 // leaves per directory tile (4096 for L = 4, 32768 for L >= 5, 0 below): shard ranges are multiples
