@@ -2700,6 +2700,12 @@ int pofa_count_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg
     ctx->dir_sums_levels = levels;
   }
   if ((rc = join_aux(ctx, s))) return rc;  // the side stream's clears (asynchronous build)
+  if (ctx->fork_cursors_at_count) {  // the cursors cleared while the counting pass runs
+    void* c = ctx->fork_cursors_at_count;
+    ctx->fork_cursors_at_count = nullptr;
+    if ((rc = fork_clear(ctx, c, (size_t)n_local * 4, s, nullptr))) return rc;
+    ctx->cursors_zeroed = c;
+  }
   // deferred ranks ride in the directory launch (whole-directory builds with tile totals)
   if ((rc = count(ctx, p, true, levels, counts_local, s, ranks, tile_sums, defer_ranks && tile_sums))) return rc;
   if (!ranks || ctx->item_scan_n >= 0) return FHV_OK;  // the total comes from the directory scan (caller)
@@ -2930,12 +2936,16 @@ int join_aux(fhv_ctx* ctx, cudaStream_t s) {
   return check_cuda(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
 }
 
-// clear the leaf counters and the cursors on the side stream (FHV_FORK_CLEARS=0: inline, A/B)
-static int fork_clears(fhv_ctx* ctx, uint32_t* counts, unsigned long long n_leaves, cudaStream_t s) {
-  static const int on = env_int("FHV_FORK_CLEARS", 1);
-  if (!on) return FHV_OK;
-  uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_leaves * 4);
-  if (!cursors) return FHV_NOMEM;
+// FHV_FORK_CLEARS: 0 inline clears (A/B); 1 both clears during the job
+// setup; 2 the counters during the job setup, the cursors during the
+// counting pass
+static int fork_mode() {
+  static const int v = env_int("FHV_FORK_CLEARS", 2);
+  return v;
+}
+
+// clear `n` words at `buf` on the side stream after the work queued on `s` so far
+int fork_clear(fhv_ctx* ctx, void* buf, size_t bytes, cudaStream_t s, void* buf2) {
   int rc;
   if (!ctx->aux) {
     if ((rc = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking)))) return rc;
@@ -2944,12 +2954,24 @@ static int fork_clears(fhv_ctx* ctx, uint32_t* counts, unsigned long long n_leav
   }
   if ((rc = check_cuda(ctx, cudaEventRecord(ctx->ev_fork, s)))) return rc;
   if ((rc = check_cuda(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0)))) return rc;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(counts, 0, (size_t)n_leaves * 4, ctx->aux)))) return rc;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_leaves * 4, ctx->aux)))) return rc;
+  if ((rc = check_cuda(ctx, cudaMemsetAsync(buf, 0, bytes, ctx->aux)))) return rc;
+  if (buf2 && (rc = check_cuda(ctx, cudaMemsetAsync(buf2, 0, bytes, ctx->aux)))) return rc;
   if ((rc = check_cuda(ctx, cudaEventRecord(ctx->ev_join, ctx->aux)))) return rc;
   ctx->join_pending = true;
+  return FHV_OK;
+}
+
+// the asynchronous build's leaf counters (and, mode 1, cursors) cleared on the side stream
+static int fork_clears(fhv_ctx* ctx, uint32_t* counts, unsigned long long n_leaves, cudaStream_t s) {
+  const int mode = fork_mode();
+  if (!mode) return FHV_OK;
+  uint32_t* cursors = (uint32_t*)scratch(ctx, kCursors, (size_t)n_leaves * 4);
+  if (!cursors) return FHV_NOMEM;
+  int rc = fork_clear(ctx, counts, (size_t)n_leaves * 4, s, mode == 1 ? cursors : nullptr);
+  if (rc) return rc;
   ctx->counts_zeroed = counts;
-  ctx->cursors_zeroed = cursors;
+  ctx->cursors_zeroed = mode == 1 ? cursors : nullptr;
+  ctx->fork_cursors_at_count = mode == 2 ? cursors : nullptr;
   return FHV_OK;
 }
 

@@ -102,6 +102,7 @@ struct fhv_ctx {
   bool join_pending = false;
   const void* counts_zeroed = nullptr;   // buffers the side stream cleared for this build
   const void* cursors_zeroed = nullptr;
+  void* fork_cursors_at_count = nullptr;  // clear these cursors on the side stream at the counting pass
   int last_cuda_error = 0;
 };
 
@@ -145,6 +146,8 @@ int scan_expand_items(fhv_ctx* ctx, const uint32_t* job_items, unsigned long lon
                       cudaStream_t s);
 // join the side stream's clears into `s` (no-op when nothing is pending)
 int join_aux(fhv_ctx* ctx, cudaStream_t s);
+// zero `bytes` at buf (and buf2) on the side stream after the work queued on `s`; join with join_aux
+int fork_clear(fhv_ctx* ctx, void* buf, size_t bytes, cudaStream_t s, void* buf2);
 // the deferred item-rank scan on its own (no-op when none is pending)
 int run_deferred_item_scan(fhv_ctx* ctx, cudaStream_t s);
 // leaves per directory tile (4096 for L = 4, 32768 for L >= 5, 0 below): shard ranges are multiples
