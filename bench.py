@@ -909,6 +909,7 @@ def main():
     # buffered, so step k+1's upload and step k-1's read-back overlap step
     # k's kernels (a two-deep pipeline, as a serving loop would run it).
     if not args.profile_only:
+        NB = int(os.environ.get("FHV_E2E_BUFFERS", "2"))  # pipeline depth (scene / image buffer sets)
         # The scene crosses PCIe every step.  --upload indexed (default): as an
         # IndexedMesh (shared vertex rows + u32 faces, 43 MB for C3 instead of
         # the 149-MB triangle soup) that the device expands into the soup
@@ -921,7 +922,7 @@ def main():
         if indexed:
             mesh = IndexedMesh.from_scene(scene)
             arrays = mesh.arrays()
-            stage = [IndexedUpload(mesh, dev) for _ in range(2)]
+            stage = [IndexedUpload(mesh, dev) for _ in range(NB)]
             for d_, src in zip(stage[0].tensors(), arrays):
                 d_.copy_(torch.from_numpy(np.ascontiguousarray(src)))
             ref_soup = DeviceScene(scene, dev)
@@ -939,17 +940,17 @@ def main():
                 (scene.material_id.view(np.int32), scene.object_id.view(np.int32))
         del probe
         pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays]
-        bufs_in = [ds, DeviceScene(scene, dev)]
-        bufs_out = [img, ImageBuffer(W, H, torch.empty((H, W, 4), dtype=torch.float64, device=dev),
-                                     torch.empty((H, W), dtype=torch.float64, device=dev))]
-        out_px = [torch.empty((H, W, 4), dtype=torch.float64).pin_memory() for _ in range(2)]
-        out_dp = [torch.empty((H, W), dtype=torch.float64).pin_memory() for _ in range(2)]
+        bufs_in = [ds] + [DeviceScene(scene, dev) for _ in range(NB - 1)]
+        bufs_out = [img] + [ImageBuffer(W, H, torch.empty((H, W, 4), dtype=torch.float64, device=dev),
+                                        torch.empty((H, W), dtype=torch.float64, device=dev)) for _ in range(NB - 1)]
+        out_px = [torch.empty((H, W, 4), dtype=torch.float64).pin_memory() for _ in range(NB)]
+        out_dp = [torch.empty((H, W), dtype=torch.float64).pin_memory() for _ in range(NB)]
         h2d = sum(p.numel() * p.element_size() for p in pin)
 
         def dst_of(k):
             if indexed:
-                return stage[k % 2].tensors()
-            b = bufs_in[k % 2]
+                return stage[k % NB].tensors()
+            b = bufs_in[k % NB]
             return (b.pos, b.vnrm) + (() if derive_fn else (b.fnrm,)) + (b.mat.view(torch.int32), b.obj.view(torch.int32))
         # the link itself: the same pinned uploads alone (PCIe bound of the e2e line)
         torch.cuda.synchronize()
@@ -970,8 +971,8 @@ def main():
 
         def upload(k):
             s_in.wait_event(e_start)
-            if k >= 2:
-                s_in.wait_event(e_done[k - 2])  # buffer k%2 free again
+            if k >= NB:
+                s_in.wait_event(e_done[k - NB])  # buffer k%NB free again
             with torch.cuda.stream(s_in):
                 for d, src in zip(dst_of(k), pin):
                     d.copy_(src, non_blocking=True)
@@ -980,8 +981,8 @@ def main():
         def readback(k):
             s_out.wait_event(e_done[k])
             with torch.cuda.stream(s_out):
-                out_px[k % 2].copy_(bufs_out[k % 2].pixels, non_blocking=True)
-                out_dp[k % 2].copy_(bufs_out[k % 2].depth, non_blocking=True)
+                out_px[k % NB].copy_(bufs_out[k % NB].pixels, non_blocking=True)
+                out_dp[k % NB].copy_(bufs_out[k % NB].depth, non_blocking=True)
                 e_out[k].record(s_out)
 
         barrier()
@@ -993,18 +994,17 @@ def main():
             if k + 1 < K:
                 upload(k + 1)
             stream.wait_event(e_in[k])
-            if k >= 2:
-                stream.wait_event(e_out[k - 2])  # image buffer k%2 read back
+            if k >= NB:
+                stream.wait_event(e_out[k - NB])  # image buffer k%NB read back
             if indexed:
-                bufs_in[k % 2].load_indexed(stage[k % 2])  # gather + ids + face normals, on the device
+                bufs_in[k % NB].load_indexed(stage[k % NB])  # gather + ids + face normals, on the device
             elif derive_fn:
-                bufs_in[k % 2].derive_face_normals()
-            step(bufs_in[k % 2], bufs_out[k % 2])
+                bufs_in[k % NB].derive_face_normals()
+            step(bufs_in[k % NB], bufs_out[k % NB])
             e_done[k].record(stream)
             readback(k)
-        stream.wait_event(e_out[K - 1])
-        if K >= 2:
-            stream.wait_event(e_out[K - 2])
+        for k in range(max(0, K - NB), K):
+            stream.wait_event(e_out[k])
         e3.record(stream)
         barrier()
         check_tickets()
@@ -1014,10 +1014,10 @@ def main():
             t2 = all_max(t2)
         ms_e2e = float(t2.item())
         torch.cuda.synchronize()
-        ok = np.array_equal(out_dp[(K - 1) % 2].numpy(), bufs_out[(K - 1) % 2].depth.cpu().numpy())
+        ok = np.array_equal(out_dp[(K - 1) % NB].numpy(), bufs_out[(K - 1) % NB].depth.cpu().numpy())
         e2e = {"value": n_frags * args.steps / (ms_e2e / 1e3), "unit": "frag/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps,
-               "pipeline": "2-deep: H2D(k+1) and D2H(k-1) on copy streams overlap step k",
+               "pipeline": f"{NB} buffers: H2D(k+1) and D2H(k-1) on copy streams overlap step k",
                "upload": ("indexed mesh: %d shared vertex rows + %d u32 faces, expanded on the device into the "
                           "triangle arrays (checked byte-identical before timing)" % (mesh.n_vertices, mesh.n_triangles)
                           if indexed else "triangle arrays"),
