@@ -11,8 +11,10 @@ timeout 900 python bench.py --config C2 --steps 20 --warmup 5 > gpurun_out/${TAG
 timeout 900 python bench.py --config C4 --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_C4.jsonl 2> gpurun_out/${TAG}_bench_C4.err
 timeout 900 python bench.py --config C5 --steps 3 --warmup 1 > gpurun_out/${TAG}_bench_C5.jsonl 2> gpurun_out/${TAG}_bench_C5.err
 STAGES="launches" bash tools/gpu_round.sh $TAG
-# one C3 step's kernels (the first step's launches skipped: warm-up)
-NCU_FILTER='-k regex:k_(job_setup|scan|item_expand|raster|dir_tma|emit|leaf_fix|splat) --launch-skip 13 -c 13' \
+# one C3 step's 10 kernels (job setup, plan, count, directory + ranks,
+# emission, fix-up x2, splat x3) after the warm-up steps (the first one
+# synchronous: 9 matching launches)
+NCU_FILTER='-k regex:k_(job_setup|item_scan|raster|dir_tma|emit|leaf_fix|splat) --launch-skip 29 -c 10' \
     STAGES="full" bash tools/gpu_round.sh $TAG
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_raycast -c 1 -o gpurun_out/${TAG}_ray -f \
     python bench.py --config C2 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/${TAG}_ray_ncu.log 2>&1

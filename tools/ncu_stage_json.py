@@ -16,7 +16,7 @@ import sys
 STAGES = [("k_raster<1,", "count_leaves"), ("k_dir_tiles<1,", "scan_leaves"), ("k_dir_tma", "scan_leaves"), ("k_emit<5,", "emit_pofa"),
           ("k_emit_fast<5,", "emit_pofa"), ("k_splat_depth", "splat_depth"), ("k_splat_index_stored", "splat_index"),
           ("k_splat_resolve", "splat_resolve"), ("k_job_setup", "job_setup"), ("k_leaf_fix(", "leaf_order"),
-          ("k_leaf_fix_big", "leaf_sort")]
+          ("k_leaf_fix_big", "leaf_sort"), ("k_item_scan_expand", "item_expand")]
 # atomic / reduction traffic (north star: "atomic throughput"): warp-level
 # requests at L1, sectors at L1, requests arriving at L2, and the L1 RED/ATOM
 # pipe utilisation
