@@ -13,8 +13,8 @@ timeout 900 python bench.py --config C5 --steps 3 --warmup 1 > gpurun_out/${TAG}
 STAGES="launches" bash tools/gpu_round.sh $TAG
 # one C3 step's 10 kernels (job setup, plan, count, directory + ranks,
 # emission, fix-up x2, splat x3) after the warm-up steps (the first one
-# synchronous: 9 matching launches)
-NCU_FILTER='-k regex:k_(job_setup|item_scan|raster|dir_tma|emit|leaf_fix|splat) --launch-skip 29 -c 10' \
+# first two synchronous: 9 matching launches each, then an asynchronous one)
+NCU_FILTER='-k regex:k_(job_setup|item_scan|raster|dir_tma|emit|leaf_fix|splat) --launch-skip 28 -c 10' \
     STAGES="full" bash tools/gpu_round.sh $TAG
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_raycast -c 1 -o gpurun_out/${TAG}_ray -f \
     python bench.py --config C2 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/${TAG}_ray_ncu.log 2>&1
