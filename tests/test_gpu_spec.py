@@ -341,3 +341,47 @@ def test_async_pofl_build_and_raycast_in_a_cuda_graph():
     assert (bad, k) == (0, 3)
     assert np.array_equal(img.pixels.cpu().numpy(), rimg.pixels.cpu().numpy())
     assert fhv.RaycastStats(*st.counters.cpu().tolist()).as_dict() == rst.as_dict()
+
+
+_ASYNC_PATHS = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2211_15460_b200 as fhv
+from oracle import oracle as orc
+from paper_2211_15460_b200.raster import CaptureStrategy
+from tests._golden import golden_scene
+bad = []
+for name in ("cornell", "icosphere"):
+    s = golden_scene(name)
+    cfg = fhv.RasterConfig.from_camera(fhv.capture_camera(s, "+z", 256))
+    ref = orc.pofa_build(s, CaptureStrategy.normal_space(), cfg, 5)
+    for _ in range(3):  # the first build plans exactly; the later ones speculate
+        v = fhv.pofa_build(s, CaptureStrategy.normal_space(), cfg, 5, exact_order=True, sync=False)
+        v.wait()
+        got = v.pool.numpy()
+        for k in ("position", "normal", "material_id", "object_id", "prev_index"):
+            if not np.array_equal(got[k], ref["pool"][k]):
+                bad.append((name, k))
+        if not np.array_equal(v.directory.offsets.cpu().numpy(), ref["offsets"]):
+            bad.append((name, "offsets"))
+print("BAD", bad) if bad else print("OK")
+"""
+
+
+@pytest.mark.parametrize("env", ({"FHV_DIR_STREAM": "0"}, {"FHV_FORK_CLEARS": "0", "FHV_FUSED_EXPAND": "0"},
+                                 {"FHV_FORK_CLEARS": "1"}))
+def test_async_build_paths_bit_exact(env):
+    """The asynchronous POFA build's scheduling variants give the reference's
+    pool and offsets bit for bit: the emission-rank scan fused into the
+    directory launch or run on its own (FHV_DIR_STREAM=0: no tile-total
+    directory), the leaf-counter / cursor clears on the side stream (mode 1:
+    both at the job setup; default: cursors at the counting pass) or inline,
+    the speculative plan's fused or separate item expansion."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _ASYNC_PATHS.format(root=root)], env=dict(os.environ, **env),
+                         capture_output=True, text=True, cwd=root, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == "OK", out.stdout[-2000:]
