@@ -162,6 +162,14 @@ def test_c4_depth_complex_ppfl_vs_pofa():
     ref = orc.pofa_build(s, one, cfg, 8)
     assert ref["next_free"] == n
     assert np.array_equal(vol.directory.counts.cpu().numpy(), ref["counts"])
+    # the pool itself, in the reference's in-leaf order (the certified emission
+    # walks whole-item groups column-major; the fix-up restores the order)
+    pool = vol.pool
+    for k, t in (("position", pool.position), ("normal", pool.normal), ("material_id", pool.material_id),
+                 ("object_id", pool.object_id), ("prev_index", pool.prev_index)):
+        r = ref["pool"][k]
+        got = t[:n].view(torch.int32).cpu().numpy().reshape(r.shape)  # bit patterns (u32 ids, f32 components)
+        assert np.array_equal(got, r.view(np.int32)), k
     del ref
     # PPFL with an explicit capacity (the default 10x overalloc is too small here), bit-exact chains
     pp = fhv.build_ppfl(s, cfg, one, capacity=n, exact_order=True)
