@@ -2998,6 +2998,7 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   if (rc) {
     join_aux(ctx, s);
     ctx->counts_zeroed = ctx->cursors_zeroed = nullptr;
+    ctx->fork_cursors_at_count = nullptr;
     return rc;
   }
   const bool deferred = ctx->item_scan_n >= 0;
