@@ -1774,6 +1774,9 @@ __device__ __forceinline__ void unstage_record(const PoolRefs& pl, const uint32_
 constexpr int kFixChunks = 6;
 constexpr int kFixWarpTile = 128;                     // segments starting here are this warp's
 constexpr int kFixWarpRegion = 32 * kFixChunks;       // 192
+#ifndef FHV_FIX_PER_SM
+#define FHV_FIX_PER_SM 12  // fix-up grid: CTAs per SM (each warp strides over 128-slot tiles)
+#endif
 #ifndef FHV_FIX_WARPS
 #define FHV_FIX_WARPS 2
 #endif
@@ -2818,7 +2821,7 @@ static int pofa_scatter_async(fhv_ctx* ctx, const CaptureParams& p, int32_t leve
       LaunchScope L_(ctx, kStLeafOrder, s);
       const long long tiles = (cap + kFixWarpTile - 1) / kFixWarpTile;  // one warp each
       const long long ctas = (tiles + kFixWarps - 1) / kFixWarps;
-      k_leaf_fix<<<(int)(ctas < 148LL * 12 ? ctas : 148LL * 12), 32 * kFixWarps, 0, s>>>(
+      k_leaf_fix<<<(int)(ctas < 148LL * FHV_FIX_PER_SM ? ctas : 148LL * FHV_FIX_PER_SM), 32 * kFixWarps, 0, s>>>(
           pl, n_frags_dev, cap, big, &ctx->ctl->leaf_n[2], big_cap, &ctx->ctl->leaf_n[0], &ctx->ctl->status);
     }
     {
