@@ -271,7 +271,8 @@ __device__ __forceinline__ void setup_tangent(const CaptureParams& p, long long 
 #define FHV_SETUP_MINB 8  // 64 registers: job setup 47 -> 44 us (6: 47, 10: 46)
 #endif
 __global__ void __launch_bounds__(128, FHV_SETUP_MINB) k_job_setup(CaptureParams p, JobSetup* __restrict__ jobs,
-                                                                   uint32_t* __restrict__ job_items, int* status) {
+                                                                   uint32_t* __restrict__ job_items, int* status,
+                                                                   uint32_t* __restrict__ tile_sums) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < p.n_jobs;
        j += (long long)gridDim.x * blockDim.x) {
     long long t;
@@ -295,6 +296,11 @@ __global__ void __launch_bounds__(128, FHV_SETUP_MINB) k_job_setup(CaptureParams
     }
     jobs[j] = js;
     job_items[j] = (uint32_t)items;
+    if (tile_sums) {  // the item totals of kExpandTileJobs-job tiles (a warp's 32 jobs share one)
+      const unsigned act = __activemask();
+      const unsigned v = __reduce_add_sync(act, (unsigned)items);
+      if ((int)lane_id() == __ffs(act) - 1) atomicAdd(&tile_sums[j / kExpandTileJobs], v);
+    }
   }
 }
 
@@ -2246,13 +2252,22 @@ int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s, bool allow_spec =
   uint32_t* job_items = (uint32_t*)scratch(ctx, kJobItems, (size_t)p.n_jobs * 4);
   auto* job_item_off = (unsigned long long*)scratch(ctx, kJobItemOff, (size_t)p.n_jobs * 8);
   if (!jobs || !job_items || !job_item_off) return FHV_NOMEM;
+  const bool spec = allow_spec && ctx->last_n_jobs == p.n_jobs && ctx->item_cap > 0;
+  const bool fused = spec && fused_expand_enabled();
+  // the fused plan's tile totals, summed by the job setup (no look-back chain in the expansion)
+  uint32_t* tsum = nullptr;
+  if (fused) {
+    const size_t nt = (size_t)((p.n_jobs + kExpandTileJobs - 1) / kExpandTileJobs);
+    tsum = (uint32_t*)scratch(ctx, kJobTileSums, nt * 4);
+    if (!tsum) return FHV_NOMEM;
+    if ((rc = check_cuda(ctx, cudaMemsetAsync(tsum, 0, nt * 4, s)))) return rc;
+  }
   {
     LaunchScope L_(ctx, kStJobSetup, s);
-    k_job_setup<<<grid_for(p.n_jobs, 128), 128, 0, s>>>(p, jobs, job_items, &ctx->ctl->status);
+    k_job_setup<<<grid_for(p.n_jobs, 128), 128, 0, s>>>(p, jobs, job_items, &ctx->ctl->status, tsum);
   }
   if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
-  const bool spec = allow_spec && ctx->last_n_jobs == p.n_jobs && ctx->item_cap > 0;
-  if (spec && fused_expand_enabled()) {  // item buffers sized by the last exact plan: scan + expand in one pass
+  if (fused) {  // item buffers sized by the last exact plan: scan + expand in one pass
     const long long n_items = ctx->item_cap;
     uint32_t* item_job = (uint32_t*)scratch(ctx, kItemJob, (size_t)n_items * 4);
     uint32_t* item_p0 = (uint32_t*)scratch(ctx, kItemP0, (size_t)n_items * 4);
@@ -2260,7 +2275,7 @@ int plan(fhv_ctx* ctx, const CaptureParams& p, cudaStream_t s, bool allow_spec =
     ctx->n_items = n_items;
     ctx->spec = true;
     return scan_expand_items(ctx, job_items, job_item_off, p.n_jobs, item_job, item_p0, (unsigned long long)n_items,
-                             kItemPix, s);
+                             kItemPix, s, tsum);
   }
   if ((rc = scan_u32_to_u64(ctx, job_items, job_item_off, p.n_jobs, s))) return rc;
   if ((rc = check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->items_total, &ctx->ctl->scan_total, sizeof(unsigned long long),

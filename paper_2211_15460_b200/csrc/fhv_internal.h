@@ -111,7 +111,7 @@ namespace fhv {
 enum BufId {
   kJobs = 0, kJobItems, kJobItemOff, kItemJob, kItemP0, kItemCnt, kItemOff, kScanStatus,
   kCursors, kChainScratch, kSplatKey, kSplatWin, kSplatBox, kRays, kTmp0, kTmp1, kTriFlag, kTriOff, kTriIndex,
-  kShardBoxes, kItemMask, kJobPersp, kLeafList, kLeafKeys, kLeafRecs, kTileSums, kNumBufs
+  kShardBoxes, kItemMask, kJobPersp, kLeafList, kLeafKeys, kLeafRecs, kTileSums, kJobTileSums, kNumBufs
 };
 
 // Counts a launch and, when profiling is on, brackets it with CUDA events on
@@ -141,9 +141,12 @@ int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offs
                             int levels, cudaStream_t s);
 // speculative capture plan: job item counts -> offsets + the item records in
 // one launch (item total -> ctl->items_total; FHV_RETRY_ITEMS past cap)
+// job_tile_sums: the job setup's per-tile item totals (kExpandTileJobs jobs
+// per tile): the tiles then need no look-back chain; null: ticket order + look-back
+constexpr int kExpandTileJobs = 1024;
 int scan_expand_items(fhv_ctx* ctx, const uint32_t* job_items, unsigned long long* job_item_off, int64_t n_jobs,
                       uint32_t* item_job, uint32_t* item_p0, unsigned long long cap, uint32_t item_pix,
-                      cudaStream_t s);
+                      cudaStream_t s, const uint32_t* job_tile_sums = nullptr);
 // join the side stream's clears into `s` (no-op when nothing is pending)
 int join_aux(fhv_ctx* ctx, cudaStream_t s);
 // zero `bytes` at buf (and buf2) on the side stream after the work queued on `s`; join with join_aux

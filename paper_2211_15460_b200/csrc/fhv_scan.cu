@@ -105,15 +105,19 @@ __global__ void __launch_bounds__(kExpBlock) k_item_scan_expand(const uint32_t* 
                                                                int64_t n_jobs, uint32_t* __restrict__ item_job,
                                                                uint32_t* __restrict__ item_p0, unsigned long long cap,
                                                                uint32_t item_pix, uint64_t* status, Control* ctl,
-                                                               unsigned n_tiles) {
+                                                               unsigned n_tiles, const uint32_t* __restrict__ tsum) {
   constexpr int kT = kExpBlock * kExpItems;
+  static_assert(kT == kExpandTileJobs, "tile totals match the tile");
   __shared__ unsigned tile_s;
-  __shared__ uint64_t prefix_s, total_s;
+  __shared__ uint64_t prefix_s, total_s, tsum_s;
   __shared__ uint32_t cnt_s[kT];
   __shared__ unsigned long long off_s[kT];
-  if (threadIdx.x == 0) tile_s = draw_tile(ctl, n_tiles);
+  if (threadIdx.x == 0) tile_s = tsum ? blockIdx.x : draw_tile(ctl, n_tiles);
   __syncthreads();
   const unsigned tile = tile_s;
+  uint64_t pred = 0;  // with the job setup's tile totals: the predecessors' sum, no chain
+  if (tsum)
+    for (unsigned q = threadIdx.x; q < tile; q += kExpBlock) pred += tsum[q];
   const int64_t t0 = (int64_t)tile * kT;
   // counts striped (coalesced) into shared memory, scanned blocked
 #pragma unroll
@@ -130,7 +134,13 @@ __global__ void __launch_bounds__(kExpBlock) k_item_scan_expand(const uint32_t* 
     sum += v[i];
   }
   const uint64_t excl = block_excl_scan<kExpBlock>(sum, &total_s);
-  if (threadIdx.x < 32) {
+  if (tsum) {
+    (void)block_excl_scan<kExpBlock>(pred, &tsum_s);
+    if (threadIdx.x == 0) {
+      prefix_s = tsum_s;
+      if (tsum[tile] != (uint32_t)total_s) raise_status(&ctl->status, FHV_PASS_MISMATCH);
+    }
+  } else if (threadIdx.x < 32) {
     const uint64_t pf = lookback_warp(status, tile, total_s);
     if (threadIdx.x == 0) prefix_s = pf;
   }
@@ -859,16 +869,19 @@ int scan_leaves_and_pyramid(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offs
 
 int scan_expand_items(fhv_ctx* ctx, const uint32_t* job_items, unsigned long long* job_item_off, int64_t n_jobs,
                       uint32_t* item_job, uint32_t* item_p0, unsigned long long cap, uint32_t item_pix,
-                      cudaStream_t s) {
+                      cudaStream_t s, const uint32_t* job_tile_sums) {
   const unsigned tiles = (unsigned)((n_jobs + (int64_t)kExpBlock * kExpItems - 1) / ((int64_t)kExpBlock * kExpItems));
-  uint64_t* st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)tiles * sizeof(uint64_t));
-  if (!st) return FHV_NOMEM;
-  int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)tiles * sizeof(uint64_t), s));
-  if (rc) return rc;
+  uint64_t* st = nullptr;
+  int rc;
+  if (!job_tile_sums) {
+    st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)tiles * sizeof(uint64_t));
+    if (!st) return FHV_NOMEM;
+    if ((rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)tiles * sizeof(uint64_t), s)))) return rc;
+  }
   {
     LaunchScope L_(ctx, kStItemExpand, s);
     k_item_scan_expand<<<tiles, kExpBlock, 0, s>>>(job_items, job_item_off, n_jobs, item_job, item_p0, cap, item_pix,
-                                                   st, ctx->ctl, tiles);
+                                                   st, ctx->ctl, tiles, job_tile_sums);
   }
   return check_cuda(ctx, cudaGetLastError());
 }
