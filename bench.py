@@ -723,19 +723,22 @@ def main():
     graph = None
     acc = torch.zeros(2, dtype=torch.int64, device=dev)
 
-    def make_graph(exact: bool):
+    def make_graph(exact: bool, tris=None, out=None):
         """One step -- POFA build (every kernel, memset and copy) + splat --
         captured on its own stream; each replay also checks its build ticket
-        on the device (sticky status + count)."""
+        on the device (sticky status + count).  tris / out: the scene and
+        image buffers it reads and writes (default: ds / img)."""
         gs = torch.cuda.Stream(dev)
         gticket = torch.zeros(4, dtype=torch.int64).pin_memory()
+        g_tris = ds if tris is None else tris
+        g_out = img if out is None else out
 
         def graph_step():
-            v = fhv.pofa_build(scene, strat, cfg, L, exact_order=exact, device=dev, tris=ds, sync=False,
+            v = fhv.pofa_build(scene, strat, cfg, L, exact_order=exact, device=dev, tris=g_tris, sync=False,
                                ticket=gticket)
             rc = _lib.load().fhv_ticket_accumulate(_lib.ctx(dev), int(n_frags), _lib.ptr(acc), _lib.stream_ptr(dev))
             _lib.check(rc, "ticket")
-            fhv.splat_render(v.pool, view, w["lights"], w["radius"], scene.materials, out=img, packed=args.packed,
+            fhv.splat_render(v.pool, view, w["lights"], w["radius"], scene.materials, out=g_out, packed=args.packed,
                              shading=shading)
             return v
         with torch.cuda.stream(gs):
@@ -907,7 +910,10 @@ def main():
     # Every step copies its scene from pinned host memory and reads its f64
     # image + depth back.  The copies run on their own streams, double
     # buffered, so step k+1's upload and step k-1's read-back overlap step
-    # k's kernels (a two-deep pipeline, as a serving loop would run it).
+    # k's kernels (a two-deep pipeline, as a serving loop would run it); the
+    # step itself is a replay of the captured build + splat of its buffer
+    # set (FHV_E2E_GRAPH=0: the plain asynchronous calls, 1.83-1.88 against
+    # 1.79-1.81 ms per step).
     if not args.profile_only:
         NB = int(os.environ.get("FHV_E2E_BUFFERS", "2"))  # pipeline depth (scene / image buffer sets)
         # The scene crosses PCIe every step.  --upload indexed (default): as an
@@ -963,6 +969,14 @@ def main():
         torch.cuda.synchronize()
         h2d_gbs = 3 * h2d / (el0.elapsed_time(el1) / 1e3) / 1e9
         d2h = out_px[0].numel() * 8 + out_dp[0].numel() * 8
+        # steps: the build + splat as CUDA-graph replays, one graph per buffer
+        # set (as in the device-resident loop; no host-side allocation that
+        # could serialise the pipeline), else the plain asynchronous calls
+        e2e_graphs = None
+        if graph is not None and os.environ.get("FHV_E2E_GRAPH", "1") != "0":
+            e2e_graphs = [make_graph(args.exact_order, bufs_in[i], bufs_out[i])[0] for i in range(NB)]
+            torch.cuda.synchronize()
+            acc.zero_()
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         K = args.steps
         ev = lambda: torch.cuda.Event()  # noqa: E731
@@ -1000,7 +1014,10 @@ def main():
                 bufs_in[k % NB].load_indexed(stage[k % NB])  # gather + ids + face normals, on the device
             elif derive_fn:
                 bufs_in[k % NB].derive_face_normals()
-            step(bufs_in[k % NB], bufs_out[k % NB])
+            if e2e_graphs is not None:
+                e2e_graphs[k % NB].replay()
+            else:
+                step(bufs_in[k % NB], bufs_out[k % NB])
             e_done[k].record(stream)
             readback(k)
         for k in range(max(0, K - NB), K):
@@ -1008,6 +1025,10 @@ def main():
         e3.record(stream)
         barrier()
         check_tickets()
+        if e2e_graphs is not None:
+            bad_e, checked_e = (int(x) for x in acc.cpu().tolist())
+            if bad_e or checked_e != K:
+                raise RuntimeError(f"e2e graph replays: build ticket status {bad_e}, {checked_e}/{K} checked")
         ms_e2e = e2.elapsed_time(e3)
         t2 = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
         if world > 1:
@@ -1018,6 +1039,8 @@ def main():
         e2e = {"value": n_frags * args.steps / (ms_e2e / 1e3), "unit": "frag/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps,
                "pipeline": f"{NB} buffers: H2D(k+1) and D2H(k-1) on copy streams overlap step k",
+               "steps": ("CUDA-graph replays of the captured build + splat (one graph per buffer set; every build "
+                         "ticket checked on the device)" if e2e_graphs is not None else "asynchronous API calls"),
                "upload": ("indexed mesh: %d shared vertex rows + %d u32 faces, expanded on the device into the "
                           "triangle arrays (checked byte-identical before timing)" % (mesh.n_vertices, mesh.n_triangles)
                           if indexed else "triangle arrays"),
