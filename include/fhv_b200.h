@@ -239,7 +239,9 @@ int fhv_pofa_build(fhv_ctx *ctx, const fhv_tris_t *tris, const fhv_capture_cfg_t
    fhv_pofa_build, enqueued without any host wait, into a pool whose capacity
    is the caller's guess of the exact total (e.g. the total of the previous
    build of the same scene).  The outcome lands in *ticket (pinned host
-   memory, written by a stream-ordered copy); after synchronising the stream,
+   memory; the ticket kernel stores it directly when the ticket is device
+   memory or pinned host memory, else a stream-ordered copy delivers it);
+   after synchronising the stream,
    fhv_ticket_check(ticket, pool capacity) returns FHV_OK when the pool holds
    exactly the build's records, FHV_STALE when the speculation was wrong
    (outputs invalid: rebuild with fhv_pofa_build), or the build's own error. */

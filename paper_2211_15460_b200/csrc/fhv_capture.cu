@@ -2941,13 +2941,51 @@ extern "C" int fhv_pofa_build(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_ca
 namespace fhv {
 namespace {
 // the async build's outcome, staged in ctl->spare[4..7] for the D2H copy
-__global__ void k_ticket(Control* ctl) {
-  ctl->spare[4] = (unsigned long long)(long long)ctl->status;
-  ctl->spare[5] = ctl->frags_total;
-  ctl->spare[6] = ctl->scan_total;
-  ctl->spare[7] = ctl->alloc;
+// the build's ticket: in ctl->spare[4..7] and, when the caller's ticket is
+// device-accessible (device memory, or pinned host memory through its
+// mapping), stored there directly -- no stream-ordered copy, whose copy
+// engine may be busy with the previous step's image read-back
+__device__ __forceinline__ void put_ticket(Control* ctl, unsigned long long* out, unsigned long long st,
+                                           unsigned long long a, unsigned long long b, unsigned long long c) {
+  ctl->spare[4] = st;
+  ctl->spare[5] = a;
+  ctl->spare[6] = b;
+  ctl->spare[7] = c;
+  if (out) {
+    out[0] = st;
+    out[1] = a;
+    out[2] = b;
+    out[3] = c;
+    __threadfence_system();
+  }
+}
+__global__ void k_ticket(Control* ctl, unsigned long long* out) {
+  put_ticket(ctl, out, (unsigned long long)(long long)ctl->status, ctl->frags_total, ctl->scan_total, ctl->alloc);
 }
 }  // namespace
+// a device-accessible address of the caller's ticket (device / managed
+// memory as is, pinned host memory through its mapping), else null (then a
+// stream-ordered copy delivers it)
+unsigned long long* ticket_device_view(fhv_ticket_t* t) {
+  static const int on = env_int("FHV_TICKET_DIRECT", 1);
+  if (!on) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, t) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged)
+    return reinterpret_cast<unsigned long long*>(a.devicePointer ? a.devicePointer : (void*)t);
+  if (a.type == cudaMemoryTypeHost && a.devicePointer) return reinterpret_cast<unsigned long long*>(a.devicePointer);
+  return nullptr;
+}
+
+// the ticket kernel's result to the caller: stored by the kernel, or copied
+int deliver_ticket(fhv_ctx* ctx, fhv_ticket_t* ticket, bool stored, cudaStream_t s) {
+  if (stored) return FHV_OK;
+  return check_cuda(ctx, cudaMemcpyAsync(ticket, &ctx->ctl->spare[4], sizeof(fhv_ticket_t), cudaMemcpyDefault, s));
+}
+
 int join_aux(fhv_ctx* ctx, cudaStream_t s) {
   if (!ctx->join_pending) return FHV_OK;
   ctx->join_pending = false;
@@ -3028,15 +3066,16 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   if ((rc = pofa_scatter_async(ctx, p, levels, 0, n_leaves, counts, offsets, 0, pool, flags, s, false,
                                 &ctx->ctl->frags_total, 0)))
     return rc;
+  unsigned long long* tk_dev = ticket_device_view(ticket);
   {
     LaunchScope L_(ctx, kStScan, s);
-    k_ticket<<<1, 1, 0, s>>>(ctx->ctl);
+    k_ticket<<<1, 1, 0, s>>>(ctx->ctl, tk_dev);
   }
   if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
   // pass-1 bookkeeping for a follow-up fhv_pofa_scatter is not kept: the
   // ticket is the only result
   ctx->pass1_levels = -1;
-  return check_cuda(ctx, cudaMemcpyAsync(ticket, &ctx->ctl->spare[4], sizeof(fhv_ticket_t), cudaMemcpyDefault, s));
+  return deliver_ticket(ctx, ticket, tk_dev != nullptr, s);
 }
 
 // One rank's share of pofa_build with no host wait and no collective: the
@@ -3073,13 +3112,14 @@ extern "C" int fhv_pofa_shard_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, 
       (rc = pofa_scatter_async(ctx, p, levels, lo, hi, counts_local, offsets_local, base, pool, flags, s, false,
                                &ctx->ctl->frags_total, 0)))
     return rc;
+  unsigned long long* tk_dev = ticket_device_view(ticket);
   {
     LaunchScope L_(ctx, kStScan, s);
-    k_ticket<<<1, 1, 0, s>>>(ctx->ctl);
+    k_ticket<<<1, 1, 0, s>>>(ctx->ctl, tk_dev);
   }
   if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
   ctx->pass1_levels = -1;  // the ticket is the only result
-  return check_cuda(ctx, cudaMemcpyAsync(ticket, &ctx->ctl->spare[4], sizeof(fhv_ticket_t), cudaMemcpyDefault, s));
+  return deliver_ticket(ctx, ticket, tk_dev != nullptr, s);
 }
 
 namespace fhv {
@@ -3107,12 +3147,9 @@ namespace fhv {
 namespace {
 // the linked build's outcome in the POFA ticket's words: total in all three
 // count fields (so fhv_ticket_check / k_ticket_acc compare it with the guess)
-__global__ void k_ticket_linked(Control* ctl, int atomic_alloc) {
+__global__ void k_ticket_linked(Control* ctl, int atomic_alloc, unsigned long long* out) {
   const unsigned long long total = atomic_alloc ? ctl->alloc : ctl->scan_total;
-  ctl->spare[4] = (unsigned long long)(long long)ctl->status;
-  ctl->spare[5] = total;
-  ctl->spare[6] = total;
-  ctl->spare[7] = total;
+  put_ticket(ctl, out, (unsigned long long)(long long)ctl->status, total, total, total);
 }
 }  // namespace
 }  // namespace fhv
@@ -3146,12 +3183,13 @@ extern "C" int fhv_build_pofl_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   if ((rc = emit<kPofl>(ctx, p, o, atomic_alloc, s))) return rc;
   if ((flags & FHV_EXACT_ORDER) && (rc = chain_order(ctx, heads, pool->prev, n_keys, pool->capacity, s))) return rc;
   if ((rc = pyramid_from_heads(ctx, heads, pyramid, levels, s))) return rc;
+  unsigned long long* tk_dev = ticket_device_view(ticket);
   {
     LaunchScope L_(ctx, kStScan, s);
-    k_ticket_linked<<<1, 1, 0, s>>>(ctx->ctl, atomic_alloc ? 1 : 0);
+    k_ticket_linked<<<1, 1, 0, s>>>(ctx->ctl, atomic_alloc ? 1 : 0, tk_dev);
   }
   if ((rc = check_cuda(ctx, cudaGetLastError()))) return rc;
-  return check_cuda(ctx, cudaMemcpyAsync(ticket, &ctx->ctl->spare[4], sizeof(fhv_ticket_t), cudaMemcpyDefault, s));
+  return deliver_ticket(ctx, ticket, tk_dev != nullptr, s);
 }
 
 extern "C" int fhv_ticket_accumulate(fhv_ctx* ctx, int64_t expect_total, int64_t* acc, void* stream) {
