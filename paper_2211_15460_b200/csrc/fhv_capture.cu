@@ -3058,8 +3058,14 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
     return rc;
   }
   const bool deferred = ctx->item_scan_n >= 0;
-  if ((rc = fhv_pofa_shard_directory_nocheck(ctx, levels, counts, offsets, pyramid, s))) return rc;
-  if ((!ranks || deferred) &&
+  // the fused directory launch stores the fragment total itself; otherwise a copy
+  ctx->dir_frags_total = deferred;
+  ctx->dir_frags_stored = false;
+  rc = fhv_pofa_shard_directory_nocheck(ctx, levels, counts, offsets, pyramid, s);
+  const bool stored = ctx->dir_frags_stored;
+  ctx->dir_frags_total = ctx->dir_frags_stored = false;
+  if (rc) return rc;
+  if ((!ranks || (deferred && !stored)) &&
       (rc = check_cuda(ctx, cudaMemcpyAsync(&ctx->ctl->frags_total, &ctx->ctl->scan_total, sizeof(unsigned long long),
                                             cudaMemcpyDeviceToDevice, s))))
     return rc;

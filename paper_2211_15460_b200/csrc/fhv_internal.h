@@ -95,6 +95,8 @@ struct fhv_ctx {
   // device-side count (speculative plan) or null
   int64_t item_scan_n = -1;
   const unsigned long long* item_scan_dev = nullptr;
+  bool dir_frags_total = false;  // the directory launch also sets ctl->frags_total (asynchronous build)
+  bool dir_frags_stored = false;  // ... and it did (the fused tile-total launch ran)
   // side stream of the asynchronous build: the leaf-counter and cursor
   // clears run there, off the critical path, joined before their first use
   cudaStream_t aux = nullptr;

@@ -496,6 +496,7 @@ struct ItemScan {
   const unsigned long long* n_dev;
   uint64_t* status;
   unsigned tiles;  // 0: none
+  int frags_total;  // the last directory tile also stores the total in ctl->frags_total
 };
 constexpr int kItemScanItems = 32;  // 256 x 32 = 8192 items per tile
 
@@ -594,7 +595,10 @@ __global__ void __launch_bounds__(kDbThreads, FHV_DIR_MINB) k_dir_tma(const __gr
   if (tid < 32) {
     if (lane == 0) {
       prefix_s = pf;
-      if (tile == n_tiles - 1) ctl->scan_total = pf + t_all;
+      if (tile == n_tiles - 1) {
+        ctl->scan_total = pf + t_all;
+        if (is.frags_total) ctl->frags_total = pf + t_all;  // (the asynchronous build's pass-2 count)
+      }
     }
     if (lane < 2 * kDbChunks) {  // level L-4: two subtree roots per chunk
       unsigned m4 = 0;
@@ -811,7 +815,7 @@ static int launch_dir_bulk(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offse
     return launch_dir_tiles(ctx, true, counts, offsets, nullptr, pyramid, levels, s, lo, hi, base);
   // a pending item-rank scan rides along (tile totals given: the directory
   // tiles take no tickets)
-  ItemScan is{nullptr, nullptr, 0, nullptr, nullptr, 0u};
+  ItemScan is{nullptr, nullptr, 0, nullptr, nullptr, 0u, ranks_done && tile_sums && ctx->dir_frags_total ? 1 : 0};
   const int64_t pend = ctx->item_scan_n;
   if (ranks_done && tile_sums && pend > 0) {
     is.cnt = (const uint32_t*)ctx->bufs[kItemCnt].ptr;
@@ -838,6 +842,7 @@ static int launch_dir_bulk(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offse
                                                             base, tile_sums, is);
   }
   if (ranks_done && is.tiles) *ranks_done = true;
+  ctx->dir_frags_stored = is.frags_total != 0;
   return check_cuda(ctx, cudaGetLastError());
 }
 
