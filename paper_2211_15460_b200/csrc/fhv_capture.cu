@@ -2793,7 +2793,7 @@ static int pofa_scatter_async(fhv_ctx* ctx, const CaptureParams& p, int32_t leve
   if (ctx->cursors_zeroed != cursors && (rc = check_cuda(ctx, cudaMemsetAsync(cursors, 0, (size_t)n_local * 4, s))))
     return rc;
   ctx->cursors_zeroed = nullptr;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->alloc, 0, 8, s)))) return rc;
+  if (!ctx->ctl_fresh && (rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->alloc, 0, 8, s)))) return rc;
   if (clear_status && (rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->status, 0, sizeof(int), s)))) return rc;
   EmitOut o = empty_out();
   set_pool(o, pool);
@@ -2823,8 +2823,8 @@ static int pofa_scatter_async(fhv_ctx* ctx, const CaptureParams& p, int32_t leve
     auto* recs = (uint32_t*)scratch(ctx, kLeafRecs, (size_t)cap * 36);
     auto* nn = (unsigned long long*)scratch(ctx, kTmp1, 8);
     if (!big || !keys || !recs || !nn) return FHV_NOMEM;
-    if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->leaf_n[0], 0, 8, s)))) return rc;
-    if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->leaf_n[2], 0, 8, s)))) return rc;
+    if (!ctx->ctl_fresh && (rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->leaf_n[0], 0, 8, s)))) return rc;
+    if (!ctx->ctl_fresh && (rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->leaf_n[2], 0, 8, s)))) return rc;
     if (!n_frags_dev) {
       const unsigned long long nh = (unsigned long long)n_frags_host;
       if ((rc = check_cuda(ctx, cudaMemcpyAsync(nn, &nh, 8, cudaMemcpyHostToDevice, s)))) return rc;
@@ -3031,6 +3031,10 @@ static int fork_clears(fhv_ctx* ctx, uint32_t* counts, unsigned long long n_leav
   return FHV_OK;
 }
 
+// the asynchronous build after pass 1: directory, pass 2, ticket
+static int pofa_build_async_rest(fhv_ctx* ctx, CaptureParams& p, int32_t levels, unsigned long long n_leaves,
+                                 uint32_t* counts, uint32_t* offsets, uint8_t* pyramid, fhv_pool_t* pool,
+                                 int32_t flags, bool ranks, fhv_ticket_t* ticket, cudaStream_t s);
 }  // namespace fhv
 
 extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const fhv_capture_cfg_t* cfg,
@@ -3057,6 +3061,18 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
     ctx->fork_cursors_at_count = nullptr;
     return rc;
   }
+  // (pass 1 reset the control block and touched none of alloc / leaf_n / dir_done)
+  ctx->ctl_fresh = true;
+  rc = pofa_build_async_rest(ctx, p, levels, n_leaves, counts, offsets, pyramid, pool, flags, ranks, ticket, s);
+  ctx->ctl_fresh = false;
+  return rc;
+}
+
+namespace fhv {
+static int pofa_build_async_rest(fhv_ctx* ctx, CaptureParams& p, int32_t levels, unsigned long long n_leaves,
+                                 uint32_t* counts, uint32_t* offsets, uint8_t* pyramid, fhv_pool_t* pool,
+                                 int32_t flags, bool ranks, fhv_ticket_t* ticket, cudaStream_t s) {
+  int rc;
   const bool deferred = ctx->item_scan_n >= 0;
   // the fused directory launch stores the fragment total itself; otherwise a copy
   ctx->dir_frags_total = deferred;
@@ -3083,6 +3099,7 @@ extern "C" int fhv_pofa_build_async(fhv_ctx* ctx, const fhv_tris_t* tris, const 
   ctx->pass1_levels = -1;
   return deliver_ticket(ctx, ticket, tk_dev != nullptr, s);
 }
+}  // namespace fhv
 
 // One rank's share of pofa_build with no host wait and no collective: the
 // caller speculates every rank's fragment total from the previous build of

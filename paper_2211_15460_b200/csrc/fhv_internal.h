@@ -97,6 +97,9 @@ struct fhv_ctx {
   const unsigned long long* item_scan_dev = nullptr;
   bool dir_frags_total = false;  // the directory launch also sets ctl->frags_total (asynchronous build)
   bool dir_frags_stored = false;  // ... and it did (the fused tile-total launch ran)
+  // inside an asynchronous POFA build after its control-block reset: the
+  // counters that reset zeroed (alloc, leaf_n, dir_done) need no clears of their own
+  bool ctl_fresh = false;
   // side stream of the asynchronous build: the leaf-counter and cursor
   // clears run there, off the critical path, joined before their first use
   cudaStream_t aux = nullptr;

@@ -827,9 +827,14 @@ static int launch_dir_bulk(fhv_ctx* ctx, const uint32_t* counts, uint32_t* offse
   uint64_t* st = (uint64_t*)scratch(ctx, kScanStatus, (size_t)(tiles + is.tiles) * sizeof(uint64_t));
   if (!st) return FHV_NOMEM;
   is.status = st + tiles;
-  int rc = check_cuda(ctx, cudaMemsetAsync(st, 0, (size_t)(tiles + is.tiles) * sizeof(uint64_t), s));
-  if (rc) return rc;
-  if ((rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->dir_ticket, 0, 8, s)))) return rc;  // (done counter)
+  // (directory tiles with tile totals use no status words; a control block
+  // fresh from this build's reset already holds a zero done counter)
+  int rc = FHV_OK;
+  const size_t st_words = tile_sums ? is.tiles : tiles + is.tiles;
+  if (st_words && (rc = check_cuda(ctx, cudaMemsetAsync(tile_sums ? is.status : st, 0, st_words * sizeof(uint64_t), s))))
+    return rc;
+  if (!ctx->ctl_fresh && (rc = check_cuda(ctx, cudaMemsetAsync(&ctx->ctl->dir_ticket, 0, 8, s))))  // (done counter)
+    return rc;
   constexpr int kSmem = kDbChunks * kDbBytes + 1024;
   static bool attr = false;
   if (!attr) {
