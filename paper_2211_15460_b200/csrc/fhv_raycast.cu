@@ -548,7 +548,8 @@ __global__ void __launch_bounds__(128, FHV_RAY_MINB) k_raycast(RayParams x) {
 #define FHV_PKT_MINB 4  // CTAs per SM the opaque-nearest packet kernel is register-budgeted for (128)
 #endif
 #ifndef FHV_PKT_MINB_T
-#define FHV_PKT_MINB_T 3  // the compositing modes: 170 registers, fewer spills (C2 1.77 -> 1.74 ms; 2: 1.94)
+#define FHV_PKT_MINB_T 4  // the compositing modes (3: 166 registers without spills -- C2 1.76 -> 1.73 ms but the
+                          // 80-layer C4 view 32.5 -> 36.4 ms; 2: C2 1.94 ms)
 #endif
 constexpr int kPktHits = FHV_PKT_HITS;
 #ifndef FHV_PKT_BUF
