@@ -315,7 +315,7 @@ def extra_config(args):
             vol = fhv.build_pofl(scene, ns, cfg, 8, device=dev, sync=False, ticket=tk2)
             _lib.check(_lib.load().fhv_ticket_accumulate(_lib.ctx(dev), int(n0), _lib.ptr(acc2),
                                                          _lib.stream_ptr(dev)), "ticket")
-            buf.pixels.zero_()
+            # (every pixel is written by the cast: the buffer is reused as is)
             img, st = fhv.render_raycast(vol, view, lights, rcfg, out=buf, sync=False, shading=sh)
             return vol, st
         for _ in range(args.warmup):
@@ -464,7 +464,6 @@ def extra_config(args):
             buf4 = img_buf(1920, 1080)
 
             def step_ray4():
-                buf4.pixels.zero_()
                 return fhv.render_raycast(vol4, view4, [headlight(view4)], rc4, out=buf4, sync=False, shading=sh4)[1]
             step_ray4()
             ms_r, st4 = _timed(step_ray4, max(1, min(args.steps, 5)), stream)
@@ -507,7 +506,6 @@ def extra_config(args):
             def step():
                 sts = []
                 for v, sh in zip(views, shs):
-                    buf.pixels.zero_()
                     _, st = fhv.render_raycast(vol, v, [headlight(v)], rcfg, out=buf, sync=False, shading=sh)
                     sts.append(st.counters)
                 return sts

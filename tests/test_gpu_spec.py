@@ -385,3 +385,24 @@ def test_async_build_paths_bit_exact(env):
                          capture_output=True, text=True, cwd=root, timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip().splitlines()[-1] == "OK", out.stdout[-2000:]
+
+
+def test_raycast_writes_every_pixel_of_a_reused_buffer():
+    """A full-frame ray cast into a reused image buffer overwrites every pixel
+    (the bench's steps reuse one buffer without clearing it): a NaN-filled
+    buffer ends up equal to a fresh render."""
+    s = fhv.sample_scenes.cube972()
+    ns = CaptureStrategy.normal_space()
+    cfg = _cfg(s, 128)
+    vol = fhv.pofa_build(s, ns, cfg, 5, exact_order=True)
+    cam = fhv.viewpoint_camera("+x", (96, 64), "perspective")
+    lights = lights_for("head", cam)
+    import dataclasses
+    for mode in ("transparency", "opaque_nearest"):
+        rc = dataclasses.replace(fhv.default_raycast_config(vol), mode=mode)
+        ref, _ = fhv.render_raycast(vol, cam, lights, rc)
+        buf = fhv.ImageBuffer(96, 64, torch.full((64, 96, 4), float("nan"), dtype=torch.float64, device="cuda"),
+                              torch.full((64, 96), float("nan"), dtype=torch.float64, device="cuda"))
+        got, _ = fhv.render_raycast(vol, cam, lights, rc, out=buf)
+        assert not bool(torch.isnan(got.pixels).any()), mode
+        assert torch.equal(got.pixels, ref.pixels), mode
